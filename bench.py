@@ -1,0 +1,399 @@
+"""Benchmark: fused-graph effective HBM GB/s (% of peak) and kernel launches per graph.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+One step = one execution of the whole compiled graph (every fusion group of
+the reference plan = one stitched sm_100a launch) over one graph instance
+with inputs resident in HBM.  Default workload: C5, the BERT-base
+encoder-layer non-MatMul graph at batch 64, seq 512 (5 groups, 5.03 GB of
+compulsory traffic), the BASELINE.json config that is batch-sharded across
+GPUs.  Under torchrun each rank runs its own instance on its own GPU (weak
+scaling, replicas of independent graph instances; no collective on this
+path).  `value` = compulsory bytes of all ranks / max-over-ranks device time.
+
+`--impl reference` times the reference's own CPU executor (run_compiled,
+built from the reference sources into oracle/_ref by oracle/Makefile; else
+the C oracle port) on a bounded sample of the same workload on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Fused-graph effective HBM GB/s (% of peak) and kernel launches per graph"
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+WORKLOAD_NAMES = {
+    "C1": "LayerNorm fp32 [8192,1024]",
+    "C2": "Softmax fp32 [16,16,512,512]",
+    "C3": "bias-add grad fp32 [65536,1024] (column reduce)",
+    "C3b": "bias-add grad + dx output fp32 [65536,1024]",
+    "C4": "transpose+bias+scale fp32 B32 S512 H16 D64",
+    "C4b": "transpose+scale+bias fp32 B32 S512 H16 D64 (full bias)",
+    "C5": "BERT-base encoder-layer non-MatMul graph, batch 64 seq 512",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    rows.append(f)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def plan_path(config):
+    return os.path.join(ROOT, "workloads", "plans", f"{config}.full.json")
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def reference_sample(config):
+    """A bounded sample of the same workload for the reference's CPU executor:
+    the same rows (same lengths and op mix), fewer of them."""
+    from workloads import configs
+    if config == "C5":
+        # query block of 64 tokens: attention rows of 512, LN rows of 768, GELU rows of 3072,
+        # in the same byte proportions as b64 s512 (1/512 of it)
+        return configs.c5_bert(B=1, S=512, Sq=64), "C5 query block: batch 1, 64 query rows x 512 keys (1/512 of b64 s512)"
+    sizes = {"C1": dict(R=64, C=1024), "C2": dict(B=1, H=1, S=128, L=512), "C3": dict(N=512, C=1024),
+             "C3b": dict(N=512, C=1024), "C4": dict(B=1, S=128, H=16, D=64), "C4b": dict(B=1, S=128, H=16, D=64)}
+    return configs.build(config, **sizes[config]), f"{config} at {sizes[config]}"
+
+
+def graph_bytes(doc):
+    """Compulsory bytes: non-splat external inputs of each group once + roots once."""
+    from paper_1811_05213_b200 import host as H
+    g = H.parse_graph(doc)
+    # parameters + outputs is exact for graphs whose groups are independent (all configs)
+    b = sum(p.numel() * 4 for p in g.parameters())
+    b += sum(g.at(o).numel() * 4 for o in g.outputs)
+    return b
+
+
+def time_reference_cpu(config, threads, iters=1):
+    doc, sample = reference_sample(config)
+    nbytes = graph_bytes(doc)
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        json.dump(doc, f)
+        path = f.name
+    try:
+        if os.path.exists(REF_TOOL):
+            r = subprocess.run([REF_TOOL, "bench", path, "42", str(threads), str(iters)], capture_output=True,
+                               text=True, check=True)
+            info = json.loads(r.stdout)
+            secs = info["seconds"]
+            kind = "reference"
+            execu = "reference run_compiled (oracle/_ref, built from the reference sources)"
+        else:  # the C oracle port (dense interpreter restatement), single thread
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import sfx_testlib as T
+            from paper_1811_05213_b200 import host as H
+            g = H.parse_graph(doc)
+            inputs = T.gen_inputs_fast(g, 42, -1.0, 1.0)
+            t0 = time.perf_counter()
+            for _ in range(iters):
+                T.interpret(g, inputs, 0)
+            secs = time.perf_counter() - t0
+            threads = 1
+            kind = "port"
+            execu = "C oracle port of the reference interpreter"
+    finally:
+        os.unlink(path)
+    gbs = threads * iters * nbytes / secs / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"{sample}; {execu}; {threads} independent instances x {iters} iteration(s); "
+                      f"{nbytes} compulsory bytes per instance; {secs:.2f} s wall"}, secs
+
+
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup if os.path.exists(REF_TOOL) else 0):
+        pass  # the reference's executor has no warm-up state; warm-up steps are not repeated on CPU
+    times = []
+    cb = None
+    for _ in range(args.steps):
+        cb, secs = time_reference_cpu(args.config, threads)
+        times.append(secs)
+    ms = 1000.0 * sum(times) / len(times)
+    value = sum(cb_["value"] for cb_ in [cb]) if cb else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_obj(args.config, args.gpus),
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_obj(config, n):
+    return {"workload": f"{config}: {WORKLOAD_NAMES[config]}", "plan": f"workloads/plans/{config}.full.json "
+            "(reference compile_graph, default PipelineOptions)", "instances_per_gpu": 1,
+            "parallelism": f"batch-sharded independent graph instances x{n} (no collective)" if config not in
+            ("C3", "C3b") or n == 1 else f"batch-sharded x{n} + NCCL all-reduce of the column sums"}
+
+
+# --------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1811_05213_b200 import host as H
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = H.Context(local)
+    g, rep, bundle = H.load_bundle(plan_path(args.config))
+    cg = H.CompiledGraph(ctx, g, rep)
+    kinfo = [k.info for k in cg.kernels]
+    n_kernels = len(cg.kernels)
+
+    # inputs resident in HBM; enough rotating sets that the sets exceed L2 (126 MB)
+    per_set = sum(g.at(p).numel() * 4 for p in cg.param_ids) + sum(g.at(o).numel() * 4 for o in g.outputs)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    nsets = max(1, min(8, math.ceil(3 * l2 / per_set)))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    sets = []
+    for _ in range(nsets):
+        ins = [torch.rand(g.at(p).shape, generator=gen, device=dev, dtype=torch.float32) * 2 - 1
+               for p in cg.param_ids]
+        outs = [torch.empty(g.at(o).shape, device=dev, dtype=torch.float32) for o in g.outputs]
+        sets.append(([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], ins, outs))
+    stream = torch.cuda.Stream(device=dev)
+    algo_bytes = sum(k["algorithmic_bytes"] for k in kinfo)
+
+    def step(i):
+        pi, po, _, _ = sets[i % nsets]
+        cg.run(pi, po, stream=stream.cuda_stream, cuda_graph=True)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count()
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = ctx.launch_count() - launches0
+    if ws > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    clocks = clk.summary()
+
+    # per-kernel live timing on the launching stream (roofline of each group)
+    per_kernel = []
+    reps = max(3, min(20, args.steps))
+    for ki, k in enumerate(cg.kernels):
+        slots = {pid: i for i, pid in enumerate(cg.param_ids)}
+        outs_slot = {o: i for i, o in enumerate(g.outputs)}
+
+        def ptrs(sidx):
+            pi, po, _, _ = sets[sidx % nsets]
+            return [pi[slots[x]] for x in k.input_ids], [po[outs_slot[r]] for r in k.program.roots]
+
+        for i in range(2):
+            a, b = ptrs(i)
+            k.launch(a, b, stream.cuda_stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for i in range(reps):
+            a, b = ptrs(i)
+            ev[i][0].record(stream)
+            k.launch(a, b, stream.cuda_stream)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        avg = sum(s.elapsed_time(e) for s, e in ev) / reps
+        per_kernel.append({"group": k.program.fusion_root, "kernel": k.info["entry"],
+                           "strategy": k.info["strategy"], "ms": avg,
+                           "bytes": k.info["algorithmic_bytes"],
+                           "gbs": k.info["algorithmic_bytes"] / (avg * 1e-3) / 1e9,
+                           "grid": k.info["grid"], "block": k.info["block"], "regs": k.info["registers"]})
+
+    # end-to-end through the reference-facing host-buffer call (TensorValue in/out)
+    pin_in = [torch.empty(g.at(p).shape, dtype=torch.float32).pin_memory() for p in cg.param_ids]
+    for t, d in zip(pin_in, sets[0][2]):
+        t.copy_(d.cpu())
+    pin_out = {o: torch.empty(g.at(o).shape, dtype=torch.float32).pin_memory() for o in g.outputs}
+    import ctypes as C
+    pin_arr = (C.c_void_p * len(pin_in))(*[t.data_ptr() for t in pin_in])
+    out_arr = (C.c_void_p * len(g.outputs))(*[pin_out[o].data_ptr() for o in g.outputs])
+    h2d = sum(t.numel() * 4 for t in pin_in)
+    d2h = sum(t.numel() * 4 for t in pin_out.values())
+
+    def e2e_step():
+        H._check(H.lib().sfx_graph_run_host(cg.h, pin_arr, len(pin_in), out_arr, len(g.outputs),
+                                             C.c_void_p(stream.cuda_stream)))
+
+    e2e_step()
+    if ws > 1:
+        dist.barrier()
+    e2e_steps = max(2, min(5, args.steps))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_t = torch.tensor([e2e_s], device=dev)
+    if ws > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = peaks()
+    total_bytes = algo_bytes * ws
+    value = total_bytes / (ms_max * 1e-3) / 1e9
+    dom = max(per_kernel, key=lambda r: r["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom["kernel"])
+    except Exception:
+        pass
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu, _ = time_reference_cpu(args.config, os.cpu_count() or 1)
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand U(-1,1) inputs resident in HBM)",
+        "config": dict(config_obj(args.config, ws), **{
+            "l2_policy": f"{nsets} rotating input/output set(s) of {per_set / 1e6:.1f} MB (> L2 {l2 / 1e6:.0f} MB)",
+            "groups": n_kernels, "launches_per_graph": n_kernels}),
+        "pct_of_peak": 100.0 * value / ws / peak,
+        "peak_gbs": peak, "peak_kind": peak_kind,
+        "kernel_launches_per_graph": n_kernels,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": dom["gbs"] / peak, "traffic": traffic, "kernel": dom["kernel"],
+                     "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"],
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+        "per_kernel": per_kernel,
+        "e2e": {"value": total_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                "path": "sfx_graph_run_host (pinned host buffers, H2D + 1 launch per group + D2H)"},
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOAD_NAMES))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,647 @@
+// C ABI (include/sfx.h): context + device buffer manager, per-group kernels
+// (run_program twin), whole-module executor (run_compiled twin) with CUDA-graph
+// replay, and the NCCL all-reduce for batch-crossing column reductions.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "dyn.hpp"
+#include "ir.hpp"
+#include "jit.hpp"
+#include "lower.hpp"
+#include "sfx.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+sfx_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return SFX_OK;
+  } catch (const sfx::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = std::string("internal: ") + e.what();
+    return SFX_ERR_INVALID;
+  }
+}
+
+}  // namespace
+
+// ---- NCCL (dlopen'ed: the library is used only for the cross-GPU combine) ----
+namespace {
+typedef struct { char internal[SFX_NCCL_ID_BYTES]; } nccl_id_t;
+typedef void* nccl_comm_t;
+struct Nccl {
+  int (*GetUniqueId)(nccl_id_t*) = nullptr;
+  int (*CommInitRank)(nccl_comm_t*, int, nccl_id_t, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm_t, CUstream) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+const Nccl& nccl() {
+  static Nccl n;
+  static std::string err;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = "libnccl.so.2 not available";
+      return;
+    }
+    n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!n.GetUniqueId || !n.CommInitRank || !n.AllReduce) err = "libnccl missing symbols";
+  });
+  if (!err.empty()) throw sfx::Error(SFX_ERR_NCCL, err);
+  return n;
+}
+void check_nccl(int r, const char* what) {
+  if (r == 0) return;
+  const Nccl& n = nccl();
+  throw sfx::Error(SFX_ERR_NCCL, std::string(what) + ": " + (n.GetErrorString ? n.GetErrorString(r) : "error"));
+}
+}  // namespace
+
+struct sfx_ctx {
+  int device = 0;
+  CUdevice dev = 0;
+  CUcontext cu = nullptr;
+  std::atomic<int64_t> launches{0};
+  std::mutex mu;
+  std::multimap<uint64_t, CUdeviceptr> pool;  // freed blocks by size (buffer manager)
+  std::map<CUdeviceptr, uint64_t> live;
+  nccl_comm_t comm = nullptr;
+
+  void bind() const { sfx::check_cu(sfx::driver().cuCtxSetCurrent(cu), "cuCtxSetCurrent"); }
+
+  CUdeviceptr alloc(uint64_t bytes) {
+    bytes = std::max<uint64_t>(256, (bytes + 255) / 256 * 256);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = pool.find(bytes);
+    CUdeviceptr p = 0;
+    if (it != pool.end()) {
+      p = it->second;
+      pool.erase(it);
+    } else {
+      bind();
+      sfx::check_cu(sfx::driver().cuMemAlloc(&p, bytes), "cuMemAlloc");
+    }
+    live[p] = bytes;
+    return p;
+  }
+  void release(CUdeviceptr p) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = live.find(p);
+    if (it == live.end()) throw sfx::Error(SFX_ERR_INVALID, "sfx_free of a pointer not from sfx_alloc");
+    pool.emplace(it->second, p);
+    live.erase(it);
+  }
+};
+
+struct sfx_kernel {
+  sfx_ctx* ctx = nullptr;
+  sfx::KernelSource src;
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  CUdeviceptr ws = 0;
+  int regs = 0;
+  std::string cubin_path;
+};
+
+struct sfx_graph {
+  sfx_ctx* ctx = nullptr;
+  sfx::Graph graph;
+  std::vector<sfx_kernel*> kernels;  // per program
+  std::vector<int> order;            // program launch order (condensation Kahn order)
+  std::vector<int> params;           // Parameter nodes, ascending id = param slot order
+  std::map<int, CUdeviceptr> owned;  // intermediates + dense constants (device-resident)
+  std::map<std::vector<uint64_t>, std::pair<CUgraph, CUgraphExec>> captured;
+  std::vector<CUdeviceptr> host_bufs;  // staging for sfx_graph_run_host (params then outputs)
+};
+
+namespace {
+
+sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_compile_opts* opts) {
+  sfx_compile_opts o{};
+  if (opts) o = *opts;
+  auto k = std::make_unique<sfx_kernel>();
+  k->ctx = ctx;
+  k->src = sfx::lower_program(g, pi, o);
+  sfx::Cubin cb = sfx::compile_cubin(k->src.code, k->src.entry);
+  k->cubin_path = cb.path;
+  ctx->bind();
+  const sfx::Driver& d = sfx::driver();
+  sfx::check_cu(d.cuModuleLoadData(&k->mod, cb.image.data()), "cuModuleLoadData");
+  sfx::check_cu(d.cuModuleGetFunction(&k->fn, k->mod, k->src.entry.c_str()), "cuModuleGetFunction");
+  d.cuFuncGetAttribute(&k->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k->fn);
+  if (k->src.smem > 48 * 1024)
+    sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->src.smem),
+                  "cuFuncSetAttribute(smem)");
+  if (k->src.workspace_bytes > 0) {
+    k->ws = ctx->alloc(static_cast<uint64_t>(k->src.workspace_bytes));
+    sfx::check_cu(d.cuMemsetD32Async(k->ws, 0, (k->src.workspace_bytes + 3) / 4, nullptr), "cuMemsetD32Async");
+    sfx::check_cu(d.cuStreamSynchronize(nullptr), "cuStreamSynchronize");
+  }
+  return k.release();
+}
+
+void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s) {
+  if (in.size() != k->src.inputs.size())
+    throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(k->src.inputs.size()) + " inputs");
+  if (out.size() != k->src.outputs.size())
+    throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(k->src.outputs.size()) + " outputs");
+  std::vector<CUdeviceptr> vals;
+  vals.reserve(in.size() + out.size() + 1);
+  for (CUdeviceptr p : in) {
+    if (!p) throw sfx::Error(SFX_ERR_EXEC, "null input pointer");
+    vals.push_back(p);
+  }
+  for (CUdeviceptr p : out) {
+    if (!p) throw sfx::Error(SFX_ERR_EXEC, "null output pointer");
+    vals.push_back(p);
+  }
+  vals.push_back(k->ws);
+  std::vector<void*> args(vals.size());
+  for (size_t i = 0; i < vals.size(); ++i) args[i] = &vals[i];
+  sfx::check_cu(sfx::driver().cuLaunchKernel(k->fn, static_cast<unsigned>(k->src.grid_x),
+                                             static_cast<unsigned>(k->src.grid_y), 1,
+                                             static_cast<unsigned>(k->src.block), 1, 1,
+                                             static_cast<unsigned>(k->src.smem), s, args.data(), nullptr),
+                "cuLaunchKernel");
+  k->ctx->launches.fetch_add(1);
+}
+
+void destroy_kernel(sfx_kernel* k) {
+  if (!k) return;
+  try {
+    k->ctx->bind();
+    if (k->mod) sfx::driver().cuModuleUnload(k->mod);
+    if (k->ws) k->ctx->release(k->ws);
+  } catch (...) {
+  }
+  delete k;
+}
+
+// run_compiled's condensation order (reference pipeline.cpp:67-131): one node
+// per program plus one per remaining instruction, Kahn with sorted ready set.
+std::vector<int> condensation_order(const sfx::Graph& g) {
+  const int P = static_cast<int>(g.programs.size());
+  std::vector<int> node_of(g.nodes.size(), -1);
+  for (int p = 0; p < P; ++p)
+    for (int m : g.programs[p].members) node_of[m] = p;
+  int n = P;
+  std::vector<int> singles;
+  for (size_t i = 0; i < g.nodes.size(); ++i)
+    if (node_of[i] < 0) {
+      node_of[i] = n++;
+      singles.push_back(static_cast<int>(i));
+    }
+  std::vector<std::set<int>> succ(n);
+  std::vector<int> indeg(n, 0);
+  for (size_t i = 0; i < g.nodes.size(); ++i)
+    for (int op : g.nodes[i].operands) {
+      int a = node_of[op], b = node_of[i];
+      if (a != b && succ[a].insert(b).second) ++indeg[b];
+    }
+  std::vector<int> ready;
+  for (int i = 0; i < n; ++i)
+    if (!indeg[i]) ready.push_back(i);
+  std::vector<int> order;
+  int processed = 0;
+  while (!ready.empty()) {
+    int v = ready.front();
+    ready.erase(ready.begin());
+    ++processed;
+    if (v < P) order.push_back(v);
+    for (int s : succ[v])
+      if (--indeg[s] == 0) ready.insert(std::lower_bound(ready.begin(), ready.end(), s), s);
+  }
+  if (processed != n) throw sfx::Error(SFX_ERR_EXEC, "condensation is cyclic");
+  return order;
+}
+
+std::vector<CUdeviceptr> gather_ptrs(const sfx_graph* G, const std::vector<int>& nodes,
+                                     const std::map<int, CUdeviceptr>& where) {
+  std::vector<CUdeviceptr> v;
+  for (int n : nodes) {
+    auto it = where.find(n);
+    if (it == where.end()) throw sfx::Error(SFX_ERR_EXEC, "missing external value " + G->graph.nodes[n].id);
+    v.push_back(it->second);
+  }
+  return v;
+}
+
+void graph_enqueue(sfx_graph* G, const uint64_t* params, const uint64_t* outputs, CUstream s) {
+  std::map<int, CUdeviceptr> where = G->owned;
+  for (size_t i = 0; i < G->params.size(); ++i) where[G->params[i]] = params[i];
+  for (size_t i = 0; i < G->graph.outputs.size(); ++i) where[G->graph.outputs[i]] = outputs[i];
+  const sfx::Driver& d = sfx::driver();
+  for (size_t i = 0; i < G->graph.outputs.size(); ++i) {
+    int o = G->graph.outputs[i];
+    const sfx::Node& n = G->graph.nodes[o];
+    if (n.op == SFX_OP_PARAMETER || n.op == SFX_OP_CONSTANT) {  // output with no producing group
+      auto src = G->owned.count(o) ? G->owned.at(o) : where.at(o);
+      for (size_t k = 0; k < G->params.size(); ++k)
+        if (G->params[k] == o) src = params[k];
+      if (src != outputs[i])
+        sfx::check_cu(d.cuMemcpyDtoDAsync(outputs[i], src, n.numel() * 4, s), "cuMemcpyDtoDAsync");
+    }
+  }
+  for (int p : G->order) {
+    sfx_kernel* k = G->kernels[p];
+    launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), s);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t sfx_abi_version(void) { return SFX_ABI_VERSION; }
+const char* sfx_last_error(void) { return g_last_error.c_str(); }
+
+sfx_status sfx_ctx_create(int32_t device, sfx_ctx** out) {
+  return guard([&] {
+    if (!out) throw sfx::Error(SFX_ERR_INVALID, "null out");
+    const sfx::Driver& d = sfx::driver();
+    auto c = std::make_unique<sfx_ctx>();
+    c->device = device;
+    sfx::check_cu(d.cuDeviceGet(&c->dev, device), "cuDeviceGet");
+    sfx::check_cu(d.cuDevicePrimaryCtxRetain(&c->cu, c->dev), "cuDevicePrimaryCtxRetain");
+    c->bind();
+    *out = c.release();
+  });
+}
+
+sfx_status sfx_ctx_destroy(sfx_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    try {
+      ctx->bind();
+      for (auto& [sz, p] : ctx->pool) sfx::driver().cuMemFree(p);
+      for (auto& [p, sz] : ctx->live) sfx::driver().cuMemFree(p);
+    } catch (...) {
+    }
+    delete ctx;
+  });
+}
+
+sfx_status sfx_alloc(sfx_ctx* ctx, uint64_t bytes, uint64_t* dptr) {
+  return guard([&] {
+    if (!ctx || !dptr) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    *dptr = ctx->alloc(bytes);
+  });
+}
+
+sfx_status sfx_free(sfx_ctx* ctx, uint64_t dptr) {
+  return guard([&] {
+    if (!ctx) throw sfx::Error(SFX_ERR_INVALID, "null ctx");
+    if (dptr) ctx->release(dptr);
+  });
+}
+
+sfx_status sfx_host_alloc(sfx_ctx* ctx, uint64_t bytes, void** hptr) {
+  return guard([&] {
+    if (!ctx || !hptr) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    ctx->bind();
+    sfx::check_cu(sfx::driver().cuMemHostAlloc(hptr, std::max<uint64_t>(bytes, 4), 0), "cuMemHostAlloc");
+  });
+}
+
+sfx_status sfx_host_free(sfx_ctx* ctx, void* hptr) {
+  return guard([&] {
+    if (!ctx) throw sfx::Error(SFX_ERR_INVALID, "null ctx");
+    ctx->bind();
+    if (hptr) sfx::check_cu(sfx::driver().cuMemFreeHost(hptr), "cuMemFreeHost");
+  });
+}
+
+sfx_status sfx_memcpy_h2d(sfx_ctx* ctx, uint64_t dst, const void* src, uint64_t bytes, void* stream) {
+  return guard([&] {
+    ctx->bind();
+    sfx::check_cu(sfx::driver().cuMemcpyHtoDAsync(dst, src, bytes, static_cast<CUstream>(stream)), "cuMemcpyHtoDAsync");
+  });
+}
+
+sfx_status sfx_memcpy_d2h(sfx_ctx* ctx, void* dst, uint64_t src, uint64_t bytes, void* stream) {
+  return guard([&] {
+    ctx->bind();
+    sfx::check_cu(sfx::driver().cuMemcpyDtoHAsync(dst, src, bytes, static_cast<CUstream>(stream)), "cuMemcpyDtoHAsync");
+  });
+}
+
+sfx_status sfx_memset_d32(sfx_ctx* ctx, uint64_t dst, uint32_t value, uint64_t count, void* stream) {
+  return guard([&] {
+    ctx->bind();
+    sfx::check_cu(sfx::driver().cuMemsetD32Async(dst, value, count, static_cast<CUstream>(stream)), "cuMemsetD32Async");
+  });
+}
+
+sfx_status sfx_stream_sync(sfx_ctx* ctx, void* stream) {
+  return guard([&] {
+    ctx->bind();
+    sfx::check_cu(sfx::driver().cuStreamSynchronize(static_cast<CUstream>(stream)), "cuStreamSynchronize");
+  });
+}
+
+int64_t sfx_launch_count(sfx_ctx* ctx) { return ctx ? ctx->launches.load() : -1; }
+
+sfx_status sfx_program_compile(sfx_ctx* ctx, const sfx_graph_desc* graph, int32_t program_index,
+                               const sfx_compile_opts* opts, sfx_kernel** out) {
+  return guard([&] {
+    if (!ctx || !out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    sfx::Graph g = sfx::graph_from_desc(graph);
+    *out = build_kernel(ctx, g, program_index, opts);
+  });
+}
+
+sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_index, const sfx_compile_opts* opts,
+                               char* source_out, uint64_t source_cap, char* cubin_path_out, uint64_t path_cap,
+                               char* strategy_out, uint64_t strategy_cap) {
+  return guard([&] {
+    sfx::Graph g = sfx::graph_from_desc(graph);
+    sfx_compile_opts o{};
+    if (opts) o = *opts;
+    sfx::KernelSource ks = sfx::lower_program(g, program_index, o);
+    sfx::Cubin cb = sfx::compile_cubin(ks.code, ks.entry);
+    auto put = [](char* dst, uint64_t cap, const std::string& s) {
+      if (!dst || cap == 0) return;
+      size_t n = std::min<size_t>(s.size(), cap - 1);
+      std::memcpy(dst, s.data(), n);
+      dst[n] = 0;
+    };
+    put(source_out, source_cap, ks.code);
+    put(cubin_path_out, path_cap, cb.path);
+    put(strategy_out, strategy_cap, ks.strategy + " " + ks.note);
+  });
+}
+
+sfx_status sfx_kernel_get_info(sfx_kernel* k, sfx_kernel_info* info) {
+  return guard([&] {
+    if (!k || !info) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    info->strategy = k->src.strategy.c_str();
+    info->entry = k->src.entry.c_str();
+    info->n_inputs = static_cast<int32_t>(k->src.inputs.size());
+    info->n_outputs = static_cast<int32_t>(k->src.outputs.size());
+    info->grid = k->src.grid_x * k->src.grid_y;
+    info->block = k->src.block;
+    info->smem_bytes = k->src.smem;
+    info->workspace_bytes = k->src.workspace_bytes;
+    info->algorithmic_bytes = k->src.algorithmic_bytes;
+    info->registers = k->regs;
+    info->vector_width = k->src.vector_width;
+  });
+}
+
+sfx_status sfx_kernel_input_instrs(sfx_kernel* k, int32_t* out, int32_t cap) {
+  return guard([&] {
+    if (!k || (!out && cap > 0)) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    for (size_t i = 0; i < k->src.inputs.size() && static_cast<int32_t>(i) < cap; ++i) out[i] = k->src.inputs[i];
+  });
+}
+
+sfx_status sfx_program_launch(sfx_kernel* k, const uint64_t* inputs, int32_t n_inputs, const uint64_t* outputs,
+                              int32_t n_outputs, void* stream) {
+  return guard([&] {
+    if (!k) throw sfx::Error(SFX_ERR_INVALID, "null kernel");
+    k->ctx->bind();
+    std::vector<CUdeviceptr> in(inputs, inputs + std::max(0, n_inputs));
+    std::vector<CUdeviceptr> out(outputs, outputs + std::max(0, n_outputs));
+    launch(k, in, out, static_cast<CUstream>(stream));
+  });
+}
+
+sfx_status sfx_kernel_destroy(sfx_kernel* k) {
+  return guard([&] { destroy_kernel(k); });
+}
+
+sfx_status sfx_graph_compile(sfx_ctx* ctx, const sfx_graph_desc* desc, const sfx_compile_opts* opts,
+                             sfx_graph** out) {
+  return guard([&] {
+    if (!ctx || !out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    auto G = std::make_unique<sfx_graph>();
+    G->ctx = ctx;
+    G->graph = sfx::graph_from_desc(desc);
+    const sfx::Graph& g = G->graph;
+    std::vector<bool> in_group(g.nodes.size(), false);
+    for (const sfx::Program& p : g.programs)
+      for (int m : p.members) in_group[m] = true;
+    for (size_t i = 0; i < g.nodes.size(); ++i) {
+      const sfx::Node& n = g.nodes[i];
+      if (in_group[i]) continue;
+      if (n.op == SFX_OP_PARAMETER) {
+        G->params.push_back(static_cast<int>(i));
+      } else if (n.op != SFX_OP_CONSTANT) {
+        throw sfx::Error(SFX_ERR_UNSUPPORTED, "instruction " + n.id + " (" +
+                                                  (n.op == SFX_OP_BATCH_MATMUL || n.op == SFX_OP_LIBRARY_CALL
+                                                       ? "matmul barrier"
+                                                       : "standalone op") +
+                                                  ") is outside the device non-MatMul path");
+      }
+    }
+    std::sort(G->params.begin(), G->params.end(), [&](int a, int b) { return g.nodes[a].id < g.nodes[b].id; });
+    G->order = condensation_order(g);
+    try {
+      for (size_t p = 0; p < g.programs.size(); ++p)
+        G->kernels.push_back(build_kernel(ctx, g, static_cast<int>(p), opts));
+      // device-resident intermediates (roots consumed by later groups) and
+      // dense constants; graph outputs and params come from the caller
+      std::set<int> outs(g.outputs.begin(), g.outputs.end());
+      const sfx::Driver& d = sfx::driver();
+      for (const sfx::Program& p : g.programs)
+        for (int r : p.roots)
+          if (!outs.count(r)) G->owned[r] = ctx->alloc(g.nodes[r].numel() * 4);
+      for (size_t i = 0; i < g.nodes.size(); ++i) {
+        const sfx::Node& n = g.nodes[i];
+        if (n.op != SFX_OP_CONSTANT || n.is_splat()) continue;
+        bool used = outs.count(static_cast<int>(i)) > 0;
+        for (const sfx::Program& p : g.programs)
+          if (std::find(p.inputs.begin(), p.inputs.end(), static_cast<int>(i)) != p.inputs.end()) used = true;
+        if (!used) continue;
+        std::vector<uint32_t> host(n.numel());
+        for (int64_t e = 0; e < n.numel(); ++e) {
+          double raw = n.literal[e];
+          if (n.dtype == SFX_F32) {
+            float f = static_cast<float>(raw);
+            std::memcpy(&host[e], &f, 4);
+          } else {
+            int32_t v = static_cast<int32_t>(raw);
+            std::memcpy(&host[e], &v, 4);
+          }
+        }
+        CUdeviceptr dp = ctx->alloc(n.numel() * 4);
+        sfx::check_cu(d.cuMemcpyHtoDAsync(dp, host.data(), n.numel() * 4, nullptr), "cuMemcpyHtoDAsync");
+        sfx::check_cu(d.cuStreamSynchronize(nullptr), "cuStreamSynchronize");
+        G->owned[static_cast<int>(i)] = dp;
+      }
+      for (size_t i = 0; i < g.nodes.size(); ++i) {
+        const sfx::Node& n = g.nodes[i];
+        if (n.is_splat() && outs.count(static_cast<int>(i))) {
+          CUdeviceptr dp = ctx->alloc(n.numel() * 4);
+          float f = static_cast<float>(n.literal[0]);
+          int32_t v = static_cast<int32_t>(n.literal[0]);
+          uint32_t bits;
+          if (n.dtype == SFX_F32) std::memcpy(&bits, &f, 4);
+          else std::memcpy(&bits, &v, 4);
+          sfx::check_cu(d.cuMemsetD32Async(dp, bits, n.numel(), nullptr), "cuMemsetD32Async");
+          G->owned[static_cast<int>(i)] = dp;
+        }
+      }
+    } catch (...) {
+      for (sfx_kernel* k : G->kernels) destroy_kernel(k);
+      for (auto& [n, p] : G->owned) ctx->release(p);
+      throw;
+    }
+    *out = G.release();
+  });
+}
+
+sfx_status sfx_graph_param_instrs(sfx_graph* G, int32_t* out, int32_t cap, int32_t* n) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    if (n) *n = static_cast<int32_t>(G->params.size());
+    for (size_t i = 0; i < G->params.size() && static_cast<int32_t>(i) < cap; ++i) out[i] = G->params[i];
+  });
+}
+
+sfx_status sfx_graph_kernel(sfx_graph* G, int32_t program_index, sfx_kernel** out) {
+  return guard([&] {
+    if (!G || !out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    if (program_index < 0 || program_index >= static_cast<int32_t>(G->kernels.size()))
+      throw sfx::Error(SFX_ERR_INVALID, "program index out of range");
+    *out = G->kernels[program_index];
+  });
+}
+
+sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params, const uint64_t* outputs,
+                         int32_t n_outputs, void* stream, int32_t use_cuda_graph) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    if (n_params != static_cast<int32_t>(G->params.size()))
+      throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(G->params.size()) + " params");
+    if (n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
+      throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(G->graph.outputs.size()) + " outputs");
+    G->ctx->bind();
+    CUstream s = static_cast<CUstream>(stream);
+    const sfx::Driver& d = sfx::driver();
+    if (!use_cuda_graph) {
+      graph_enqueue(G, params, outputs, s);
+      return;
+    }
+    if (!s) throw sfx::Error(SFX_ERR_INVALID, "CUDA-graph replay needs a non-default stream");
+    std::vector<uint64_t> key(params, params + n_params);
+    key.insert(key.end(), outputs, outputs + n_outputs);
+    auto it = G->captured.find(key);
+    if (it == G->captured.end()) {
+      int64_t before = G->ctx->launches.load();
+      sfx::check_cu(d.cuStreamBeginCapture(s, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "cuStreamBeginCapture");
+      CUgraph graph = nullptr;
+      try {
+        graph_enqueue(G, params, outputs, s);
+      } catch (...) {
+        d.cuStreamEndCapture(s, &graph);
+        if (graph) d.cuGraphDestroy(graph);
+        throw;
+      }
+      sfx::check_cu(d.cuStreamEndCapture(s, &graph), "cuStreamEndCapture");
+      G->ctx->launches.store(before);  // captured, not launched
+      CUgraphExec exec = nullptr;
+      sfx::check_cu(d.cuGraphInstantiateWithFlags(&exec, graph, 0), "cuGraphInstantiate");
+      it = G->captured.emplace(key, std::make_pair(graph, exec)).first;
+    }
+    sfx::check_cu(d.cuGraphLaunch(it->second.second, s), "cuGraphLaunch");
+    G->ctx->launches.fetch_add(static_cast<int64_t>(G->order.size()));
+  });
+}
+
+sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n_params, void* const* outputs,
+                              int32_t n_outputs, void* stream) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    if (n_params != static_cast<int32_t>(G->params.size()) ||
+        n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
+      throw sfx::Error(SFX_ERR_INVALID, "param/output count mismatch");
+    G->ctx->bind();
+    const sfx::Driver& d = sfx::driver();
+    CUstream s = static_cast<CUstream>(stream);
+    if (G->host_bufs.empty()) {
+      for (int p : G->params) G->host_bufs.push_back(G->ctx->alloc(G->graph.nodes[p].numel() * 4));
+      for (int o : G->graph.outputs) G->host_bufs.push_back(G->ctx->alloc(G->graph.nodes[o].numel() * 4));
+    }
+    std::vector<uint64_t> dp(G->host_bufs.begin(), G->host_bufs.begin() + n_params);
+    std::vector<uint64_t> dout(G->host_bufs.begin() + n_params, G->host_bufs.end());
+    for (int i = 0; i < n_params; ++i)
+      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[i], params[i], G->graph.nodes[G->params[i]].numel() * 4, s),
+                    "cuMemcpyHtoDAsync");
+    graph_enqueue(G, dp.data(), dout.data(), s);
+    for (int i = 0; i < n_outputs; ++i)
+      sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], dout[i], G->graph.nodes[G->graph.outputs[i]].numel() * 4, s),
+                    "cuMemcpyDtoHAsync");
+    sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
+  });
+}
+
+sfx_status sfx_graph_destroy(sfx_graph* G) {
+  return guard([&] {
+    if (!G) return;
+    try {
+      G->ctx->bind();
+      const sfx::Driver& d = sfx::driver();
+      for (auto& [key, ge] : G->captured) {
+        d.cuGraphExecDestroy(ge.second);
+        d.cuGraphDestroy(ge.first);
+      }
+    } catch (...) {
+    }
+    for (sfx_kernel* k : G->kernels) destroy_kernel(k);
+    for (auto& [n, p] : G->owned) G->ctx->release(p);
+    for (CUdeviceptr p : G->host_bufs) G->ctx->release(p);
+    delete G;
+  });
+}
+
+sfx_status sfx_nccl_unique_id(void* id_out) {
+  return guard([&] {
+    nccl_id_t id;
+    check_nccl(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof id);
+  });
+}
+
+sfx_status sfx_nccl_init(sfx_ctx* ctx, const void* id, int32_t nranks, int32_t rank) {
+  return guard([&] {
+    if (!ctx || !id) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    ctx->bind();
+    nccl_id_t nid;
+    std::memcpy(&nid, id, sizeof nid);
+    check_nccl(nccl().CommInitRank(&ctx->comm, nranks, nid, rank), "ncclCommInitRank");
+  });
+}
+
+sfx_status sfx_allreduce_sum_f32(sfx_ctx* ctx, uint64_t buf, uint64_t count, void* stream) {
+  return guard([&] {
+    if (!ctx || !ctx->comm) throw sfx::Error(SFX_ERR_NCCL, "NCCL communicator not initialised");
+    ctx->bind();
+    // ncclFloat32 = 7, ncclSum = 0
+    check_nccl(nccl().AllReduce(reinterpret_cast<const void*>(buf), reinterpret_cast<void*>(buf), count, 7, 0,
+                                ctx->comm, static_cast<CUstream>(stream)),
+               "ncclAllReduce");
+  });
+}
+
+}  // extern "C"

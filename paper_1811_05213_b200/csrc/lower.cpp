@@ -1,0 +1,987 @@
+#include "lower.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "emit.hpp"
+
+namespace sfx {
+
+namespace {
+
+constexpr int kNumSMs = 148;
+
+enum { CLS_NONE = 0, CLS_FULL = 1, CLS_ROWV = 2, CLS_COLV = 3 };
+
+struct Ctx {
+  const Graph& g;
+  const Program& p;
+  std::vector<int> topo;
+  std::vector<int> reduces;
+  std::map<int, bool> dep;
+  bool wide = false;
+  std::string name;
+  Ctx(const Graph& g_, const Program& p_) : g(g_), p(p_) {}
+};
+
+int64_t prod(const std::vector<int64_t>& d, size_t b, size_t e) {
+  int64_t n = 1;
+  for (size_t i = b; i < e; ++i) n *= d[i];
+  return n;
+}
+
+std::string sanitize(const std::string& s) {
+  std::string o;
+  for (char c : s) o += (std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
+  if (o.size() > 40) o.resize(40);
+  return o;
+}
+
+Ctx make_ctx(const Graph& g, const Program& p) {
+  Ctx c(g, p);
+  std::set<int> seen;
+  std::function<void(int)> visit = [&](int n) {
+    if (!p.is_member(n) || seen.count(n)) return;
+    seen.insert(n);
+    for (int op : g.nodes[n].operands) visit(op);
+    c.topo.push_back(n);
+  };
+  for (int m : p.members) visit(m);
+  for (int m : c.topo) {
+    const Node& n = g.nodes[m];
+    if (n.op == SFX_OP_BATCH_MATMUL || n.op == SFX_OP_LIBRARY_CALL)
+      throw Error(SFX_ERR_UNSUPPORTED, "group member " + n.id +
+                                           " is a matmul; the device path covers non-MatMul groups only");
+    bool d = n.op == SFX_OP_REDUCE;
+    for (int op : n.operands)
+      if (p.is_member(op) && c.dep[op]) d = true;
+    c.dep[m] = d;
+    if (n.op == SFX_OP_REDUCE) c.reduces.push_back(m);
+  }
+  int64_t big = 0;
+  for (int m : p.members) big = std::max(big, g.nodes[m].numel());
+  for (int e : p.externals) big = std::max(big, g.nodes[e].numel());
+  c.wide = big >= (int64_t{1} << 30) || p.blocks >= (int64_t{1} << 30);
+  c.name = sanitize(g.nodes[p.fusion_root >= 0 ? p.fusion_root : p.roots[0]].id);
+  return c;
+}
+
+// ---- kernel scaffolding ---------------------------------------------------
+
+std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block) {
+  std::ostringstream os;
+  os << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << entry << "(";
+  bool first = true;
+  int64_t biggest_root = 0;
+  for (int r : c.p.roots) biggest_root = std::max(biggest_root, c.g.nodes[r].numel());
+  for (size_t k = 0; k < c.p.inputs.size(); ++k) {
+    int n = c.p.inputs[k];
+    std::string name = "in" + std::to_string(k);
+    os << (first ? "" : ", ") << "const " << ctype(c.g.nodes[n].dtype) << "* __restrict__ " << name;
+    first = false;
+    em.input_ptr[n] = name;
+    if (c.g.nodes[n].numel() * 4 >= (int64_t{1} << 20)) em.streaming.insert(n);
+  }
+  for (size_t r = 0; r < c.p.roots.size(); ++r) {
+    os << (first ? "" : ", ") << ctype(c.g.nodes[c.p.roots[r]].dtype) << "* __restrict__ out" << r;
+    first = false;
+  }
+  os << (first ? "" : ", ") << "unsigned* __restrict__ ws)";
+  return os.str();
+}
+
+void fill_common(const Ctx& c, KernelSource& ks) {
+  ks.inputs = c.p.inputs;
+  ks.outputs = c.p.roots;
+  int64_t b = 0;
+  for (int n : c.p.inputs) b += c.g.nodes[n].numel() * 4;
+  for (int n : c.p.roots) b += c.g.nodes[n].numel() * 4;
+  ks.algorithmic_bytes = b;
+}
+
+std::string assemble(const std::string& sig, const Code& body) {
+  std::string s = kPrelude;
+  s += "\n";
+  s += sig;
+  s += " {\n";
+  s += body.text;
+  s += "}\n";
+  return s;
+}
+
+int root_slot(const Ctx& c, int node) {
+  for (size_t r = 0; r < c.p.roots.size(); ++r)
+    if (c.p.roots[r] == node) return static_cast<int>(r);
+  return -1;
+}
+
+// index component splitting a linear (row, col) pair for a node of `dims`,
+// when its dims split as [row dims | col dims] with prod(row dims) == R
+int prefix_split(const std::vector<int64_t>& dims, int64_t R) {
+  int64_t acc = 1;
+  for (size_t k = 0; k <= dims.size(); ++k) {
+    if (acc == R) return static_cast<int>(k);
+    if (k < dims.size()) acc *= dims[k];
+  }
+  return -1;
+}
+
+std::vector<Ix> rowcol_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t R, int64_t C,
+                             const Ix& row, const Ix& col) {
+  int k = prefix_split(dims, R);
+  if (k >= 0 && prod(dims, k, dims.size()) == C) {
+    std::vector<int64_t> rd(dims.begin(), dims.begin() + k), cd(dims.begin() + k, dims.end());
+    std::vector<Ix> a = em.from_linear(row, rd);
+    std::vector<Ix> b = em.from_linear(col, cd);
+    a.insert(a.end(), b.begin(), b.end());
+    return a;
+  }
+  // no [row|col] split of this shape: go through the linear index
+  Ix L;
+  std::string rb = em.ivar(Emitter::imul(row.e, C));
+  if (col.kind == IX_PLUS) {
+    L = em.lane_plus(em.ivar(Emitter::iadd(rb, col.base)));
+  } else {
+    L = em.uni(em.ivar(Emitter::iadd(rb, col.e)));
+    L.kind = col.kind;
+  }
+  return em.from_linear(L, dims);
+}
+
+bool bcast_is_reshape(const Node& m) {
+  std::set<int64_t> mapped(m.dim_map.begin(), m.dim_map.end());
+  for (int i = 0; i < m.rank(); ++i)
+    if (!mapped.count(i) && m.dims[i] != 1) return false;
+  return true;
+}
+
+bool transpose_is_reshape(const Node& m) {
+  int64_t prev = -1;
+  for (int i = 0; i < m.rank(); ++i) {
+    if (m.dims[i] == 1) continue;
+    if (m.perm[i] < prev) return false;
+    prev = m.perm[i];
+  }
+  return true;
+}
+
+// ---- ROW analysis ------------------------------------------------------------
+
+struct RowPlan {
+  int64_t R = 0, C = 0;
+  std::map<int, int> cls;
+  std::map<int, int> level;
+  int max_level = 0;
+};
+
+bool analyze_row(const Ctx& c, RowPlan* rp, std::string* why) {
+  const Graph& g = c.g;
+  if (c.reduces.empty()) return *why = "no reduction", false;
+  for (int r : c.reduces) {
+    const Node& n = g.nodes[r];
+    const Node& in = g.nodes[n.operands[0]];
+    std::vector<int64_t> rd = n.reduce_dims;
+    std::sort(rd.begin(), rd.end());
+    int k = in.rank() - static_cast<int>(rd.size());
+    for (size_t i = 0; i < rd.size(); ++i)
+      if (rd[i] != k + static_cast<int64_t>(i)) return *why = "reduce " + n.id + " is not over trailing dims", false;
+    int64_t R = prod(in.dims, 0, k), C = prod(in.dims, k, in.dims.size());
+    if (rp->R == 0) {
+      rp->R = R;
+      rp->C = C;
+    } else if (rp->R != R || rp->C != C) {
+      return *why = "reductions with different row geometry", false;
+    }
+  }
+  if (rp->C <= 1) return *why = "degenerate row length", false;
+  const int64_t R = rp->R, C = rp->C;
+  auto cls_of_numel = [&](int64_t n) { return n == R * C ? CLS_FULL : (n == R ? CLS_ROWV : CLS_NONE); };
+  for (int m : c.topo) {
+    const Node& n = g.nodes[m];
+    if (!c.dep.at(m)) continue;
+    int cls = cls_of_numel(n.numel());
+    if (n.op == SFX_OP_REDUCE) {
+      int op = n.operands[0];
+      if (c.p.is_member(op) && c.dep.at(op) && rp->cls[op] != CLS_FULL)
+        return *why = "reduce operand " + g.nodes[op].id + " is not row-shaped", false;
+      rp->cls[m] = CLS_ROWV;
+      int lv = 1;
+      std::function<void(int)> walk;
+      std::set<int> seen;
+      walk = [&](int x) {
+        if (!c.p.is_member(x) || seen.count(x)) return;
+        seen.insert(x);
+        if (x != m && g.nodes[x].op == SFX_OP_REDUCE) lv = std::max(lv, rp->level[x] + 1);
+        if (x == m || g.nodes[x].op != SFX_OP_REDUCE)
+          for (int o : g.nodes[x].operands) walk(o);
+      };
+      walk(m);
+      rp->level[m] = lv;
+      rp->max_level = std::max(rp->max_level, lv);
+      continue;
+    }
+    if (cls == CLS_NONE) return *why = "member " + n.id + " is neither row- nor element-shaped", false;
+    for (int op : n.operands) {
+      if (!c.p.is_member(op) || !c.dep.at(op)) continue;
+      int oc = rp->cls[op];
+      const Node& o = g.nodes[op];
+      switch (n.op) {
+        case SFX_OP_ELEMENTWISE:
+        case SFX_OP_RESHAPE:
+        case SFX_OP_BITCAST:
+          if (oc != cls) return *why = "class mismatch at " + n.id, false;
+          break;
+        case SFX_OP_BROADCAST: {
+          if (bcast_is_reshape(n) && oc == cls) break;
+          bool prefix = cls == CLS_FULL && oc == CLS_ROWV;
+          for (size_t j = 0; prefix && j < n.dim_map.size(); ++j)
+            if (n.dim_map[j] != static_cast<int64_t>(j)) prefix = false;
+          if (prefix && prod(n.dims, n.dim_map.size(), n.dims.size()) == C) break;
+          return *why = "broadcast " + n.id + " does not map rows to rows", false;
+        }
+        case SFX_OP_TRANSPOSE: {
+          if (oc != cls) return *why = "class mismatch at " + n.id, false;
+          if (transpose_is_reshape(n)) break;
+          int k = prefix_split(n.dims, R);
+          bool ok = cls == CLS_FULL && k >= 0;
+          for (int i = 0; ok && i < k; ++i)
+            if (n.perm[i] != i) ok = false;
+          if (ok) break;
+          return *why = "transpose " + n.id + " moves data across rows", false;
+        }
+        default:
+          return *why = "unsupported op at " + n.id, false;
+      }
+      (void)o;
+    }
+    rp->cls[m] = cls;
+  }
+  for (int r : c.p.roots) {
+    int cls = cls_of_numel(g.nodes[r].numel());
+    if (cls == CLS_NONE) return *why = "root " + g.nodes[r].id + " is neither row- nor element-shaped", false;
+    if (c.dep.at(r) && rp->cls[r] != cls) return *why = "root class mismatch", false;
+  }
+  return true;
+}
+
+// ---- COL analysis ------------------------------------------------------------
+
+struct ColPlan {
+  int64_t R = 0, C = 0;  // R = reduced extent (rows), C = output elements (columns)
+};
+
+bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
+  const Graph& g = c.g;
+  if (c.reduces.empty()) return *why = "no reduction", false;
+  for (int r : c.reduces) {
+    const Node& n = g.nodes[r];
+    const Node& in = g.nodes[n.operands[0]];
+    if (c.p.is_member(n.operands[0]) && c.dep.at(n.operands[0]))
+      return *why = "nested reduction at " + n.id, false;
+    std::vector<int64_t> rd = n.reduce_dims;
+    std::sort(rd.begin(), rd.end());
+    for (size_t i = 0; i < rd.size(); ++i)
+      if (rd[i] != static_cast<int64_t>(i)) return *why = "reduce " + n.id + " is not over leading dims", false;
+    int k = static_cast<int>(rd.size());
+    int64_t R = prod(in.dims, 0, k), C = prod(in.dims, k, in.dims.size());
+    if (cp->R == 0) {
+      cp->R = R;
+      cp->C = C;
+    } else if (cp->R != R || cp->C != C) {
+      return *why = "column reductions with different geometry", false;
+    }
+  }
+  const int64_t R = cp->R, C = cp->C;
+  if (R <= 1) return *why = "degenerate column length", false;
+  for (int m : c.topo) {
+    const Node& n = g.nodes[m];
+    if (!c.dep.at(m) || n.op == SFX_OP_REDUCE) continue;
+    if (n.numel() != C) return *why = "member " + n.id + " needs the reduced columns broadcast back", false;
+    switch (n.op) {
+      case SFX_OP_ELEMENTWISE:
+      case SFX_OP_RESHAPE:
+      case SFX_OP_BITCAST:
+        break;
+      case SFX_OP_BROADCAST:
+        if (!bcast_is_reshape(n)) return *why = "broadcast of reduced columns at " + n.id, false;
+        break;
+      case SFX_OP_TRANSPOSE:
+        if (!transpose_is_reshape(n)) return *why = "transpose of reduced columns at " + n.id, false;
+        break;
+      default:
+        return *why = "unsupported op at " + n.id, false;
+    }
+  }
+  for (int r : c.p.roots) {
+    int64_t n = g.nodes[r].numel();
+    if (c.dep.at(r)) {
+      if (n != C) return *why = "root " + g.nodes[r].id + " mixes reduced and unreduced data", false;
+    } else if (n != R * C && n != C) {
+      return *why = "root " + g.nodes[r].id + " has unrelated shape", false;
+    }
+  }
+  return true;
+}
+
+// ---- MAP -----------------------------------------------------------------------
+
+bool analyze_map(const Ctx& c, std::string* why) {
+  if (!c.reduces.empty()) return *why = "group has reductions", false;
+  return true;
+}
+
+KernelSource lower_map(const Ctx& c) {
+  KernelSource ks;
+  ks.strategy = "map";
+  ks.entry = "sfx_map_" + c.name;
+  fill_common(c, ks);
+  const int B = 256;
+  // shape classes: roots with identical dims share one loop (and their CSE)
+  std::map<std::vector<int64_t>, std::vector<int>> classes;
+  for (int r : c.p.roots) classes[c.g.nodes[r].dims].push_back(r);
+  int vmax = 1;
+  int64_t max_items = 1;
+  std::vector<std::pair<int, int64_t>> vw;  // per class: V, items
+  for (auto& [dims, roots] : classes) {
+    int64_t n = prod(dims, 0, dims.size());
+    int V = (!dims.empty() && dims.back() % 4 == 0) ? 4 : 1;
+    vw.push_back({V, n / V});
+    vmax = std::max(vmax, V);
+    max_items = std::max(max_items, n / V);
+  }
+  Code body;
+  // one emitter per class (lane count differs)
+  std::string sig;
+  {
+    Emitter probe(c.g, c.p, 1, c.wide);
+    sig = signature(c, probe, ks.entry, B);
+  }
+  std::string idx_t = c.wide ? "long long" : "int";
+  body.line("const " + idx_t + " it = (" + idx_t + ")blockIdx.x * " + std::to_string(B) + " + threadIdx.x;");
+  size_t ci = 0;
+  for (auto& [dims, roots] : classes) {
+    auto [V, items] = vw[ci++];
+    Emitter em(c.g, c.p, V, c.wide);
+    signature(c, em, ks.entry, B);
+    em.code = &body;
+    body.line("if (it < " + fmt_i(items) + ") {");
+    body.indent++;
+    em.push();
+    std::string base = V == 1 ? "it" : em.ivar(Emitter::imul("it", V));
+    std::vector<std::vector<std::string>> vals(roots.size(), std::vector<std::string>(V));
+    for (int lane = 0; lane < V; ++lane) {
+      em.lane = lane;
+      Ix L = V == 1 ? em.uni(base) : em.lane_plus(base);
+      for (size_t k = 0; k < roots.size(); ++k) {
+        std::vector<Ix> comps = em.from_linear(L, c.g.nodes[roots[k]].dims);
+        vals[k][lane] = em.value(roots[k], comps);
+      }
+    }
+    for (size_t k = 0; k < roots.size(); ++k) {
+      std::string out = "out" + std::to_string(root_slot(c, roots[k]));
+      if (V == 4)
+        body.line("sfx_st4(" + out + " + " + base + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
+                  vals[k][2] + ", " + vals[k][3] + ");");
+      else
+        body.line(out + "[" + base + "] = " + vals[k][0] + ";");
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = (max_items + B - 1) / B;
+  ks.vector_width = vmax;
+  ks.note = "kLoop over " + std::to_string(classes.size()) + " root shape class(es)";
+  return ks;
+}
+
+// ---- ROW ------------------------------------------------------------------------
+
+KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "row";
+  ks.entry = "sfx_row_" + c.name;
+  fill_common(c, ks);
+  const int64_t R = rp.R, C = rp.C;
+  int V = (C % 4 == 0) ? 4 : 1;
+  int TPR = 1;
+  for (int t = 32; t >= 1; t /= 2)
+    if (C % (static_cast<int64_t>(t) * V) == 0) {
+      TPR = t;
+      break;
+    }
+  if (o.threads_per_row > 0) {
+    int t = o.threads_per_row;
+    if (t > 32 || (t & (t - 1)) || C % (static_cast<int64_t>(t) * V) != 0)
+      throw Error(SFX_ERR_INVALID, "threads_per_row must be a power of two <= 32 dividing the row");
+    TPR = t;
+  }
+  const int64_t NCH = C / (static_cast<int64_t>(TPR) * V);
+  if (NCH * V > 64) throw Error(SFX_ERR_UNSUPPORTED, "row of " + std::to_string(C) + " elements exceeds the register-resident row template");
+  const int B = 256;
+  int RPC = B / TPR;
+  if (o.rows_per_cta > 0 && o.rows_per_cta <= RPC) RPC = o.rows_per_cta;
+  const int threads = RPC * TPR;
+
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, threads);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("const int tid = threadIdx.x;");
+  body.line("const int lr = tid & " + std::to_string(TPR - 1) + ";");
+  body.line("const " + it + " row = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + (tid / " +
+            std::to_string(TPR) + ");");
+  body.line("if (row >= " + fmt_i(R) + ") return;");
+  if (TPR > 1) {
+    if (TPR == 32)
+      body.line("const sfx_u32 gmask = 0xffffffffu;");
+    else
+      body.line("const sfx_u32 gmask = " + std::to_string((1u << TPR) - 1) + "u << ((tid & 31) & " +
+                std::to_string(32 - TPR) + ");");
+    body.line("const int gleader = (tid & 31) & " + std::to_string(32 - TPR) + ";");
+  }
+  std::vector<std::string> cb(NCH);
+  for (int64_t j = 0; j < NCH; ++j) {
+    cb[j] = "cb" + std::to_string(j);
+    body.line("const " + it + " " + cb[j] + " = lr * " + std::to_string(V) + " + " +
+              fmt_i(j * TPR * V) + ";");
+  }
+  Ix rowix = em.uni("row");
+  auto col_ix = [&](int64_t j, int lane) {
+    em.lane = lane;
+    return V == 1 ? em.uni(cb[j]) : em.lane_plus(cb[j]);
+  };
+  std::map<int, std::string> reduced;  // reduce node -> combined value
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    if (c.g.nodes[node].op != SFX_OP_REDUCE) return "";
+    auto f = reduced.find(node);
+    if (f == reduced.end()) throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
+    return f->second;
+  };
+
+  for (int lv = 1; lv <= rp.max_level; ++lv) {
+    std::vector<int> red;
+    for (int r : c.reduces)
+      if (rp.level.at(r) == lv) red.push_back(r);
+    std::vector<std::string> acc(red.size()), first(red.size());
+    for (size_t k = 0; k < red.size(); ++k) {
+      acc[k] = em.fresh("acc");
+      body.line(std::string(ctype(c.g.nodes[red[k]].dtype)) + " " + acc[k] + ";");
+    }
+    for (int64_t j = 0; j < NCH; ++j)
+      for (int lane = 0; lane < V; ++lane) {
+        Ix col = col_ix(j, lane);
+        for (size_t k = 0; k < red.size(); ++k) {
+          const Node& rn = c.g.nodes[red[k]];
+          const Node& in = c.g.nodes[rn.operands[0]];
+          std::vector<Ix> comps = rowcol_comps(em, in.dims, R, C, rowix, col);
+          std::string v = em.value(rn.operands[0], comps);
+          if (j == 0 && lane == 0) {
+            body.line(acc[k] + " = " + v + ";");
+            first[k] = v;
+          } else {
+            const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                            : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+            body.line(acc[k] + " = " + f + "(" + acc[k] + ", " + v + ");");
+          }
+        }
+      }
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                      : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+      for (int m = TPR / 2; m >= 1; m /= 2)
+        body.line(acc[k] + " = " + f + "(" + acc[k] + ", sfx_shfl_xor(" + acc[k] + ", " +
+                  std::to_string(m) + ", gmask));");
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+        std::string f0 = TPR > 1 ? "sfx_shfl(" + first[k] + ", gleader, gmask)" : first[k];
+        body.line(acc[k] + " = sfx_fold_first(" + f0 + ", " + acc[k] + ");");
+      }
+      reduced[red[k]] = acc[k];
+    }
+  }
+
+  // final phase: element roots (vectorised stores) and row roots (lane 0)
+  std::vector<int> full_roots, row_roots;
+  for (int r : c.p.roots) (c.g.nodes[r].numel() == R * C ? full_roots : row_roots).push_back(r);
+  const std::string rb = em.ivar(Emitter::imul("row", C));
+  for (int64_t j = 0; j < NCH; ++j) {
+    std::vector<std::vector<std::string>> vals(full_roots.size(), std::vector<std::string>(V));
+    for (int lane = 0; lane < V; ++lane) {
+      Ix col = col_ix(j, lane);
+      for (size_t k = 0; k < full_roots.size(); ++k)
+        vals[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rowix, col));
+    }
+    std::string addr = em.ivar(Emitter::iadd(rb, cb[j]));
+    for (size_t k = 0; k < full_roots.size(); ++k) {
+      std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+      if (V == 4)
+        body.line("sfx_st4(" + out + " + " + addr + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
+                  vals[k][2] + ", " + vals[k][3] + ");");
+      else
+        body.line(out + "[" + addr + "] = " + vals[k][0] + ";");
+    }
+  }
+  if (!row_roots.empty()) {
+    em.lane = 0;
+    body.line("if (lr == 0) {");
+    body.indent++;
+    em.push();
+    for (int r : row_roots) {
+      std::string v = em.value(r, em.from_linear(rowix, c.g.nodes[r].dims));
+      body.line("out" + std::to_string(root_slot(c, r)) + "[row] = " + v + ";");
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  ks.code = assemble(sig, body);
+  ks.block = threads;
+  ks.grid_x = (R + RPC - 1) / RPC;
+  ks.vector_width = V;
+  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " threads/row=" +
+            std::to_string(TPR) + " elems/thread=" + std::to_string(NCH * V) + " levels=" +
+            std::to_string(rp.max_level);
+  return ks;
+}
+
+// ---- COL ------------------------------------------------------------------------
+
+KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
+  KernelSource ks;
+  ks.strategy = "col";
+  ks.entry = "sfx_col_" + c.name;
+  fill_common(c, ks);
+  const int64_t R = cp.R, C = cp.C;
+  const int V = (C % 4 == 0) ? 4 : 1;
+  const int WARPS = 8, B = WARPS * 32;
+  const int64_t TC = 32 * V;
+  const int64_t tiles = (C + TC - 1) / TC;
+  int64_t S = std::max<int64_t>(1, (kNumSMs * 4 + tiles - 1) / tiles);
+  S = std::min<int64_t>(S, std::max<int64_t>(1, R / 64));
+  S = std::min<int64_t>(S, 65535);
+  const int64_t RS = (R + S - 1) / S;
+  const int NR = static_cast<int>(c.reduces.size());
+
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, B);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  // workspace: tickets[tiles] (256-B padded), then partials[NR][S][C]
+  const int64_t ticket_words = (tiles + 63) / 64 * 64;
+  ks.workspace_bytes = ticket_words * 4 + static_cast<int64_t>(NR) * S * C * 4;
+
+  body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + lane * " + std::to_string(V) + ";");
+  body.line("const bool cok = c0 < " + fmt_i(C) + ";");
+  body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
+  std::vector<std::vector<std::string>> acc(NR, std::vector<std::string>(V));
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    std::string init;
+    if (rn.reducer == SFX_REDUCE_SUM) init = rn.dtype == SFX_F32 ? "0.0f" : "0";
+    else if (rn.dtype == SFX_F32) init = "sfx_bits_f(0x7fc00000)";  // NaN = identity of fmaxf/fminf
+    else init = rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+    for (int l = 0; l < V; ++l) {
+      acc[k][l] = em.fresh("acc");
+      body.line(std::string(ctype(rn.dtype)) + " " + acc[k][l] + " = " + init + ";");
+    }
+  }
+  std::vector<int> full_roots, col_roots;
+  for (int r : c.p.roots) (c.dep.at(r) || c.g.nodes[r].numel() != R * C ? col_roots : full_roots).push_back(r);
+
+  body.line("if (cok) {");
+  body.indent++;
+  body.line("#pragma unroll 4");
+  body.line("for (" + it + " r = r_begin + warp; r < r_end; r += " + std::to_string(WARPS) + ") {");
+  body.indent++;
+  em.push();
+  Ix rix = em.uni("r");
+  std::string rbase = em.ivar(Emitter::imul("r", C));
+  std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+  for (int lane = 0; lane < V; ++lane) {
+    em.lane = lane;
+    Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+    for (size_t k = 0; k < full_roots.size(); ++k)
+      fv[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rix, col));
+    for (int k = 0; k < NR; ++k) {
+      const Node& rn = c.g.nodes[c.reduces[k]];
+      const Node& in = c.g.nodes[rn.operands[0]];
+      std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rix, col));
+      const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                      : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+      body.line(acc[k][lane] + " = " + f + "(" + acc[k][lane] + ", " + v + ");");
+    }
+  }
+  if (!full_roots.empty()) {
+    std::string addr = em.ivar(Emitter::iadd(rbase, "c0"));
+    for (size_t k = 0; k < full_roots.size(); ++k) {
+      std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+      if (V == 4)
+        body.line("sfx_st4(" + out + " + " + addr + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
+                  ", " + fv[k][3] + ");");
+      else
+        body.line(out + "[" + addr + "] = " + fv[k][0] + ";");
+    }
+  }
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.indent--;
+  body.line("}");
+
+  // CTA combine through shared memory (deterministic warp order)
+  for (int k = 0; k < NR; ++k) {
+    const char* T = ctype(c.g.nodes[c.reduces[k]].dtype);
+    body.line(std::string("__shared__ ") + T + " sp" + std::to_string(k) + "[" + std::to_string(WARPS) + "][" +
+              fmt_i(TC) + "];");
+    for (int l = 0; l < V; ++l)
+      body.line("sp" + std::to_string(k) + "[warp][lane * " + std::to_string(V) + " + " + std::to_string(l) +
+                "] = " + acc[k][l] + ";");
+  }
+  body.line("__syncthreads();");
+  body.line("unsigned* tickets = ws;");
+  body.line("if (warp == 0 && cok) {");
+  body.indent++;
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const char* T = ctype(rn.dtype);
+    const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                    : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+    std::string part = "part" + std::to_string(k);
+    body.line(std::string(T) + "* " + part + " = (" + T + "*)(ws + " + fmt_i(ticket_words) + ") + " +
+              fmt_i(static_cast<int64_t>(k) * S * C) + ";");
+    for (int l = 0; l < V; ++l) {
+      std::string sidx = "lane * " + std::to_string(V) + " + " + std::to_string(l);
+      std::string t = em.fresh("t");
+      body.line(std::string(T) + " " + t + " = sp" + std::to_string(k) + "[0][" + sidx + "];");
+      for (int w = 1; w < WARPS; ++w)
+        body.line(t + " = " + f + "(" + t + ", sp" + std::to_string(k) + "[" + std::to_string(w) + "][" + sidx + "]);");
+      body.line(part + "[(" + it + ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + "] = " + t + ";");
+    }
+  }
+  body.indent--;
+  body.line("}");
+  body.line("__threadfence();");
+  body.line("__syncthreads();");
+  body.line("__shared__ unsigned s_last;");
+  body.line("if (threadIdx.x == 0) s_last = (atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1u);");
+  body.line("__syncthreads();");
+  body.line("if (!s_last) return;");
+  body.line("__threadfence();");
+  // finisher: ordered combine over stripes, then the column roots
+  body.line("if (warp == 0 && cok) {");
+  body.indent++;
+  em.push();
+  std::map<int, std::vector<std::string>> total;
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const char* T = ctype(rn.dtype);
+    const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                    : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+    std::string part = "fp" + std::to_string(k);
+    body.line(std::string("const ") + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(ticket_words) +
+              ") + " + fmt_i(static_cast<int64_t>(k) * S * C) + " + c0;");
+    std::vector<std::string> tv(V);
+    for (int l = 0; l < V; ++l) {
+      tv[l] = em.fresh("tot");
+      body.line(std::string(T) + " " + tv[l] + " = __ldcg(" + part + " + " + std::to_string(l) + ");");
+    }
+    body.line("for (" + it + " s = 1; s < " + fmt_i(S) + "; ++s) {");
+    for (int l = 0; l < V; ++l)
+      body.line("  " + tv[l] + " = " + f + "(" + tv[l] + ", __ldcg(" + part + " + s * " + fmt_i(C) + " + " +
+                std::to_string(l) + "));");
+    body.line("}");
+    if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+      // sequential std::max/min fold semantics: a NaN first element wins
+      const Node& in = c.g.nodes[rn.operands[0]];
+      for (int l = 0; l < V; ++l) {
+        em.lane = l;
+        Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+        std::string f0 = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, em.uni("0"), col));
+        body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
+      }
+    }
+    total[c.reduces[k]] = tv;
+  }
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    auto f = total.find(node);
+    if (f == total.end()) return "";
+    return f->second[em.lane];
+  };
+  for (int r : col_roots) {
+    std::vector<std::string> v(V);
+    for (int l = 0; l < V; ++l) {
+      em.lane = l;
+      Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+      v[l] = em.value(r, em.from_linear(col, c.g.nodes[r].dims));
+    }
+    std::string out = "out" + std::to_string(root_slot(c, r));
+    if (V == 4)
+      body.line("sfx_st4(" + out + " + c0, " + v[0] + ", " + v[1] + ", " + v[2] + ", " + v[3] + ");");
+    else
+      body.line(out + "[c0] = " + v[0] + ";");
+  }
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.line("if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;");
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = tiles;
+  ks.grid_y = S;
+  ks.vector_width = V;
+  ks.note = "reduced=" + std::to_string(R) + " cols=" + std::to_string(C) + " tiles=" + std::to_string(tiles) +
+            " stripes=" + std::to_string(S);
+  return ks;
+}
+
+// ---- LITERAL --------------------------------------------------------------------
+
+// chunk_box geometry (reference schedule.cpp:52-76) for a materialised member
+struct Box {
+  std::vector<std::string> lo;
+  std::vector<int64_t> len;
+};
+
+Box chunk_box(Emitter& em, const Node& n, const Stmt& s, const std::string& blk) {
+  Box b;
+  const int rank = n.rank();
+  b.lo.assign(rank, "0");
+  b.len = n.dims;
+  if (rank == 0) return b;
+  const int64_t sd = s.split_dim;
+  const int64_t slice_len = n.dims[sd] / s.sword;
+  std::string slice = em.ivar(Emitter::imod(blk, s.sword));
+  std::string fixed = em.ivar(Emitter::idiv(blk, s.sword));
+  b.lo[sd] = em.ivar(Emitter::imul(slice, slice_len));
+  b.len[sd] = slice_len;
+  if (s.sched == SFX_SCHED_ROW) {
+    for (int64_t i = sd - 1; i >= 0; --i) {
+      b.lo[i] = em.ivar(Emitter::imod(fixed, n.dims[i]));
+      fixed = em.ivar(Emitter::idiv(fixed, n.dims[i]));
+      b.len[i] = 1;
+    }
+  } else {
+    for (int64_t i = rank - 1; i > sd; --i) {
+      b.lo[i] = em.ivar(Emitter::imod(fixed, n.dims[i]));
+      fixed = em.ivar(Emitter::idiv(fixed, n.dims[i]));
+      b.len[i] = 1;
+    }
+  }
+  return b;
+}
+
+KernelSource lower_literal(const Ctx& c) {
+  KernelSource ks;
+  ks.strategy = "literal";
+  ks.entry = "sfx_lit_" + c.name;
+  fill_common(c, ks);
+  const Graph& g = c.g;
+  const Program& p = c.p;
+  // materialised members and their statements
+  std::map<int, const Stmt*> mat;
+  int64_t max_chunk = 1;
+  for (const Stmt& s : p.stmts)
+    if (s.kind == SFX_STMT_MATERIALIZE) {
+      mat[s.instr] = &s;
+      max_chunk = std::max(max_chunk, g.nodes[s.instr].numel() / p.blocks);
+    }
+  int B = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, (max_chunk + 31) / 32 * 32)));
+  Emitter em(g, p, 1, c.wide);
+  std::string sig = signature(c, em, ks.entry, B);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  int64_t staging = 0;  // extra smem for two-phase writes into an aliased buffer
+  // ready-set simulation (reference exec.cpp:300-392): arena reads only of
+  // members materialised earlier in this block and not overwritten since.
+  std::set<int> ready;
+  std::set<int> read_now;
+  std::string blk = "blk";
+  std::map<int, Box> boxes;
+  em.resolve = [&](int node, const std::vector<Ix>& comps) -> std::string {
+    if (!ready.count(node)) return "";
+    read_now.insert(node);
+    const Node& n = g.nodes[node];
+    const Stmt& s = *mat.at(node);
+    Box& b = boxes[node];
+    std::vector<Ix> local(comps.size());
+    std::string L = "0";
+    for (size_t d = 0; d < comps.size(); ++d) {
+      std::string off = b.lo[d] == "0" ? comps[d].e : "(" + comps[d].e + "-" + b.lo[d] + ")";
+      L = Emitter::iadd(Emitter::imul(L, b.len[d]), off);
+      if (!Emitter::is_lit(L)) L = em.ivar(L);
+    }
+    std::string v = em.fresh("s");
+    const char* T = ctype(n.dtype);
+    em.code->line(std::string("const ") + T + " " + v + " = ((const " + T + "*)(sfx_arena + " + fmt_i(s.offset) +
+                  "))[" + L + "];");
+    return v;
+  };
+  body.line("extern __shared__ __align__(16) unsigned char sfx_arena[];");
+  body.line("for (" + it + " blk = blockIdx.x; blk < " + fmt_i(p.blocks) + "; blk += gridDim.x) {");
+  body.indent++;
+  em.push();
+  for (const Stmt& s : p.stmts) {
+    if (s.kind == SFX_STMT_BARRIER) {
+      body.line("__syncthreads();");
+      continue;
+    }
+    if (s.kind != SFX_STMT_MATERIALIZE) continue;
+    const Node& n = g.nodes[s.instr];
+    Box b = chunk_box(em, n, s, blk);
+    const int64_t chunk = n.numel() / p.blocks;
+    const char* T = ctype(n.dtype);
+    // detect whether this write aliases a ready buffer it reads (two-phase commit)
+    bool shared_dest = s.dest == SFX_DEST_SHARED;
+    std::string stage;
+    Code saved;
+    read_now.clear();
+    Code tmp;
+    tmp.indent = body.indent + 1;
+    Code* outer = em.code;
+    // emit the element loop body into tmp first to learn which buffers it reads
+    em.code = &tmp;
+    em.push();
+    std::string k = em.fresh("k");
+    std::vector<Ix> local = em.from_linear(em.uni(k), b.len);
+    std::vector<Ix> comps(n.rank());
+    for (int d = 0; d < n.rank(); ++d) comps[d] = em.uni(em.ivar(Emitter::iadd(b.lo[d], local[d].e)));
+    std::string v = em.value(s.instr, comps);
+    bool hazard = false;
+    if (shared_dest)
+      for (int r : read_now) {
+        const Stmt& rs = *mat.at(r);
+        int64_t len = g.nodes[r].numel() / p.blocks * 4;
+        if (rs.offset < s.offset + s.bytes && s.offset < rs.offset + len) hazard = true;
+      }
+    if (shared_dest) {
+      if (hazard) {
+        staging = std::max<int64_t>(staging, chunk * 4);
+        tmp.line(std::string("((") + T + "*)(sfx_arena + " + fmt_i(p.arena_bytes) + "))[" + k + "] = " + v + ";");
+      } else {
+        tmp.line(std::string("((") + T + "*)(sfx_arena + " + fmt_i(s.offset) + "))[" + k + "] = " + v + ";");
+      }
+    } else {
+      std::string lin = "0";
+      for (int d = 0; d < n.rank(); ++d) lin = Emitter::iadd(Emitter::imul(lin, n.dims[d]), comps[d].e);
+      tmp.line("out" + std::to_string(s.root_index) + "[" + lin + "] = " + v + ";");
+    }
+    em.pop();
+    em.code = outer;
+    body.line("for (" + it + " " + k + " = threadIdx.x; " + k + " < " + fmt_i(chunk) + "; " + k + " += " +
+              std::to_string(B) + ") {");
+    body.text += tmp.text;
+    body.line("}");
+    if (shared_dest && hazard) {
+      body.line("__syncthreads();");
+      body.line("for (" + it + " " + k + " = threadIdx.x; " + k + " < " + fmt_i(chunk) + "; " + k + " += " +
+                std::to_string(B) + ")");
+      body.line(std::string("  ((") + T + "*)(sfx_arena + " + fmt_i(s.offset) + "))[" + k + "] = ((" + T +
+                "*)(sfx_arena + " + fmt_i(p.arena_bytes) + "))[" + k + "];");
+    }
+    if (shared_dest) {
+      for (auto itr = ready.begin(); itr != ready.end();) {
+        const Stmt& rs = *mat.at(*itr);
+        int64_t len = g.nodes[*itr].numel() / p.blocks * 4;
+        bool overlap = rs.offset < s.offset + s.bytes && s.offset < rs.offset + len;
+        if (overlap && *itr != s.instr)
+          itr = ready.erase(itr);
+        else
+          ++itr;
+      }
+      ready.insert(s.instr);
+      boxes[s.instr] = b;
+    }
+  }
+  body.line("__syncthreads();");
+  em.pop();
+  body.indent--;
+  body.line("}");
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = std::min<int64_t>(p.blocks, static_cast<int64_t>(kNumSMs) * 16);
+  ks.smem = static_cast<int>(p.arena_bytes + staging);
+  ks.vector_width = 1;
+  ks.note = "reference geometry: blocks=" + std::to_string(p.blocks) + " arena=" + std::to_string(p.arena_bytes) + "B";
+  return ks;
+}
+
+}  // namespace
+
+std::string choose_strategy(const Graph& g, int pi, std::string* why) {
+  const Program& p = g.programs.at(pi);
+  Ctx c = make_ctx(g, p);
+  std::string w;
+  if (analyze_map(c, &w)) return "map";
+  std::string reasons = "map: " + w;
+  RowPlan rp;
+  if (analyze_row(c, &rp, &w)) {
+    int V = rp.C % 4 == 0 ? 4 : 1;
+    int TPR = 1;
+    for (int t = 32; t >= 1; t /= 2)
+      if (rp.C % (static_cast<int64_t>(t) * V) == 0) {
+        TPR = t;
+        break;
+      }
+    if (rp.C / TPR <= 64) return "row";
+    w = "row too long for registers";
+  }
+  reasons += "; row: " + w;
+  ColPlan cp;
+  if (analyze_col(c, &cp, &w)) return "col";
+  reasons += "; col: " + w;
+  if (why) *why = reasons;
+  return "literal";
+}
+
+KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
+  if (pi < 0 || pi >= static_cast<int>(g.programs.size())) throw Error(SFX_ERR_INVALID, "program index out of range");
+  const Program& p = g.programs[pi];
+  Ctx c = make_ctx(g, p);
+  std::string why;
+  int strat = o.strategy;
+  if (strat == SFX_STRATEGY_AUTO) {
+    std::string s = choose_strategy(g, pi, &why);
+    strat = s == "map" ? SFX_STRATEGY_MAP : s == "row" ? SFX_STRATEGY_ROW : s == "col" ? SFX_STRATEGY_COL
+                                                                                        : SFX_STRATEGY_LITERAL;
+  }
+  KernelSource ks;
+  switch (strat) {
+    case SFX_STRATEGY_MAP:
+      if (!analyze_map(c, &why)) throw Error(SFX_ERR_UNSUPPORTED, "map template not applicable: " + why);
+      ks = lower_map(c);
+      break;
+    case SFX_STRATEGY_ROW: {
+      RowPlan rp;
+      if (!analyze_row(c, &rp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "row template not applicable: " + why);
+      ks = lower_row(c, rp, o);
+      break;
+    }
+    case SFX_STRATEGY_COL: {
+      ColPlan cp;
+      if (!analyze_col(c, &cp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "col template not applicable: " + why);
+      ks = lower_col(c, cp);
+      break;
+    }
+    case SFX_STRATEGY_LITERAL:
+      ks = lower_literal(c);
+      if (!why.empty()) ks.note += " (" + why + ")";
+      break;
+    default:
+      throw Error(SFX_ERR_INVALID, "unknown strategy");
+  }
+  return ks;
+}
+
+}  // namespace sfx

@@ -1,0 +1,52 @@
+// Fusion-group -> sm_100a kernel lowering (the subsystem BASELINE.json's
+// north_star says changes: schedule selection per group, launch dimensions,
+// shared-memory allocation across the stitched ops).  Input is one reference
+// KernelProgram (reference proj/include/stitchfuse/kernelgen.hpp:48-54); output
+// is the CUDA source of ONE stitched kernel plus its launch geometry.
+//
+// Strategies (chosen by GroupAnalyzer = analyze_* below):
+//   map     — no reductions: 1-D kLoop over root elements, 128-bit vector
+//             loads/stores, everything thread-composed in registers.
+//   row     — reductions over trailing dims (LayerNorm, softmax): a thread
+//             group per row, row held in registers, warp-shuffle combine,
+//             reduced scalars broadcast back through registers.
+//   col     — reductions over leading dims (bias-grad): column tiles x row
+//             stripes, shared-memory partials, single-launch deterministic
+//             cross-CTA combine (last-CTA ticket), elementwise roots written in
+//             the same pass.
+//   literal — any plan the reference emits: the KernelProgram executed as
+//             written (reference blocks/chunk_box/arena/barriers, reference
+//             fold order) with the arena in shared memory.  Correctness tier.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "ir.hpp"
+
+namespace sfx {
+
+struct KernelSource {
+  std::string strategy;
+  std::string entry;
+  std::string code;          // complete CUDA translation unit (prelude included)
+  int64_t grid_x = 1, grid_y = 1;
+  int block = 256;
+  int smem = 0;              // dynamic shared memory bytes
+  int64_t workspace_bytes = 0;
+  std::vector<int> inputs;   // node ids per input slot (Program::inputs)
+  std::vector<int> outputs;  // node ids per output slot (Program::roots)
+  int64_t algorithmic_bytes = 0;
+  int vector_width = 1;
+  std::string note;          // why this strategy / geometry
+};
+
+KernelSource lower_program(const Graph& g, int program_index, const sfx_compile_opts& opts);
+
+// Strategy the analyzer would pick (without generating code), with the reason
+// the faster templates were rejected.
+std::string choose_strategy(const Graph& g, int program_index, std::string* why);
+
+extern const char* kPrelude;
+
+}  // namespace sfx

@@ -1,0 +1,98 @@
+// Device prelude prepended to every generated stitched kernel (compiled by
+// NVRTC for sm_100a with -fmad=false, IEEE div/sqrt).  Scalar semantics follow
+// the reference's compute_element / apply_unary / apply_binary exactly
+// (reference proj/src/exec.cpp:18-65, 141-204):
+//   max/min are std::max/std::min ((a<b)?b:a, (b<a)?b:a) — NaN handling differs
+//   from fmaxf; compare yields 1/0; select tests pred != 0; scale multiplies in
+//   double; rsqrt is 1/sqrt; i32 arithmetic wraps.
+// Self-contained: no CUDA headers, so NVRTC needs no include path.
+typedef unsigned int sfx_u32;
+typedef unsigned long long sfx_u64;
+
+struct __align__(16) sfx_f4 { float x, y, z, w; };
+struct __align__(16) sfx_i4 { int x, y, z, w; };
+
+// ---- f32 ----
+__device__ __forceinline__ float sfx_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sfx_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float sfx_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float sfx_max(float a, float b) { return (a < b) ? b : a; }
+__device__ __forceinline__ float sfx_min(float a, float b) { return (b < a) ? b : a; }
+__device__ __forceinline__ float sfx_neg(float a) { return -a; }
+__device__ __forceinline__ float sfx_cmp(float a, float b) { return a > b ? 1.0f : 0.0f; }
+__device__ __forceinline__ float sfx_sel(float p, float t, float f) { return p != 0.0f ? t : f; }
+__device__ __forceinline__ float sfx_scale_d(float a, double s) { return (float)((double)a * s); }
+__device__ __forceinline__ float sfx_scale_f(float a, float s) { return __fmul_rn(a, s); }
+__device__ __forceinline__ float sfx_exp(float a) { return expf(a); }
+__device__ __forceinline__ float sfx_log(float a) { return logf(a); }
+__device__ __forceinline__ float sfx_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float sfx_pow(float a, float b) { return powf(a, b); }
+__device__ __forceinline__ float sfx_tanh(float a) { return tanhf(a); }
+__device__ __forceinline__ float sfx_sqrt(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ float sfx_rsqrt(float a) { return __fdiv_rn(1.0f, __fsqrt_rn(a)); }
+
+// ---- i32 (two's-complement wrap, like the reference's x86 build) ----
+__device__ __forceinline__ int sfx_add(int a, int b) { return (int)((sfx_u32)a + (sfx_u32)b); }
+__device__ __forceinline__ int sfx_sub(int a, int b) { return (int)((sfx_u32)a - (sfx_u32)b); }
+__device__ __forceinline__ int sfx_mul(int a, int b) { return (int)((sfx_u32)a * (sfx_u32)b); }
+__device__ __forceinline__ int sfx_max(int a, int b) { return (a < b) ? b : a; }
+__device__ __forceinline__ int sfx_min(int a, int b) { return (b < a) ? b : a; }
+__device__ __forceinline__ int sfx_neg(int a) { return (int)(0u - (sfx_u32)a); }
+__device__ __forceinline__ int sfx_cmp(int a, int b) { return a > b ? 1 : 0; }
+__device__ __forceinline__ int sfx_sel(int p, int t, int f) { return p != 0 ? t : f; }
+// static_cast<int32_t>(x * scalar) on x86-64 (cvttsd2si): out-of-range/NaN -> INT_MIN
+__device__ __forceinline__ int sfx_scale_d(int a, double s) {
+  double p = (double)a * s;
+  if (!(p > -2147483649.0 && p < 2147483648.0)) return (int)0x80000000u;
+  return (int)p;
+}
+
+__device__ __forceinline__ float sfx_bits_f(int a) { return __int_as_float(a); }
+__device__ __forceinline__ int sfx_bits_i(float a) { return __float_as_int(a); }
+
+// ---- reduce folds (reference exec.cpp:67-74: sum = add, max/min = std::max/min) ----
+__device__ __forceinline__ float sfx_fold_sum(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ int sfx_fold_sum(int a, int b) { return sfx_add(a, b); }
+// Parallel max/min: the sequential std::max fold returns the first element if
+// it is NaN, else the max over the non-NaN elements.  Partial folds therefore
+// ignore NaN (fmaxf/fminf semantics) and the first element is re-applied at the end.
+__device__ __forceinline__ float sfx_fold_pmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float sfx_fold_pmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ int sfx_fold_pmax(int a, int b) { return a < b ? b : a; }
+__device__ __forceinline__ int sfx_fold_pmin(int a, int b) { return b < a ? b : a; }
+__device__ __forceinline__ float sfx_fold_first(float first, float acc) { return (first != first) ? first : acc; }
+__device__ __forceinline__ int sfx_fold_first(int first, int acc) { return acc; }
+
+// ---- memory ----
+// Streaming 128-bit loads: read-only path, no L1 allocation (data read once).
+__device__ __forceinline__ sfx_f4 sfx_ld4s(const float* p) {
+  sfx_f4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ sfx_i4 sfx_ld4s(const int* p) {
+  sfx_i4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+// Reused 128-bit loads (broadcast vectors): default caching.
+__device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
+__device__ __forceinline__ sfx_i4 sfx_ld4(const int* p) { return *reinterpret_cast<const sfx_i4*>(p); }
+__device__ __forceinline__ float sfx_ld(const float* p) { return __ldg(p); }
+__device__ __forceinline__ int sfx_ld(const int* p) { return __ldg(p); }
+__device__ __forceinline__ void sfx_st4(float* p, float a, float b, float c, float d) {
+  sfx_f4 v; v.x = a; v.y = b; v.z = c; v.w = d;
+  *reinterpret_cast<sfx_f4*>(p) = v;
+}
+__device__ __forceinline__ void sfx_st4(int* p, int a, int b, int c, int d) {
+  sfx_i4 v; v.x = a; v.y = b; v.z = c; v.w = d;
+  *reinterpret_cast<sfx_i4*>(p) = v;
+}
+
+// ---- cross-thread combine ----
+__device__ __forceinline__ float sfx_shfl_xor(float v, int m, sfx_u32 mask) { return __shfl_xor_sync(mask, v, m); }
+__device__ __forceinline__ int sfx_shfl_xor(int v, int m, sfx_u32 mask) { return __shfl_xor_sync(mask, v, m); }
+__device__ __forceinline__ float sfx_shfl(float v, int src, sfx_u32 mask) { return __shfl_sync(mask, v, src); }
+__device__ __forceinline__ int sfx_shfl(int v, int src, sfx_u32 mask) { return __shfl_sync(mask, v, src); }

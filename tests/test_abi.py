@@ -1,0 +1,147 @@
+"""CPU-side checks of the product boundary: libsfx.so loads without a GPU,
+exports every symbol include/sfx.h declares, rejects what the reference
+rejects, and every committed reference plan lowers to CUDA that NVRTC compiles
+to sm_100a SASS (no GPU needed for that)."""
+
+import os
+import re
+import subprocess
+
+import pytest
+
+import sfx_testlib as T
+from paper_1811_05213_b200 import host as H
+
+HEADER = os.path.join(T.ROOT, "include", "sfx.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:sfx_status|int32_t|int64_t|const char\*)\s+(sfx_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = H.lib()
+    names = declared_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(H.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", H.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (sfx_\w+)", out))
+    assert set(names) <= exported
+    assert L.sfx_abi_version() == 1
+
+
+def test_ctx_create_without_gpu_fails_loudly():
+    import ctypes as C
+    if os.path.exists("/dev/nvidia0"):
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    st = H.lib().sfx_ctx_create(0, C.byref(h))
+    assert st == 4  # SFX_ERR_CUDA
+    assert b"libcuda" in H.lib().sfx_last_error() or b"cuInit" in H.lib().sfx_last_error()
+
+
+WORKLOADS = sorted(f[:-5] for f in os.listdir(T.PLANS) if f.endswith(".json"))
+
+EXPECTED = {  # strategy the GroupAnalyzer must pick at full size
+    ("C1", "y"): "row", ("C2", "y"): "row", ("C3", "db"): "col", ("C3b", "db"): "col",
+    ("C3b", "dx_out"): "map", ("C4", "y"): "map", ("C4b", "y"): "map", ("C5", "ctx_r"): "map",
+    ("C5", "gelu"): "map", ("C5", "h1"): "row", ("C5", "h2"): "row", ("C5", "probs_d"): "row",
+}
+
+
+@pytest.mark.parametrize("wl", WORKLOADS)
+def test_workload_plans_lower_and_compile_for_sm100a(wl):
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, wl + ".json"))
+    name, size = wl.split(".")
+    assert len(rep.kernels) == b["fused_kernels"]
+    for k in rep.kernels:
+        for strategy in ("auto", "literal"):
+            src, cubin, note = H.codegen(g, k.program, strategy)
+            assert os.path.getsize(cubin) > 0
+            assert "extern \"C\" __global__" in src
+            if strategy == "auto" and size == "full":
+                assert note.split()[0] == EXPECTED[(name, k.program.fusion_root)], note
+
+
+def test_full_size_streams_are_128bit():
+    """The map/row/col kernels on the named shapes move HBM data with LDG.E.128 / STG.E.128."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C5.full.json"))
+    for k in rep.kernels:
+        src, cubin, note = H.codegen(g, k.program)
+        sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+        assert re.search(r"LDG\.E(\.\w+)*\.128", sass), k.program.fusion_root
+        assert re.search(r"STG\.E(\.\w+)*\.128", sass), k.program.fusion_root
+
+
+def _eligible(stream, limit=None):
+    d = T.load_json(os.path.join(T.GOLDEN, f"random_{stream}.json"))
+    out = [c for c in d["cases"] if c["device_eligible"]]
+    return out[:limit] if limit else out
+
+
+def test_random_graph_groups_lower_and_compile():
+    """Every group of the device-eligible reference random graphs compiles in both tiers."""
+    n = 0
+    for case in _eligible("pipeline"):
+        g = H.graph_from_json(case["bundle"]["graph"])
+        rep = H.CompileReport.from_bundle(case["bundle"])
+        for k in rep.kernels:
+            for strategy in ("auto", "literal"):
+                H.codegen(g, k.program, strategy)
+                n += 1
+    assert n > 40
+
+
+def test_matmul_group_is_rejected_as_unsupported():
+    """fuse_dot groups contain BatchMatMul: outside the non-MatMul device path."""
+    d = T.load_json(os.path.join(T.GOLDEN, "random_acceptance.json"))
+    for case in d["cases"]:
+        if case["bundle"]["options"]["fuse_dot"]:
+            g = H.graph_from_json(case["bundle"]["graph"])
+            rep = H.CompileReport.from_bundle(case["bundle"])
+            for k in rep.kernels:
+                if any(g.at(m).op == "batch_matmul" for m in k.program.members):
+                    with pytest.raises(H.ExecError) as e:
+                        H.codegen(g, k.program)
+                    assert e.value.status == 2
+                    return
+    pytest.skip("no fused matmul group in the stream")
+
+
+def test_malformed_program_is_rejected():
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C1.small.json"))
+    p = rep.kernels[0].program
+    bad = H.KernelProgram(p.fusion_root, p.members, p.roots, p.blocks, p.block_threads, p.arena_bytes,
+                          [s for s in p.statements if s.get("dest") != "output"])
+    with pytest.raises(H.ExecError) as e:
+        H.codegen(g, bad)
+    assert e.value.status == 1 and "not all roots written" in str(e.value)
+    over = [dict(s) for s in p.statements]
+    for s in over:
+        if s.get("dest") == "shared":
+            s["offset"] = p.arena_bytes
+    with pytest.raises(H.ExecError) as e:
+        H.codegen(g, H.KernelProgram(p.fusion_root, p.members, p.roots, p.blocks, p.block_threads,
+                                     p.arena_bytes, over))
+    assert "arena overflow" in str(e.value)
+
+
+def test_forcing_an_inapplicable_template_fails():
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C3.small.json"))
+    with pytest.raises(H.ExecError) as e:
+        H.codegen(g, rep.kernels[0].program, "row")
+    assert e.value.status == 2
+    with pytest.raises(H.ExecError):
+        H.codegen(g, rep.kernels[0].program, "map")
+
+
+def test_parse_graph_lowers_mean_like_the_reference():
+    from workloads import configs
+    g = H.parse_graph(configs.dumps(configs.c1_layernorm(R=4, C=8)))
+    gb, rep, b = H.load_bundle(os.path.join(T.PLANS, "C1.small.json"))
+    assert [i.id for i in g.instructions] == [i.id for i in gb.instructions]
+    assert g.at("ln.mean").op == "scale" and g.at("ln.mean").scalar == 1.0 / 8
+    assert g.at("ln.mean.sum").op == "reduce"

@@ -1,0 +1,54 @@
+"""Regenerates workloads/plans/*.json: each file is the reference's own
+compile_graph() output ("plan bundle": graph + fusion plan + KernelProgram per
+group) for one BASELINE.json config, exported by oracle/_ref/ref_tool (built
+from /root/reference by oracle/Makefile).  Run in the build container only —
+the reference does not exist on the GPU box; the committed bundles travel.
+
+    python workloads/make_workloads.py
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+
+from workloads import configs  # noqa: E402
+
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+
+
+def plan_bundle(doc: dict) -> dict:
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        f.write(configs.dumps(doc))
+        path = f.name
+    try:
+        out = subprocess.run([REF_TOOL, "plan", path], check=True, capture_output=True, text=True)
+    finally:
+        os.unlink(path)
+    return json.loads(out.stdout)
+
+
+def main():
+    outdir = os.path.join(HERE, "plans")
+    os.makedirs(outdir, exist_ok=True)
+    for size_name, table in (("full", configs.FULL), ("small", configs.SMALL)):
+        for name, sizes in table.items():
+            bundle = plan_bundle(configs.build(name, **sizes))
+            bundle["workload"] = {"name": name, "size": size_name, "sizes": sizes}
+            path = os.path.join(outdir, f"{name}.{size_name}.json")
+            with open(path, "w") as f:
+                json.dump(bundle, f, indent=1)
+                f.write("\n")
+            print(f"{path}: fused={bundle['fused_kernels']} baseline={bundle['baseline_kernels']}"
+                  f" groups={[k['fusion_root'] for k in bundle['kernels']]}")
+
+
+if __name__ == "__main__":
+    main()
