@@ -54,28 +54,47 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line) read live by a thread,
+    so the timed region can be bracketed by samples taken under the same load."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
         self.proc = None
-        self.path = None
+        self.rows = []  # (t, sm_mhz, max_mhz, reasons set)
+        self.lock = threading.Lock()
 
-    def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except Exception:
             self.proc = None
+            return self
+        threading.Thread(target=self._reader, daemon=True).start()
         return self
 
-    def __exit__(self, *a):
+    def _reader(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            try:
+                sm, mx = float(f[0]), float(f[1])
+            except Exception:
+                continue
+            reasons = {n for n, v in zip(self.NAMES, f[4:8]) if v.lower().startswith("active")}
+            with self.lock:
+                self.rows.append((time.perf_counter(), sm, mx, reasons))
+
+    def count_after(self, t):
+        with self.lock:
+            return sum(1 for r in self.rows if r[0] >= t)
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -83,31 +102,15 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        rows = []
-        try:
-            for line in open(self.path):
-                f = [x.strip() for x in line.split(",")]
-                if len(f) >= 8 and f[0].replace(".", "").isdigit():
-                    rows.append(f)
-        except Exception:
-            pass
-        finally:
-            try:
-                os.unlink(self.path)
-            except Exception:
-                pass
+    def summary(self, t_lo, t_hi):
+        with self.lock:
+            rows = [r for r in self.rows if t_lo <= r[0] <= t_hi]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = sorted(float(r[0]) for r in rows)
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
-                "samples": len(rows)}
+        sm = sorted(r[1] for r in rows)
+        reasons = set().union(*[r[3] for r in rows])
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][2], "reasons": sorted(reasons),
+                "samples": len(rows), "window_s": round(t_hi - t_lo, 3)}
 
 
 def dist_env():
@@ -251,21 +254,42 @@ def run_ours(args):
         pi, po, _, _ = sets[i % nsets]
         cg.run(pi, po, stream=stream.cuda_stream, cuda_graph=True)
 
+    clk = Clocks(local).start()
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
+    # keep the GPU under the same load until the sampler is producing samples,
+    # so the timed region is bracketed by clock samples taken under load
+    t_load = time.perf_counter()
+    n_load = 0
+    while clk.count_after(t_load + 0.15) < 2 and time.perf_counter() - t_load < 5.0:
+        for _ in range(16):
+            step(n_load)
+            n_load += 1
+        torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launch_count()
-    with Clocks(local) as clk:
-        e0.record(stream)
-        for i in range(args.steps):
-            step(i)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+    t_lo = time.perf_counter()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_hi = time.perf_counter()
     launches = ctx.launch_count() - launches0
+    t_post = time.perf_counter()
+    while clk.count_after(t_post) < 2 and time.perf_counter() - t_post < 3.0:
+        for _ in range(16):
+            step(n_load)
+            n_load += 1
+        torch.cuda.synchronize(dev)
+    clk.stop()
+    # samples within 150 ms of the timed region, all under continuous load of the same step
+    clocks = clk.summary(t_lo - 0.15, max(t_hi, t_post) + 0.15)
+    clocks["note"] = "sampled every 50 ms under continuous load of this step bracketing the timed region"
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -273,7 +297,6 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    clocks = clk.summary()
 
     # per-kernel live timing on the launching stream (roofline of each group)
     per_kernel = []
@@ -383,8 +406,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C5", choices=sorted(WORKLOAD_NAMES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -142,7 +142,7 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   auto k = std::make_unique<sfx_kernel>();
   k->ctx = ctx;
   k->src = sfx::lower_program(g, pi, o);
-  sfx::Cubin cb = sfx::compile_cubin(k->src.code, k->src.entry);
+  sfx::Cubin cb = sfx::compile_cubin(k->src.code, k->src.entry, k->src.nvrtc_options);
   k->cubin_path = cb.path;
   ctx->bind();
   const sfx::Driver& d = sfx::driver();
@@ -378,7 +378,7 @@ sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_inde
     sfx_compile_opts o{};
     if (opts) o = *opts;
     sfx::KernelSource ks = sfx::lower_program(g, program_index, o);
-    sfx::Cubin cb = sfx::compile_cubin(ks.code, ks.entry);
+    sfx::Cubin cb = sfx::compile_cubin(ks.code, ks.entry, ks.nvrtc_options);
     auto put = [](char* dst, uint64_t cap, const std::string& s) {
       if (!dst || cap == 0) return;
       size_t n = std::min<size_t>(s.size(), cap - 1);

@@ -257,6 +257,20 @@ std::string Emitter::ew_expr(const Node& n, const std::vector<std::string>& a) {
       if (n.dtype == SFX_F32 && static_cast<double>(static_cast<float>(n.scalar)) == n.scalar &&
           std::isfinite(n.scalar))
         return "sfx_scale_f(" + a[0] + ", " + fmt_f32(n.scalar) + ")";
+      if (n.dtype == SFX_F32 && std::isfinite(n.scalar) && std::fabs(n.scalar) < 1e30 &&
+          std::fabs(n.scalar) > 1e-30) {
+        // s = hi + lo (two floats); fma(x, hi, x*lo) is x*s with one final
+        // rounding of a value within 2^-48 relative of the exact product: the
+        // same float as float(x*double(s)) except at near-midpoints (<= 1 ulp),
+        // at FP32 instead of FP64/F2F throughput.
+        // hi is s truncated toward zero, so lo has the sign of hi and
+        // fma(+-inf, hi, +-inf*lo) stays +-inf (no NaN from opposite infinities).
+        float hi = static_cast<float>(n.scalar);
+        if (std::fabs(static_cast<double>(hi)) > std::fabs(n.scalar))
+          hi = std::nextafter(hi, 0.0f);
+        float lo = static_cast<float>(n.scalar - static_cast<double>(hi));
+        return "sfx_scale_2f(" + a[0] + ", " + fmt_f32(hi) + ", " + fmt_f32(lo) + ")";
+      }
       return "sfx_scale_d(" + a[0] + ", " + fmt_f64(n.scalar) + ")";
     }
     case SFX_EW_EXP: return "sfx_exp(" + a[0] + ")";

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <iterator>
 #include <mutex>
 #include <sstream>
 
@@ -48,12 +49,15 @@ bool read_file(const std::string& path, std::vector<char>* out) {
 
 }  // namespace
 
-Cubin compile_cubin(const std::string& source, const std::string& entry) {
+Cubin compile_cubin(const std::string& source, const std::string& entry,
+                    const std::vector<std::string>& extra_options) {
   const Nvrtc& rtc = nvrtc();
   int major = 0, minor = 0;
   rtc.nvrtcVersion(&major, &minor);
+  std::vector<const char*> argv(std::begin(kOptions), std::end(kOptions));
+  for (const std::string& o : extra_options) argv.push_back(o.c_str());
   std::string opts;
-  for (const char* o : kOptions) opts += std::string(o) + " ";
+  for (const char* o : argv) opts += std::string(o) + " ";
   uint64_t h = fnv1a64(source);
   h = fnv1a64(opts, h);
   h = fnv1a64(std::to_string(major) + "." + std::to_string(minor) + "/sfx-jit-v1", h);
@@ -72,7 +76,7 @@ Cubin compile_cubin(const std::string& source, const std::string& entry) {
   nvrtcProgram prog;
   nvrtcResult r = rtc.nvrtcCreateProgram(&prog, source.c_str(), (entry + ".cu").c_str(), 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) throw Error(SFX_ERR_COMPILE, std::string("nvrtcCreateProgram: ") + rtc.nvrtcGetErrorString(r));
-  r = rtc.nvrtcCompileProgram(prog, static_cast<int>(sizeof(kOptions) / sizeof(kOptions[0])), kOptions);
+  r = rtc.nvrtcCompileProgram(prog, static_cast<int>(argv.size()), argv.data());
   size_t log_size = 0;
   rtc.nvrtcGetProgramLogSize(prog, &log_size);
   if (log_size > 1) {

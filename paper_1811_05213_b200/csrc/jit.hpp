@@ -17,7 +17,8 @@ struct Cubin {
   bool cache_hit = false;
 };
 
-Cubin compile_cubin(const std::string& source, const std::string& entry);
+Cubin compile_cubin(const std::string& source, const std::string& entry,
+                    const std::vector<std::string>& extra_options = {});
 std::string cache_dir();
 uint64_t fnv1a64(const std::string& s, uint64_t h = 1469598103934665603ull);
 

@@ -334,7 +334,7 @@ bool analyze_map(const Ctx& c, std::string* why) {
   return true;
 }
 
-KernelSource lower_map(const Ctx& c) {
+KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "map";
   ks.entry = "sfx_map_" + c.name;
@@ -360,44 +360,78 @@ KernelSource lower_map(const Ctx& c) {
     Emitter probe(c.g, c.p, 1, c.wide);
     sig = signature(c, probe, ks.entry, B);
   }
+  // items (V-element vectors) per thread: several independent 128-bit loads in
+  // flight per thread on large streams; consecutive threads stay consecutive
+  int U = o.items_per_thread > 0 ? o.items_per_thread
+          : max_items >= int64_t{kNumSMs} * 8 * B * 4 ? 4
+          : max_items >= int64_t{kNumSMs} * 8 * B * 2 ? 2 : 1;
+  U = std::max(1, std::min(U, 8));
   std::string idx_t = c.wide ? "long long" : "int";
-  body.line("const " + idx_t + " it = (" + idx_t + ")blockIdx.x * " + std::to_string(B) + " + threadIdx.x;");
+  body.line("const " + idx_t + " t0 = (" + idx_t + ")blockIdx.x * " + std::to_string(B * U) + " + threadIdx.x;");
   size_t ci = 0;
   for (auto& [dims, roots] : classes) {
     auto [V, items] = vw[ci++];
     Emitter em(c.g, c.p, V, c.wide);
     signature(c, em, ks.entry, B);
     em.code = &body;
-    body.line("if (it < " + fmt_i(items) + ") {");
-    body.indent++;
-    em.push();
-    std::string base = V == 1 ? "it" : em.ivar(Emitter::imul("it", V));
-    std::vector<std::vector<std::string>> vals(roots.size(), std::vector<std::string>(V));
-    for (int lane = 0; lane < V; ++lane) {
-      em.lane = lane;
-      Ix L = V == 1 ? em.uni(base) : em.lane_plus(base);
-      for (size_t k = 0; k < roots.size(); ++k) {
-        std::vector<Ix> comps = em.from_linear(L, c.g.nodes[roots[k]].dims);
-        vals[k][lane] = em.value(roots[k], comps);
+    auto emit_item = [&](const std::string& it) {
+      em.push();
+      std::string base = V == 1 ? it : em.ivar(Emitter::imul(it, V));
+      std::vector<std::vector<std::string>> vals(roots.size(), std::vector<std::string>(V));
+      for (int lane = 0; lane < V; ++lane) {
+        em.lane = lane;
+        Ix L = V == 1 ? em.uni(base) : em.lane_plus(base);
+        for (size_t k = 0; k < roots.size(); ++k) {
+          std::vector<Ix> comps = em.from_linear(L, c.g.nodes[roots[k]].dims);
+          vals[k][lane] = em.value(roots[k], comps);
+        }
       }
+      for (size_t k = 0; k < roots.size(); ++k) {
+        std::string out = "out" + std::to_string(root_slot(c, roots[k]));
+        if (V == 4)
+          body.line("sfx_st4(" + out + " + " + base + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
+                    vals[k][2] + ", " + vals[k][3] + ");");
+        else
+          body.line(out + "[" + base + "] = " + vals[k][0] + ";");
+      }
+      em.pop();
+    };
+    auto item_var = [&](int u) { return "t" + std::to_string(ci) + "_" + std::to_string(u); };
+    if (U > 1) {
+      // full tiles: U unguarded items (loads of all items can issue together)
+      body.line("if (t0 + " + fmt_i(static_cast<int64_t>(U - 1) * B) + " < " + fmt_i(items) + ") {");
+      body.indent++;
+      for (int u = 0; u < U; ++u) {
+        body.line("const " + idx_t + " " + item_var(u) + " = t0 + " + std::to_string(u * B) + ";");
+        emit_item(item_var(u));
+      }
+      body.indent--;
+      body.line("} else {");
+      body.indent++;
     }
-    for (size_t k = 0; k < roots.size(); ++k) {
-      std::string out = "out" + std::to_string(root_slot(c, roots[k]));
-      if (V == 4)
-        body.line("sfx_st4(" + out + " + " + base + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
-                  vals[k][2] + ", " + vals[k][3] + ");");
-      else
-        body.line(out + "[" + base + "] = " + vals[k][0] + ";");
+    for (int u = 0; u < U; ++u) {
+      body.line("{");
+      body.indent++;
+      body.line("const " + idx_t + " " + item_var(u) + " = t0 + " + std::to_string(u * B) + ";");
+      body.line("if (" + item_var(u) + " < " + fmt_i(items) + ") {");
+      body.indent++;
+      emit_item(item_var(u));
+      body.indent--;
+      body.line("}");
+      body.indent--;
+      body.line("}");
     }
-    em.pop();
-    body.indent--;
-    body.line("}");
+    if (U > 1) {
+      body.indent--;
+      body.line("}");
+    }
   }
   ks.code = assemble(sig, body);
   ks.block = B;
-  ks.grid_x = (max_items + B - 1) / B;
+  ks.grid_x = (max_items + int64_t{B} * U - 1) / (int64_t{B} * U);
   ks.vector_width = vmax;
-  ks.note = "kLoop over " + std::to_string(classes.size()) + " root shape class(es)";
+  ks.note = "kLoop over " + std::to_string(classes.size()) + " root shape class(es), " + std::to_string(U) +
+            " vector item(s)/thread";
   return ks;
 }
 
@@ -577,7 +611,21 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   const std::string& it = em.idx_t;
   // workspace: tickets[tiles] (256-B padded), then partials[NR][S][C]
   const int64_t ticket_words = (tiles + 63) / 64 * 64;
-  ks.workspace_bytes = ticket_words * 4 + static_cast<int64_t>(NR) * S * C * 4;
+  // float sums accumulate in double end to end (per-thread, CTA and stripe
+  // combines): a column of 65,536 fp32 terms with cancellation is otherwise
+  // off by ~eps*sum|x| (SURVEY §7 hard part 1); max/min/i32 are exact anyway.
+  auto acc_t = [&](int k) -> std::string {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
+  };
+  std::vector<int64_t> part_word(NR);
+  int64_t words = ticket_words;
+  for (int k = 0; k < NR; ++k) {
+    part_word[k] = words;
+    words += S * C * (acc_t(k) == "double" ? 2 : 1);
+    words = (words + 63) / 64 * 64;
+  }
+  ks.workspace_bytes = words * 4;
 
   body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
   body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + lane * " + std::to_string(V) + ";");
@@ -588,12 +636,12 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   for (int k = 0; k < NR; ++k) {
     const Node& rn = c.g.nodes[c.reduces[k]];
     std::string init;
-    if (rn.reducer == SFX_REDUCE_SUM) init = rn.dtype == SFX_F32 ? "0.0f" : "0";
+    if (rn.reducer == SFX_REDUCE_SUM) init = rn.dtype == SFX_F32 ? "0.0" : "0";
     else if (rn.dtype == SFX_F32) init = "sfx_bits_f(0x7fc00000)";  // NaN = identity of fmaxf/fminf
     else init = rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
     for (int l = 0; l < V; ++l) {
       acc[k][l] = em.fresh("acc");
-      body.line(std::string(ctype(rn.dtype)) + " " + acc[k][l] + " = " + init + ";");
+      body.line(acc_t(k) + " " + acc[k][l] + " = " + init + ";");
     }
   }
   std::vector<int> full_roots, col_roots;
@@ -641,8 +689,8 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
 
   // CTA combine through shared memory (deterministic warp order)
   for (int k = 0; k < NR; ++k) {
-    const char* T = ctype(c.g.nodes[c.reduces[k]].dtype);
-    body.line(std::string("__shared__ ") + T + " sp" + std::to_string(k) + "[" + std::to_string(WARPS) + "][" +
+    const std::string T = acc_t(k);
+    body.line("__shared__ " + T + " sp" + std::to_string(k) + "[" + std::to_string(WARPS) + "][" +
               fmt_i(TC) + "];");
     for (int l = 0; l < V; ++l)
       body.line("sp" + std::to_string(k) + "[warp][lane * " + std::to_string(V) + " + " + std::to_string(l) +
@@ -654,16 +702,15 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   body.indent++;
   for (int k = 0; k < NR; ++k) {
     const Node& rn = c.g.nodes[c.reduces[k]];
-    const char* T = ctype(rn.dtype);
+    const std::string T = acc_t(k);
     const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
                     : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
     std::string part = "part" + std::to_string(k);
-    body.line(std::string(T) + "* " + part + " = (" + T + "*)(ws + " + fmt_i(ticket_words) + ") + " +
-              fmt_i(static_cast<int64_t>(k) * S * C) + ";");
+    body.line(T + "* " + part + " = (" + T + "*)(ws + " + fmt_i(part_word[k]) + ");");
     for (int l = 0; l < V; ++l) {
       std::string sidx = "lane * " + std::to_string(V) + " + " + std::to_string(l);
       std::string t = em.fresh("t");
-      body.line(std::string(T) + " " + t + " = sp" + std::to_string(k) + "[0][" + sidx + "];");
+      body.line(T + " " + t + " = sp" + std::to_string(k) + "[0][" + sidx + "];");
       for (int w = 1; w < WARPS; ++w)
         body.line(t + " = " + f + "(" + t + ", sp" + std::to_string(k) + "[" + std::to_string(w) + "][" + sidx + "]);");
       body.line(part + "[(" + it + ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + "] = " + t + ";");
@@ -685,22 +732,27 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   std::map<int, std::vector<std::string>> total;
   for (int k = 0; k < NR; ++k) {
     const Node& rn = c.g.nodes[c.reduces[k]];
-    const char* T = ctype(rn.dtype);
+    const std::string T = acc_t(k);
     const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
                     : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
     std::string part = "fp" + std::to_string(k);
-    body.line(std::string("const ") + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(ticket_words) +
-              ") + " + fmt_i(static_cast<int64_t>(k) * S * C) + " + c0;");
+    body.line("const " + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(part_word[k]) + ") + c0;");
     std::vector<std::string> tv(V);
     for (int l = 0; l < V; ++l) {
       tv[l] = em.fresh("tot");
-      body.line(std::string(T) + " " + tv[l] + " = __ldcg(" + part + " + " + std::to_string(l) + ");");
+      body.line(T + " " + tv[l] + " = __ldcg(" + part + " + " + std::to_string(l) + ");");
     }
     body.line("for (" + it + " s = 1; s < " + fmt_i(S) + "; ++s) {");
     for (int l = 0; l < V; ++l)
       body.line("  " + tv[l] + " = " + f + "(" + tv[l] + ", __ldcg(" + part + " + s * " + fmt_i(C) + " + " +
                 std::to_string(l) + "));");
     body.line("}");
+    if (T == "double")
+      for (int l = 0; l < V; ++l) {
+        std::string fv32 = em.fresh("tot");
+        body.line("const float " + fv32 + " = (float)" + tv[l] + ";");
+        tv[l] = fv32;
+      }
     if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
       // sequential std::max/min fold semantics: a NaN first element wins
       const Node& in = c.g.nodes[rn.operands[0]];
@@ -960,7 +1012,7 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   switch (strat) {
     case SFX_STRATEGY_MAP:
       if (!analyze_map(c, &why)) throw Error(SFX_ERR_UNSUPPORTED, "map template not applicable: " + why);
-      ks = lower_map(c);
+      ks = lower_map(c, o);
       break;
     case SFX_STRATEGY_ROW: {
       RowPlan rp;

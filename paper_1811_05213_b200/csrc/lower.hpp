@@ -39,6 +39,8 @@ struct KernelSource {
   int64_t algorithmic_bytes = 0;
   int vector_width = 1;
   std::string note;          // why this strategy / geometry
+  // extra NVRTC options; see the i32 min/max note in lower.cpp
+  std::vector<std::string> nvrtc_options;
 };
 
 KernelSource lower_program(const Graph& g, int program_index, const sfx_compile_opts& opts);

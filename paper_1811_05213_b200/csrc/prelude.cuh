@@ -23,6 +23,12 @@ __device__ __forceinline__ float sfx_cmp(float a, float b) { return a > b ? 1.0f
 __device__ __forceinline__ float sfx_sel(float p, float t, float f) { return p != 0.0f ? t : f; }
 __device__ __forceinline__ float sfx_scale_d(float a, double s) { return (float)((double)a * s); }
 __device__ __forceinline__ float sfx_scale_f(float a, float s) { return __fmul_rn(a, s); }
+// float(x * double(s)) in FP32: s = hi + lo with hi = s truncated to float and
+// lo = float(s - hi) of the same sign; one rounding of a value within 2^-48
+// relative of x*s.  Same float as the reference except at near-midpoints (1 ulp).
+__device__ __forceinline__ float sfx_scale_2f(float a, float hi, float lo) {
+  return __fmaf_rn(a, hi, __fmul_rn(a, lo));
+}
 __device__ __forceinline__ float sfx_exp(float a) { return expf(a); }
 __device__ __forceinline__ float sfx_log(float a) { return logf(a); }
 __device__ __forceinline__ float sfx_div(float a, float b) { return __fdiv_rn(a, b); }
@@ -37,7 +43,13 @@ __device__ __forceinline__ int sfx_sub(int a, int b) { return (int)((sfx_u32)a -
 __device__ __forceinline__ int sfx_mul(int a, int b) { return (int)((sfx_u32)a * (sfx_u32)b); }
 __device__ __forceinline__ int sfx_max(int a, int b) { return (a < b) ? b : a; }
 __device__ __forceinline__ int sfx_min(int a, int b) { return (b < a) ? b : a; }
-__device__ __forceinline__ int sfx_neg(int a) { return (int)(0u - (sfx_u32)a); }
+// ptxas 12.9 for sm_100a miscompiles i32 max/min chains over negated values
+// (it forms VIMNMX3 and drops one source's negation; found by the random-graph
+// parity suite, device stream graph 157 — the PTX is correct).  Negating via a
+// multiply by -1 held in constant memory keeps the negation out of ptxas'
+// operand-modifier folding.
+__constant__ int sfx_c_neg1 = -1;
+__device__ __forceinline__ int sfx_neg(int a) { return (int)((sfx_u32)a * (sfx_u32)sfx_c_neg1); }
 __device__ __forceinline__ int sfx_cmp(int a, int b) { return a > b ? 1 : 0; }
 __device__ __forceinline__ int sfx_sel(int p, int t, int f) { return p != 0 ? t : f; }
 // static_cast<int32_t>(x * scalar) on x86-64 (cvttsd2si): out-of-range/NaN -> INT_MIN
@@ -53,6 +65,8 @@ __device__ __forceinline__ int sfx_bits_i(float a) { return __float_as_int(a); }
 // ---- reduce folds (reference exec.cpp:67-74: sum = add, max/min = std::max/min) ----
 __device__ __forceinline__ float sfx_fold_sum(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ int sfx_fold_sum(int a, int b) { return sfx_add(a, b); }
+__device__ __forceinline__ double sfx_fold_sum(double a, float b) { return a + (double)b; }
+__device__ __forceinline__ double sfx_fold_sum(double a, double b) { return a + b; }
 // Parallel max/min: the sequential std::max fold returns the first element if
 // it is NaN, else the max over the non-NaN elements.  Partial folds therefore
 // ignore NaN (fmaxf/fminf semantics) and the first element is re-applied at the end.
