@@ -178,11 +178,23 @@ void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector
   vals.push_back(k->ws);
   std::vector<void*> args(vals.size());
   for (size_t i = 0; i < vals.size(); ++i) args[i] = &vals[i];
-  sfx::check_cu(sfx::driver().cuLaunchKernel(k->fn, static_cast<unsigned>(k->src.grid_x),
-                                             static_cast<unsigned>(k->src.grid_y), 1,
-                                             static_cast<unsigned>(k->src.block), 1, 1,
-                                             static_cast<unsigned>(k->src.smem), s, args.data(), nullptr),
-                "cuLaunchKernel");
+  // programmatic dependent launch (every generated kernel begins with
+  // griddepcontrol.wait, so stream order is preserved)
+  CUlaunchAttribute attr[1];
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg{};
+  cfg.gridDimX = static_cast<unsigned>(k->src.grid_x);
+  cfg.gridDimY = static_cast<unsigned>(k->src.grid_y);
+  cfg.gridDimZ = 1;
+  cfg.blockDimX = static_cast<unsigned>(k->src.block);
+  cfg.blockDimY = 1;
+  cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = static_cast<unsigned>(k->src.smem);
+  cfg.hStream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  sfx::check_cu(sfx::driver().cuLaunchKernelEx(&cfg, k->fn, args.data(), nullptr), "cuLaunchKernelEx");
   k->ctx->launches.fetch_add(1);
 }
 

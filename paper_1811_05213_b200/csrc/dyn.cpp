@@ -54,6 +54,7 @@ const Driver& driver() {
     SFX_BIND(cuModuleUnload)
     SFX_BIND(cuModuleGetFunction)
     SFX_BIND(cuLaunchKernel)
+    SFX_BIND(cuLaunchKernelEx)
     SFX_BIND(cuFuncGetAttribute)
     SFX_BIND(cuFuncSetAttribute)
     SFX_BIND(cuGetErrorName)

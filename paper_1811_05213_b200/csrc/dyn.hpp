@@ -32,6 +32,7 @@ struct Driver {
   SFX_DRV(cuModuleUnload)
   SFX_DRV(cuModuleGetFunction)
   SFX_DRV(cuLaunchKernel)
+  SFX_DRV(cuLaunchKernelEx)
   SFX_DRV(cuFuncGetAttribute)
   SFX_DRV(cuFuncSetAttribute)
   SFX_DRV(cuGetErrorName)

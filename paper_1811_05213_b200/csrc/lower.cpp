@@ -108,6 +108,11 @@ std::string assemble(const std::string& sig, const Code& body) {
   s += "\n";
   s += sig;
   s += " {\n";
+  // Programmatic dependent launch: the runtime launches this grid while the
+  // previous one drains; wait here until that grid's writes are visible
+  // (full dependency kept), then let the next grid launch early.
+  s += "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  s += "  asm volatile(\"griddepcontrol.launch_dependents;\" :::);\n";
   s += body.text;
   s += "}\n";
   return s;
@@ -472,6 +477,14 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   body.line("const int lr = tid & " + std::to_string(TPR - 1) + ";");
   body.line("const " + it + " row = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + (tid / " +
             std::to_string(TPR) + ");");
+  // small row-invariant operands (bias / gamma / beta vectors) are re-read by
+  // every row of the CTA: pull them into L1 now, under the first loads' latency
+  for (size_t k = 0; k < c.p.inputs.size(); ++k) {
+    const Node& n = c.g.nodes[c.p.inputs[k]];
+    if (n.numel() == R * C || n.numel() * 4 > 64 * 1024) continue;
+    body.line("for (int pf = tid * 32; pf < " + fmt_i(n.numel()) + "; pf += " + std::to_string(threads * 32) +
+              ") sfx_prefetch_l1(in" + std::to_string(k) + " + pf);");
+  }
   body.line("if (row >= " + fmt_i(R) + ") return;");
   if (TPR > 1) {
     if (TPR == 32)
@@ -647,40 +660,60 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   std::vector<int> full_roots, col_roots;
   for (int r : c.p.roots) (c.dep.at(r) || c.g.nodes[r].numel() != R * C ? col_roots : full_roots).push_back(r);
 
+  // one row of this thread's column vector: elementwise roots stored, reduce
+  // operands folded into the per-lane accumulators
+  auto emit_row = [&](const std::string& r) {
+    Ix rix = em.uni(r);
+    std::string rbase = em.ivar(Emitter::imul(r, C));
+    std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+    for (int lane = 0; lane < V; ++lane) {
+      em.lane = lane;
+      Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+      for (size_t k = 0; k < full_roots.size(); ++k)
+        fv[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rix, col));
+      for (int k = 0; k < NR; ++k) {
+        const Node& rn = c.g.nodes[c.reduces[k]];
+        const Node& in = c.g.nodes[rn.operands[0]];
+        std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rix, col));
+        const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                        : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+        body.line(acc[k][lane] + " = " + f + "(" + acc[k][lane] + ", " + v + ");");
+      }
+    }
+    if (!full_roots.empty()) {
+      std::string addr = em.ivar(Emitter::iadd(rbase, "c0"));
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+        if (V == 4)
+          body.line("sfx_st4(" + out + " + " + addr + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
+                    ", " + fv[k][3] + ");");
+        else
+          body.line(out + "[" + addr + "] = " + fv[k][0] + ";");
+      }
+    }
+  };
+  // UR rows per iteration, unguarded, so all their 128-bit loads are in flight
+  // together; then the remainder one row at a time
+  const int UR = 4;
   body.line("if (cok) {");
   body.indent++;
-  body.line("#pragma unroll 4");
-  body.line("for (" + it + " r = r_begin + warp; r < r_end; r += " + std::to_string(WARPS) + ") {");
+  body.line(it + " r = r_begin + warp;");
+  body.line("for (; r + " + std::to_string((UR - 1) * WARPS) + " < r_end; r += " + std::to_string(UR * WARPS) +
+            ") {");
   body.indent++;
   em.push();
-  Ix rix = em.uni("r");
-  std::string rbase = em.ivar(Emitter::imul("r", C));
-  std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
-  for (int lane = 0; lane < V; ++lane) {
-    em.lane = lane;
-    Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
-    for (size_t k = 0; k < full_roots.size(); ++k)
-      fv[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rix, col));
-    for (int k = 0; k < NR; ++k) {
-      const Node& rn = c.g.nodes[c.reduces[k]];
-      const Node& in = c.g.nodes[rn.operands[0]];
-      std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rix, col));
-      const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
-                      : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
-      body.line(acc[k][lane] + " = " + f + "(" + acc[k][lane] + ", " + v + ");");
-    }
+  for (int u = 0; u < UR; ++u) {
+    std::string ru = "r" + std::to_string(u);
+    body.line("const " + it + " " + ru + " = r + " + std::to_string(u * WARPS) + ";");
+    emit_row(ru);
   }
-  if (!full_roots.empty()) {
-    std::string addr = em.ivar(Emitter::iadd(rbase, "c0"));
-    for (size_t k = 0; k < full_roots.size(); ++k) {
-      std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
-      if (V == 4)
-        body.line("sfx_st4(" + out + " + " + addr + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
-                  ", " + fv[k][3] + ");");
-      else
-        body.line(out + "[" + addr + "] = " + fv[k][0] + ";");
-    }
-  }
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.line("for (; r < r_end; r += " + std::to_string(WARPS) + ") {");
+  body.indent++;
+  em.push();
+  emit_row("r");
   em.pop();
   body.indent--;
   body.line("}");

@@ -79,17 +79,24 @@ __device__ __forceinline__ int sfx_fold_first(int first, int acc) { return acc; 
 
 // ---- memory ----
 // Streaming 128-bit loads: read-only path, no L1 allocation (data read once).
+// Not `volatile`: the inputs are read-only for the kernel's lifetime, and the
+// scheduler must be free to hoist the next rows' loads above the current
+// row's arithmetic (memory-level parallelism).
 __device__ __forceinline__ sfx_f4 sfx_ld4s(const float* p) {
   sfx_f4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   return v;
 }
 __device__ __forceinline__ sfx_i4 sfx_ld4s(const int* p) {
   sfx_i4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
+}
+// L1 prefetch of a small read-only operand shared by the CTA's rows.
+__device__ __forceinline__ void sfx_prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
 }
 // Reused 128-bit loads (broadcast vectors): default caching.
 __device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
