@@ -1,0 +1,223 @@
+// See stitchfuse_device.hpp.  Flattens the reference's TensorGraph /
+// KernelProgram (ir.hpp:82-125, kernelgen.hpp:25-54) into the C-ABI
+// descriptors of include/sfx.h and drives libsfx.so.
+#include "stitchfuse_device.hpp"
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <variant>
+
+#include "sfx.h"
+
+namespace stitchfuse_device {
+
+using namespace stitchfuse;
+
+namespace {
+
+void check(sfx_status st) {
+  if (st != SFX_OK) throw ExecError(std::string("device executor: ") + sfx_last_error());
+}
+
+sfx_ctx* context() {
+  static sfx_ctx* ctx = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* d = std::getenv("SFX_DEVICE");
+    check(sfx_ctx_create(d ? std::atoi(d) : 0, &ctx));
+  });
+  return ctx;
+}
+
+// Owns every array the descriptor points into.
+struct Desc {
+  std::vector<sfx_instr> instrs;
+  std::vector<std::vector<double>> literals;
+  std::vector<int32_t> outputs;
+  std::vector<std::vector<int32_t>> members, roots;
+  std::vector<std::vector<sfx_stmt>> stmts;
+  std::vector<sfx_program> programs;
+  std::map<InstrId, int32_t> index;
+  sfx_graph_desc desc{};
+
+  Desc(const TensorGraph& g, const std::vector<const KernelProgram*>& progs) {
+    const auto& ins = g.instructions();
+    for (size_t i = 0; i < ins.size(); ++i) index[ins[i].id] = static_cast<int32_t>(i);
+    instrs.resize(ins.size());
+    literals.resize(ins.size());
+    for (size_t i = 0; i < ins.size(); ++i) {
+      const Instruction& in = ins[i];
+      sfx_instr& s = instrs[i];
+      std::memset(&s, 0, sizeof s);
+      s.id = in.id.c_str();
+      s.opcode = static_cast<int32_t>(in.opcode);  // same enumerator order (ir.hpp:41-52)
+      s.kind = static_cast<int32_t>(in.kind);      // ir.hpp:54-73
+      s.dtype = in.shape.etype == ElementType::F32 ? SFX_F32 : SFX_I32;
+      if (in.shape.rank() > SFX_MAX_RANK) throw ExecError("rank above SFX_MAX_RANK: " + in.id);
+      s.rank = static_cast<int32_t>(in.shape.rank());
+      for (int d = 0; d < s.rank; ++d) s.dims[d] = in.shape.dims[d];
+      s.n_operands = static_cast<int32_t>(in.operands.size());
+      for (int k = 0; k < s.n_operands && k < 3; ++k) s.operands[k] = index.at(in.operands[k]);
+      for (size_t k = 0; k < in.permutation.size(); ++k) s.permutation[k] = in.permutation[k];
+      s.n_dim_map = static_cast<int32_t>(in.broadcast_dim_map.size());
+      for (size_t k = 0; k < in.broadcast_dim_map.size(); ++k) s.broadcast_dim_map[k] = in.broadcast_dim_map[k];
+      s.n_reduce_dims = static_cast<int32_t>(in.reduce_dims.size());
+      for (size_t k = 0; k < in.reduce_dims.size(); ++k) s.reduce_dims[k] = in.reduce_dims[k];
+      s.reducer = static_cast<int32_t>(in.reducer);  // Sum, Max, Min (ir.hpp:75)
+      s.scalar = in.scalar;
+      literals[i] = in.literal;
+      s.n_literal = static_cast<int64_t>(literals[i].size());
+      s.literal = literals[i].empty() ? nullptr : literals[i].data();
+    }
+    for (const InstrId& o : g.outputs()) outputs.push_back(index.at(o));
+    for (const KernelProgram* p : progs) {
+      members.emplace_back();
+      for (const InstrId& m : p->comp.members) members.back().push_back(index.at(m));
+      roots.emplace_back();
+      for (const InstrId& r : p->comp.roots) roots.back().push_back(index.at(r));
+      stmts.emplace_back();
+      for (const Statement& st : p->statements) {
+        sfx_stmt t;
+        std::memset(&t, 0, sizeof t);
+        if (const auto* m = std::get_if<MaterializeStmt>(&st)) {
+          t.kind = SFX_STMT_MATERIALIZE;
+          t.instr = index.at(m->instr);
+          t.split_dim = m->schedule.split_dim;
+          t.sword = m->schedule.sword;
+          t.sched_type = m->schedule.type == SchedType::Row ? SFX_SCHED_ROW : SFX_SCHED_COL;
+          if (const auto* sh = std::get_if<SharedDest>(&m->dest)) {
+            t.dest = SFX_DEST_SHARED;
+            t.offset = sh->offset;
+            t.bytes = sh->bytes;
+          } else {
+            t.dest = SFX_DEST_OUTPUT;
+            t.root_index = std::get<OutputDest>(m->dest).root_index;
+          }
+        } else if (std::holds_alternative<BarrierStmt>(st)) {
+          t.kind = SFX_STMT_BARRIER;
+        } else {
+          t.kind = SFX_STMT_INLINE;
+          t.instr = index.at(std::get<InlineBindingStmt>(st).instr);
+        }
+        stmts.back().push_back(t);
+      }
+    }
+    for (size_t k = 0; k < progs.size(); ++k) {
+      const KernelProgram* p = progs[k];
+      sfx_program sp;
+      std::memset(&sp, 0, sizeof sp);
+      sp.n_members = static_cast<int32_t>(members[k].size());
+      sp.members = members[k].data();
+      sp.n_roots = static_cast<int32_t>(roots[k].size());
+      sp.roots = roots[k].data();
+      sp.fusion_root = index.count(p->comp.fusion_root) ? index.at(p->comp.fusion_root) : -1;
+      sp.blocks = p->plan.blocks;
+      sp.block_threads = p->plan.block_threads;
+      sp.arena_bytes = p->arena_bytes;
+      sp.n_stmts = static_cast<int32_t>(stmts[k].size());
+      sp.stmts = stmts[k].data();
+      programs.push_back(sp);
+    }
+    desc.n_instrs = static_cast<int32_t>(instrs.size());
+    desc.instrs = instrs.data();
+    desc.n_outputs = static_cast<int32_t>(outputs.size());
+    desc.outputs = outputs.data();
+    desc.n_programs = static_cast<int32_t>(programs.size());
+    desc.programs = programs.data();
+  }
+};
+
+const void* host_data(const TensorValue& v) {
+  return v.shape.etype == ElementType::F32 ? static_cast<const void*>(v.f32.data())
+                                           : static_cast<const void*>(v.i32.data());
+}
+void* host_data(TensorValue& v) {
+  return v.shape.etype == ElementType::F32 ? static_cast<void*>(v.f32.data()) : static_cast<void*>(v.i32.data());
+}
+
+sfx_compile_opts g_opts{};
+
+}  // namespace
+
+long long launches() { return sfx_launch_count(context()); }
+void set_strategy(int sfx_strategy) { g_opts.strategy = sfx_strategy; }
+
+std::vector<TensorValue> run_program(const KernelProgram& program, const TensorGraph& graph,
+                                     const std::map<InstrId, TensorValue>& externals) {
+  sfx_ctx* ctx = context();
+  Desc d(graph, {&program});
+  sfx_kernel* k = nullptr;
+  check(sfx_program_compile(ctx, &d.desc, 0, &g_opts, &k));
+  std::unique_ptr<sfx_kernel, decltype(&sfx_kernel_destroy)> guard(k, &sfx_kernel_destroy);
+  sfx_kernel_info info;
+  check(sfx_kernel_get_info(k, &info));
+  std::vector<int32_t> slots(info.n_inputs);
+  check(sfx_kernel_input_instrs(k, slots.data(), info.n_inputs));
+  std::vector<uint64_t> in, out;
+  auto free_all = [&] {
+    for (uint64_t p : in) sfx_free(ctx, p);
+    for (uint64_t p : out) sfx_free(ctx, p);
+  };
+  try {
+    for (int32_t s : slots) {
+      const InstrId& id = graph.instructions()[s].id;
+      auto it = externals.find(id);
+      if (it == externals.end()) throw ExecError("missing external value " + id);
+      uint64_t p = 0;
+      uint64_t bytes = static_cast<uint64_t>(it->second.shape.byte_size());
+      check(sfx_alloc(ctx, bytes, &p));
+      in.push_back(p);
+      check(sfx_memcpy_h2d(ctx, p, host_data(it->second), bytes, nullptr));
+    }
+    std::vector<TensorValue> res;
+    for (const InstrId& r : program.comp.roots) {
+      res.push_back(TensorValue::zeros(graph.at(r).shape));
+      uint64_t p = 0;
+      check(sfx_alloc(ctx, static_cast<uint64_t>(graph.at(r).shape.byte_size()), &p));
+      out.push_back(p);
+    }
+    check(sfx_program_launch(k, in.data(), static_cast<int32_t>(in.size()), out.data(),
+                             static_cast<int32_t>(out.size()), nullptr));
+    for (size_t i = 0; i < res.size(); ++i)
+      check(sfx_memcpy_d2h(ctx, host_data(res[i]), out[i], static_cast<uint64_t>(res[i].shape.byte_size()), nullptr));
+    check(sfx_stream_sync(ctx, nullptr));
+    free_all();
+    return res;
+  } catch (...) {
+    free_all();
+    throw;
+  }
+}
+
+std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const TensorGraph& graph,
+                                            const std::map<InstrId, TensorValue>& inputs) {
+  sfx_ctx* ctx = context();
+  std::vector<const KernelProgram*> progs;
+  for (const CompiledKernel& k : report.kernels) progs.push_back(&k.program);
+  Desc d(graph, progs);
+  sfx_graph* g = nullptr;
+  check(sfx_graph_compile(ctx, &d.desc, &g_opts, &g));
+  std::unique_ptr<sfx_graph, decltype(&sfx_graph_destroy)> guard(g, &sfx_graph_destroy);
+  int32_t n = 0;
+  std::vector<int32_t> params(graph.instructions().size());
+  check(sfx_graph_param_instrs(g, params.data(), static_cast<int32_t>(params.size()), &n));
+  std::vector<const void*> pin;
+  for (int32_t i = 0; i < n; ++i) {
+    const InstrId& id = graph.instructions()[params[i]].id;
+    auto it = inputs.find(id);
+    if (it == inputs.end()) throw ExecError("missing input for parameter " + id);
+    if (it->second.shape != graph.at(id).shape) throw ExecError("input shape mismatch for " + id);
+    pin.push_back(host_data(it->second));
+  }
+  std::map<InstrId, TensorValue> values;
+  std::vector<void*> pout;
+  for (const InstrId& o : graph.outputs()) values[o] = TensorValue::zeros(graph.at(o).shape);
+  for (const InstrId& o : graph.outputs()) pout.push_back(host_data(values[o]));
+  check(sfx_graph_run_host(g, pin.data(), n, pout.data(), static_cast<int32_t>(pout.size()), nullptr));
+  return values;
+}
+
+}  // namespace stitchfuse_device

@@ -1,0 +1,210 @@
+// TEST INFRASTRUCTURE — the reference's own executor tests, replayed through
+// the device executor via the reference-side binding (integration/).
+// Everything here is reference code or reference types: random graphs from
+// tests/support.cpp:168-284, inputs from random_inputs (:286-298), plans from
+// compile_graph / resolve_schedule / plan_shared_memory / emit_program, the
+// oracle is the reference's interpret, the check is the reference's
+// values_close(…, 1e-5) (:300-316).
+//
+//   device_parity random <seed> <count> [--fuse-dot-alternate] [--literal]
+//        test_pipeline.cpp:106-123 / test_acceptance.cpp:41-62 (criterion 2)
+//   device_parity schedules [--literal]
+//        test_exec.cpp:108-137: every satisfiable root schedule of the
+//        device-eligible fixtures runs and equals interpret
+//   device_parity shrink [--literal]
+//        test_exec.cpp:139-155: lowered smem limits (shrunk plans) keep outputs
+// Prints one JSON line; exit 0 iff every eligible case passed.
+#include <cstring>
+#include <iostream>
+#include <random>
+#include <sstream>
+
+#include "../../integration/stitchfuse_device.hpp"
+#include "json.hpp"
+#include "sfx.h"
+#include "stitchfuse/fixtures.hpp"
+#include "stitchfuse/pipeline.hpp"
+#include "support.hpp"
+
+using namespace stitchfuse;
+using json = nlohmann::json;
+
+namespace {
+
+bool eligible(const TensorGraph& g) {
+  for (const Instruction& i : g.instructions())
+    if (i.opcode == Opcode::BatchMatMul || i.opcode == Opcode::LibraryCall) return false;
+  return true;
+}
+
+struct Tally {
+  int cases = 0, passed = 0;
+  json failures = json::array();
+  void fail(const std::string& what) {
+    if (failures.size() < 20) failures.push_back(what);
+  }
+};
+
+bool compare(const TensorGraph& g, const std::map<InstrId, TensorValue>& ref,
+             const std::map<InstrId, TensorValue>& dev, std::string* why) {
+  for (const InstrId& o : g.outputs())
+    if (!testsupport::values_close(dev.at(o), ref.at(o), 1e-5)) {
+      *why = "output " + o;
+      return false;
+    }
+  return true;
+}
+
+void run_case(const std::string& name, const TensorGraph& g, const CompileReport& report,
+              const std::map<InstrId, TensorValue>& inputs, Tally& t) {
+  ++t.cases;
+  try {
+    auto ref = interpret(g, inputs);
+    long long before = stitchfuse_device::launches();
+    auto dev = stitchfuse_device::run_compiled(report, g, inputs);
+    long long launched = stitchfuse_device::launches() - before;
+    std::string why;
+    if (launched != static_cast<long long>(report.kernels.size())) {
+      t.fail(name + ": launched " + std::to_string(launched) + " kernels for " +
+             std::to_string(report.kernels.size()) + " fused groups");
+    } else if (!compare(g, ref, dev, &why)) {
+      t.fail(name + ": " + why);
+    } else {
+      ++t.passed;
+    }
+  } catch (const std::exception& e) {
+    t.fail(name + ": " + e.what());
+  }
+}
+
+int finish(const std::string& mode, const Tally& t, int extra_skipped) {
+  json line = {{"mode", mode}, {"cases", t.cases}, {"passed", t.passed}, {"skipped_ineligible", extra_skipped},
+               {"failures", t.failures}};
+  std::cout << line.dump() << std::endl;
+  return t.cases > 0 && t.passed == t.cases ? 0 : 1;
+}
+
+int cmd_random(uint64_t seed, int count, bool alternate) {
+  std::mt19937_64 rng(seed);
+  testsupport::RandomGraphConfig cfg;
+  Tally t;
+  int skipped = 0;
+  for (int i = 0; i < count; ++i) {
+    TensorGraph g = testsupport::random_graph(rng, cfg);
+    PipelineOptions o;
+    o.fuse_dot = alternate && (i % 2 == 0);  // test_acceptance.cpp:48, test_pipeline.cpp:111
+    PerfLibrary lib;
+    CostModelParams params;
+    CompileReport report = compile_graph(g, o, lib, params);
+    auto inputs = testsupport::random_inputs(g, rng);  // same rng stream as test_acceptance.cpp:50-53
+    if (!eligible(g)) {
+      ++skipped;
+      continue;
+    }
+    run_case("graph " + std::to_string(i), g, report, inputs, t);
+  }
+  return finish("random seed " + std::to_string(seed), t, skipped);
+}
+
+int cmd_schedules() {
+  Tally t;
+  int skipped = 0;
+  for (const auto& [name, text] : fixture_graphs()) {
+    TensorGraph g = parse_graph(text);
+    if (!eligible(g)) {
+      ++skipped;
+      continue;
+    }
+    PipelineOptions options;
+    SpanMap sm = compute_span(g);
+    FusionPlan fusion = fuse_module(g, options);
+    std::mt19937_64 rng(101);
+    auto inputs = testsupport::random_inputs(g, rng);
+    auto reference = interpret(g, inputs);
+    for (const FusedComputation& comp : fusion.computations) {
+      if (comp.roots.size() != 1) continue;
+      const InstrId& root = comp.roots[0];
+      for (const Schedule& sched : enumerate_schedules(g.at(root).shape)) {
+        ResolveResult r = resolve_schedule(comp, g, {{root, sched}}, options);
+        if (!r.ok()) continue;
+        SmemResult smem = plan_shared_memory(comp, g, sm, *r.plan, options);
+        if (!std::holds_alternative<SharedMemPlan>(smem)) continue;
+        KernelProgram program = emit_program(comp, g, sm, *r.plan, std::get<SharedMemPlan>(smem), options);
+        if (check_program(program, g)) continue;
+        std::map<InstrId, TensorValue> externals;
+        for (const InstrId& id : comp.members)
+          for (const InstrId& op : g.at(id).operands)
+            if (!comp.members.count(op)) externals[op] = reference.at(op);
+        ++t.cases;
+        std::string label = name + " " + root + " " + to_string(sched);
+        try {
+          auto outs = stitchfuse_device::run_program(program, g, externals);
+          bool ok = true;
+          for (size_t k = 0; k < comp.roots.size(); ++k)
+            ok = ok && testsupport::values_close(outs[k], reference.at(comp.roots[k]), 1e-5);
+          if (ok) ++t.passed;
+          else t.fail(label);
+        } catch (const std::exception& e) {
+          t.fail(label + ": " + e.what());
+        }
+      }
+    }
+  }
+  return finish("schedules", t, skipped);
+}
+
+int cmd_shrink(uint64_t seed, int count) {
+  Tally t;
+  int skipped = 0;
+  std::mt19937_64 rng(seed);
+  testsupport::RandomGraphConfig cfg;
+  cfg.allow_library_calls = false;
+  std::vector<std::pair<std::string, TensorGraph>> graphs;
+  for (const auto& [name, text] : fixture_graphs()) graphs.push_back({name, parse_graph(text)});
+  for (int i = 0; i < count; ++i) graphs.push_back({"random " + std::to_string(i), testsupport::random_graph(rng, cfg)});
+  for (const auto& [name, g] : graphs) {
+    if (!eligible(g)) {
+      ++skipped;
+      continue;
+    }
+    std::mt19937_64 irng(103);
+    auto inputs = testsupport::random_inputs(g, irng);
+    for (int64_t limit : {20480, 1024, 256}) {
+      PipelineOptions options;
+      options.smem_limit = limit;
+      PerfLibrary lib;
+      CostModelParams params;
+      CompileReport report;
+      try {
+        report = compile_graph(g, options, lib, params);
+      } catch (const std::exception&) {
+        continue;  // planner cannot meet this limit
+      }
+      run_case(name + " smem_limit " + std::to_string(limit), g, report, inputs, t);
+    }
+  }
+  return finish("shrink", t, skipped);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  try {
+    if (argc < 2) throw std::runtime_error("usage: device_parity random|schedules|shrink ...");
+    std::vector<std::string> pos;
+    bool alt = false;
+    for (int i = 1; i < argc; ++i) {
+      if (!std::strcmp(argv[i], "--literal")) stitchfuse_device::set_strategy(SFX_STRATEGY_LITERAL);
+      else if (!std::strcmp(argv[i], "--fuse-dot-alternate")) alt = true;
+      else pos.push_back(argv[i]);
+    }
+    std::string cmd = pos.at(0);
+    if (cmd == "random") return cmd_random(std::stoull(pos.at(1)), std::stoi(pos.at(2)), alt);
+    if (cmd == "schedules") return cmd_schedules();
+    if (cmd == "shrink") return cmd_shrink(pos.size() > 1 ? std::stoull(pos[1]) : 7, pos.size() > 2 ? std::stoi(pos[2]) : 30);
+    throw std::runtime_error("unknown command " + cmd);
+  } catch (const std::exception& e) {
+    std::cerr << "device_parity error: " << e.what() << "\n";
+    return 2;
+  }
+}

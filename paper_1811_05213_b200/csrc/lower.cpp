@@ -477,14 +477,6 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   body.line("const int lr = tid & " + std::to_string(TPR - 1) + ";");
   body.line("const " + it + " row = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + (tid / " +
             std::to_string(TPR) + ");");
-  // small row-invariant operands (bias / gamma / beta vectors) are re-read by
-  // every row of the CTA: pull them into L1 now, under the first loads' latency
-  for (size_t k = 0; k < c.p.inputs.size(); ++k) {
-    const Node& n = c.g.nodes[c.p.inputs[k]];
-    if (n.numel() == R * C || n.numel() * 4 > 64 * 1024) continue;
-    body.line("for (int pf = tid * 32; pf < " + fmt_i(n.numel()) + "; pf += " + std::to_string(threads * 32) +
-              ") sfx_prefetch_l1(in" + std::to_string(k) + " + pf);");
-  }
   body.line("if (row >= " + fmt_i(R) + ") return;");
   if (TPR > 1) {
     if (TPR == 32)

@@ -458,6 +458,20 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().sfx_launch_count(self.h))
 
+    # ---- batch-crossing column reductions across GPUs (NCCL) ----
+    def nccl_init(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().sfx_nccl_init(self.h, buf, nranks, rank))
+
+    def allreduce_sum_f32(self, dptr: int, count: int, stream=0):
+        _check(lib().sfx_allreduce_sum_f32(self.h, int(dptr), int(count), C.c_void_p(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().sfx_nccl_unique_id(buf))
+    return buf.raw
+
 
 _default_ctx = None
 

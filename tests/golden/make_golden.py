@@ -37,7 +37,7 @@ import sfx_testlib as T  # noqa: E402
 
 STREAMS = [
     ("acceptance", 20000, 200, ["--fuse-dot-alternate"]),
-    ("pipeline", 113, 40, []),
+    ("pipeline", 113, 40, ["--fuse-dot-alternate"]),
     ("device", 4242, 200, ["--no-libcalls"]),
 ]
 

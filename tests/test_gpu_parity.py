@@ -172,3 +172,25 @@ def test_column_reduce_is_deterministic_and_relaunchable(ctx):
     for _ in range(3):
         assert np.array_equal(cg.run_host(inputs)["db"], a)
     cg.close()
+
+
+DEVICE_PARITY = os.path.join(T.ROOT, "oracle", "_ref", "device_parity")
+
+
+@pytest.mark.skipif(not os.path.exists(DEVICE_PARITY), reason="reference harness not built (needs /root/reference at build time)")
+@pytest.mark.parametrize("args", [
+    ["random", "20000", "200", "--fuse-dot-alternate"],          # acceptance criterion 2
+    ["random", "113", "40", "--fuse-dot-alternate"],             # test_pipeline.cpp:106-123
+    ["random", "113", "40", "--fuse-dot-alternate", "--literal"],
+    ["schedules"], ["schedules", "--literal"],                  # test_exec.cpp:108-137
+    ["shrink"],                                                  # test_exec.cpp:139-155
+])
+def test_reference_suites_through_device_binding(args):
+    """The reference's own test loops (its random graphs, its inputs, its
+    compile_graph, its interpret and values_close), with run_compiled /
+    run_program swapped for the device executor through integration/."""
+    import json
+    import subprocess
+    r = subprocess.run([DEVICE_PARITY] + args, capture_output=True, text=True, timeout=1200)
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.returncode == 0 and line["passed"] == line["cases"] > 0, line
