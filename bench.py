@@ -264,15 +264,47 @@ def run_ours(args):
         dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0], ws, rank)
 
+    # independent graph instances in flight on separate streams (SURVEY §7
+    # hard part 5): small graphs otherwise expose launch/ramp/tail latency.
+    # Concurrent instances always use distinct buffer sets; kernels that own a
+    # workspace (cross-CTA column combine) run one instance at a time.
+    has_ws = any(k["workspace_bytes"] > 0 for k in kinfo)
+    inflight = args.inflight if args.inflight > 0 else (1 if per_set > (512 << 20) or has_ws else 4)
+    if has_ws:
+        inflight = 1
+    inflight = max(1, min(inflight, nsets if nsets > 1 else 1))
+    while len(sets) < inflight:  # never share a buffer set between concurrent instances
+        ins = [torch.rand(g.at(p).shape, generator=gen, device=dev, dtype=torch.float32) * 2 - 1
+               for p in cg.param_ids]
+        outs = [torch.empty(g.at(o).shape, device=dev, dtype=torch.float32) for o in g.outputs]
+        sets.append(([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], ins, outs))
+    nsets = len(sets)
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(inflight - 1)]
+
     def step(i):
+        s = streams[i % inflight]
         pi, po, _, outs = sets[i % nsets]
-        cg.run(pi, po, stream=stream.cuda_stream, cuda_graph=True)
+        cg.run(pi, po, stream=s.cuda_stream, cuda_graph=True)
         for oi in colsum_outputs:
-            ctx.allreduce_sum_f32(po[oi], outs[oi].numel(), stream.cuda_stream)
+            ctx.allreduce_sum_f32(po[oi], outs[oi].numel(), s.cuda_stream)
+
+    def fork():
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        for s in streams[1:]:
+            s.wait_event(ev)
+
+    def join():
+        for s in streams[1:]:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            stream.wait_event(ev)
 
     clk = Clocks(local).start()
+    fork()
     for i in range(args.warmup):
         step(i)
+    join()
     torch.cuda.synchronize(dev)
     # keep the GPU under the same load until the sampler is producing samples,
     # so the timed region is bracketed by clock samples taken under load
@@ -290,8 +322,10 @@ def run_ours(args):
     launches0 = ctx.launch_count()
     t_lo = time.perf_counter()
     e0.record(stream)
+    fork()
     for i in range(args.steps):
         step(i)
+    join()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     t_hi = time.perf_counter()
@@ -404,7 +438,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand U(-1,1) inputs resident in HBM)",
         "config": dict(config_obj(args.config, ws), **{
             "l2_policy": f"{nsets} rotating input/output set(s) of {per_set / 1e6:.1f} MB (> L2 {l2 / 1e6:.0f} MB)",
-            "groups": n_kernels, "launches_per_graph": n_kernels}),
+            "groups": n_kernels, "launches_per_graph": n_kernels,
+            "instances_in_flight": inflight}),
         "pct_of_peak": 100.0 * value / ws / peak,
         "peak_gbs": peak, "peak_kind": peak_kind,
         "kernel_launches_per_graph": n_kernels,
@@ -434,6 +469,8 @@ def main():
     ap.add_argument("--config", default="C5", choices=sorted(WORKLOAD_NAMES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--inflight", type=int, default=0,
+                    help="independent graph instances in flight per GPU (0 = auto)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -207,6 +207,32 @@ std::string Emitter::load(int node, const std::vector<Ix>& comps) {
   if (pit == input_ptr.end()) throw Error(SFX_ERR_EXEC, "missing external value " + n.id);
   const std::string& ptr = pit->second;
   Ix L = linearize(comps, n.dims);
+  auto st = staged.find(node);
+  if (st != staged.end()) {  // row staged in shared memory by the TMA pipeline
+    const std::string& sp = st->second.first;
+    const std::string& rb = st->second.second;
+    if (L.kind == IX_PLUS && V == 4) {
+      std::string key = "sld4:" + sp + ":" + L.base;
+      std::string q = find(key);
+      if (q.empty()) {
+        q = fresh("q");
+        code->line("const sfx_f4 " + q + " = sfx_lds4(" + sp + " + (" + L.base + " - " + rb + "));");
+        bind(key, q);
+        ++loads_vec;
+      }
+      static const char* xyzw[] = {".x", ".y", ".z", ".w"};
+      return q + xyzw[lane];
+    }
+    std::string key = "sld:" + sp + ":" + L.e;
+    std::string v = find(key);
+    if (v.empty()) {
+      v = fresh("v");
+      code->line("const float " + v + " = " + sp + "[" + L.e + " - " + rb + "];");
+      bind(key, v);
+      ++loads_scalar;
+    }
+    return v;
+  }
   if (L.kind == IX_PLUS && V == 4) {
     std::string key = "ld4:" + ptr + ":" + L.base;
     std::string q = find(key);

@@ -58,6 +58,9 @@ class Emitter {
   Code* code = nullptr;
   std::map<int, std::string> input_ptr;  // external node -> kernel parameter
   std::set<int> streaming;               // externals read once (no-L1-allocate loads)
+  // externals staged in shared memory for the current row: node ->
+  // (const float* smem pointer variable, linear index of the row's first element)
+  std::map<int, std::pair<std::string, std::string>> staged;
   // Strategy hook for member nodes: return a variable name to use instead of
   // evaluating the member's op, or "" to evaluate it inline.
   std::function<std::string(int node, const std::vector<Ix>& comps)> resolve;

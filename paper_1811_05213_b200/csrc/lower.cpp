@@ -442,6 +442,8 @@ KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
 
 // ---- ROW ------------------------------------------------------------------------
 
+void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH);
+
 KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "row";
@@ -486,9 +488,27 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
                 std::to_string(32 - TPR) + ");");
     body.line("const int gleader = (tid & 31) & " + std::to_string(32 - TPR) + ";");
   }
+  emit_row_body(c, rp, em, body, TPR, V, NCH);
+  ks.code = assemble(sig, body);
+  ks.block = threads;
+  ks.grid_x = (R + RPC - 1) / RPC;
+  ks.vector_width = V;
+  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " threads/row=" +
+            std::to_string(TPR) + " elems/thread=" + std::to_string(NCH * V) + " levels=" +
+            std::to_string(rp.max_level);
+  return ks;
+}
+
+// The row body shared by the register-resident and the TMA-pipelined row
+// templates: reduction phases (per-thread fold -> shuffle tree -> broadcast
+// back through registers) then the element and row roots.  Expects `row`,
+// `lr` (lane within the row group), `gmask`, `gleader` in scope.
+void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH) {
+  const int64_t R = rp.R, C = rp.C;
+  const std::string& it = em.idx_t;
   std::vector<std::string> cb(NCH);
   for (int64_t j = 0; j < NCH; ++j) {
-    cb[j] = "cb" + std::to_string(j);
+    cb[j] = em.fresh("cb");
     body.line("const " + it + " " + cb[j] + " = lr * " + std::to_string(V) + " + " +
               fmt_i(j * TPR * V) + ";");
   }
@@ -581,13 +601,148 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
     body.indent--;
     body.line("}");
   }
+}
+
+// External inputs of the row space ([R, C] elements) that are only ever read
+// at the current row — safe to stream row by row into shared memory.  An
+// operand is row-local when every path to it from a root or a reduction goes
+// through row-preserving edges (elementwise, reshape/bitcast, reduce over the
+// row, broadcast of a row scalar, reshape-like broadcast/transpose, transpose
+// permuting columns only).
+std::set<int> row_local_inputs(const Ctx& c, const RowPlan& rp) {
+  const Graph& g = c.g;
+  const int64_t R = rp.R, C = rp.C;
+  std::set<int> local, unsafe;
+  std::function<void(int, bool)> walk = [&](int n, bool ok) {
+    if (!c.p.is_member(n)) {
+      (ok ? local : unsafe).insert(n);
+      return;
+    }
+    const Node& m = g.nodes[n];
+    for (int o : m.operands) {
+      bool edge = true;
+      switch (m.op) {
+        case SFX_OP_ELEMENTWISE: case SFX_OP_RESHAPE: case SFX_OP_BITCAST: case SFX_OP_REDUCE:
+          break;
+        case SFX_OP_BROADCAST: {
+          bool prefix = g.nodes[o].numel() == R;
+          for (size_t j = 0; prefix && j < m.dim_map.size(); ++j)
+            if (m.dim_map[j] != static_cast<int64_t>(j)) prefix = false;
+          edge = bcast_is_reshape(m) || prefix;
+          break;
+        }
+        case SFX_OP_TRANSPOSE: {
+          int k = prefix_split(m.dims, R);
+          edge = transpose_is_reshape(m);
+          if (!edge && k >= 0 && prod(m.dims, k, m.dims.size()) == C) {
+            edge = true;
+            for (int i = 0; i < k; ++i)
+              if (m.perm[i] != i) edge = false;
+          }
+          break;
+        }
+        default:
+          edge = false;
+      }
+      walk(o, ok && edge);
+    }
+  };
+  for (int r : c.p.roots) walk(r, true);
+  std::set<int> out;
+  for (int e : local)
+    if (!unsafe.count(e) && g.nodes[e].numel() == R * C && g.nodes[e].dtype == SFX_F32) out.insert(e);
+  return out;
+}
+
+// Row template with TMA bulk-copy staging: persistent warps, one row per warp
+// per iteration; the row-local [R, C] inputs of the next NBUF rows are
+// streamed into shared memory by cp.async.bulk (the TMA engine) and tracked by
+// an mbarrier per stage, so HBM reads run continuously behind the arithmetic.
+KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs) {
+  KernelSource ks;
+  ks.strategy = "row";
+  ks.entry = "sfx_rowp_" + c.name;
+  fill_common(c, ks);
+  const int64_t R = rp.R, C = rp.C;
+  const int V = 4, TPR = 32;
+  const int64_t NCH = C / (TPR * V);
+  const int WARPS = 4, NBUF = 2;
+  std::vector<int> staged(staged_inputs.begin(), staged_inputs.end());
+  const int64_t row_bytes = C * 4;
+  const int64_t stage_bytes = row_bytes * static_cast<int64_t>(staged.size());
+  const int64_t data_bytes = WARPS * NBUF * stage_bytes;
+  const int smem = static_cast<int>(data_bytes + WARPS * NBUF * 8);
+  const int ctas_per_sm = std::max(1, std::min<int>(8, static_cast<int>((220 * 1024) / smem)));
+  const int64_t grid = std::min<int64_t>((R + WARPS - 1) / WARPS, int64_t{kNumSMs} * ctas_per_sm);
+
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, WARPS * 32);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
+  body.line("const int lr = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const sfx_u32 gmask = 0xffffffffu;");
+  body.line("const int gleader = 0;");
+  body.line("unsigned long long* bars = (unsigned long long*)(sfx_smem + " + fmt_i(data_bytes) + ") + warp * " +
+            std::to_string(NBUF) + ";");
+  body.line("unsigned char* stages = sfx_smem + (" + it + ")warp * " + fmt_i(NBUF * stage_bytes) + ";");
+  body.line("if (lr == 0) {");
+  body.line("  for (int s = 0; s < " + std::to_string(NBUF) + "; ++s) sfx_mbar_init(bars + s, 1);");
+  body.line("  sfx_fence_mbar_init();");
+  body.line("}");
+  body.line("__syncwarp();");
+  body.line("const " + it + " row0 = (" + it + ")blockIdx.x * " + std::to_string(WARPS) + " + warp;");
+  body.line("const " + it + " rstride = (" + it + ")gridDim.x * " + std::to_string(WARPS) + ";");
+  // issue(stage, row): expect_tx + one bulk copy per staged input
+  auto issue = [&](const std::string& s, const std::string& r) {
+    body.line("{");
+    body.line("  unsigned long long* bar = bars + " + s + ";");
+    body.line("  sfx_mbar_expect_tx(bar, " + fmt_i(stage_bytes) + "u);");
+    for (size_t k = 0; k < staged.size(); ++k)
+      body.line("  sfx_bulk_g2s(stages + " + s + " * " + fmt_i(stage_bytes) + " + " +
+                fmt_i(static_cast<int64_t>(k) * row_bytes) + ", " + em.input_ptr.at(staged[k]) + " + (" + r +
+                ") * " + fmt_i(C) + ", " + fmt_i(row_bytes) + "u, bar);");
+    body.line("}");
+  };
+  body.line("if (lr == 0) {");
+  body.indent++;
+  for (int s = 0; s < NBUF; ++s) {
+    body.line("if (row0 + " + std::to_string(s) + " * rstride < " + fmt_i(R) + ")");
+    issue(std::to_string(s), "row0 + " + std::to_string(s) + " * rstride");
+  }
+  body.indent--;
+  body.line("}");
+  body.line("for (int itr = 0;; ++itr) {");
+  body.indent++;
+  body.line("const " + it + " row = row0 + (" + it + ")itr * rstride;");
+  body.line("if (row >= " + fmt_i(R) + ") break;");
+  body.line("const int stg = itr % " + std::to_string(NBUF) + ";");
+  body.line("sfx_mbar_wait(bars + stg, (unsigned)((itr / " + std::to_string(NBUF) + ") & 1));");
+  em.push();
+  std::string rbase = em.ivar(Emitter::imul("row", C));
+  for (size_t k = 0; k < staged.size(); ++k) {
+    std::string p = em.fresh("st");
+    body.line("const float* " + p + " = (const float*)(stages + stg * " + fmt_i(stage_bytes) + " + " +
+              fmt_i(static_cast<int64_t>(k) * row_bytes) + ");");
+    em.staged[staged[k]] = {p, rbase};
+  }
+  emit_row_body(c, rp, em, body, TPR, V, NCH);
+  em.pop();
+  em.staged.clear();
+  body.line("__syncwarp();");
+  body.line("if (lr == 0 && row + " + std::to_string(NBUF) + " * rstride < " + fmt_i(R) + ")");
+  issue("stg", "row + " + std::to_string(NBUF) + " * rstride");
+  body.indent--;
+  body.line("}");
   ks.code = assemble(sig, body);
-  ks.block = threads;
-  ks.grid_x = (R + RPC - 1) / RPC;
+  ks.block = WARPS * 32;
+  ks.grid_x = grid;
+  ks.smem = smem;
   ks.vector_width = V;
-  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " threads/row=" +
-            std::to_string(TPR) + " elems/thread=" + std::to_string(NCH * V) + " levels=" +
-            std::to_string(rp.max_level);
+  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " TMA-staged inputs=" +
+            std::to_string(staged.size()) + " stages=" + std::to_string(NBUF) + " persistent grid=" +
+            std::to_string(grid) + " levels=" + std::to_string(rp.max_level);
   return ks;
 }
 
@@ -1042,7 +1197,21 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
     case SFX_STRATEGY_ROW: {
       RowPlan rp;
       if (!analyze_row(c, &rp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "row template not applicable: " + why);
-      ks = lower_row(c, rp, o);
+      // Register-resident rows by default.  The TMA-staged pipeline (row-local
+      // inputs streamed into shared memory by cp.async.bulk) is available on
+      // request: measured on B200 it ties on LayerNorm [8192,1024] and loses
+      // 5-25% on softmax / BERT rows (profiles/README.md), because one warp per
+      // row already keeps 8-18 independent 128-bit loads in flight.
+      std::set<int> staged = row_local_inputs(c, rp);
+      bool pipe_ok = !staged.empty() && rp.C % 128 == 0 && rp.C / 32 <= 64 &&
+                     4 * 2 * rp.C * 4 * static_cast<int64_t>(staged.size()) <= 200 * 1024 &&
+                     o.threads_per_row == 0 && o.rows_per_cta == 0;
+      if (o.row_pipeline == 2 && !pipe_ok)
+        throw Error(SFX_ERR_UNSUPPORTED, "TMA row pipeline not applicable to this group");
+      if (pipe_ok && o.row_pipeline == 2)
+        ks = lower_row_pipe(c, rp, staged);
+      else
+        ks = lower_row(c, rp, o);
       break;
     }
     case SFX_STRATEGY_COL: {

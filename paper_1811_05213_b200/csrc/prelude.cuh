@@ -94,9 +94,37 @@ __device__ __forceinline__ sfx_i4 sfx_ld4s(const int* p) {
       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
-// L1 prefetch of a small read-only operand shared by the CTA's rows.
-__device__ __forceinline__ void sfx_prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
+__device__ __forceinline__ sfx_f4 sfx_lds4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
+
+// ---- TMA bulk copies + mbarrier (sm_90+/sm_100a), used by the pipelined row template ----
+__device__ __forceinline__ unsigned sfx_smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void sfx_mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sfx_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void sfx_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void sfx_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sfx_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// one contiguous global -> shared copy by the TMA engine, completing on `bar`
+__device__ __forceinline__ void sfx_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(sfx_smem_u32(dst)), "l"(src), "r"(bytes), "r"(sfx_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void sfx_mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "SFX_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra SFX_DONE;\n"
+      "bra SFX_WAIT;\n"
+      "SFX_DONE:\n"
+      "}\n" :: "r"(sfx_smem_u32(bar)), "r"(parity) : "memory");
 }
 // Reused 128-bit loads (broadcast vectors): default caching.
 __device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }

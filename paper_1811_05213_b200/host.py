@@ -91,7 +91,7 @@ class SfxGraphDesc(C.Structure):
 
 class SfxCompileOpts(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("debug_checks", C.c_int32), ("rows_per_cta", C.c_int32),
-                ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32)]
+                ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32), ("row_pipeline", C.c_int32)]
 
 
 class SfxKernelInfo(C.Structure):
@@ -403,18 +403,18 @@ class GraphDesc:
         return C.byref(self.desc)
 
 
-def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0):
-    return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread)
+def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0):
+    return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline)
 
 
-def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto"):
+def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):
     """Lowers one group and NVRTC-compiles it for sm_100a without touching a GPU.
     Returns (cuda_source, cubin_path, strategy_note)."""
     gd = GraphDesc(graph, [program])
     src = C.create_string_buffer(1 << 22)
     path = C.create_string_buffer(4096)
     strat = C.create_string_buffer(1024)
-    opts = compile_opts(strategy)
+    opts = compile_opts(strategy, **kw)
     _check(lib().sfx_program_codegen(gd.ref(), 0, C.byref(opts), src, len(src), path, len(path), strat, len(strat)))
     return src.value.decode(), path.value.decode(), strat.value.decode()
 
@@ -530,11 +530,11 @@ class Kernel:
 class CompiledGraph:
     """The whole compiled module on device (run_compiled twin)."""
 
-    def __init__(self, ctx: Context, graph: TensorGraph, report: CompileReport, strategy="auto"):
+    def __init__(self, ctx: Context, graph: TensorGraph, report: CompileReport, strategy="auto", **kw):
         self.ctx, self.graph, self.report = ctx, graph, report
         self._gd = GraphDesc(graph, [k.program for k in report.kernels])
         h = C.c_void_p()
-        opts = compile_opts(strategy)
+        opts = compile_opts(strategy, **kw)
         _check(lib().sfx_graph_compile(ctx.h, self._gd.ref(), C.byref(opts), C.byref(h)))
         self.h = h
         n = C.c_int32()
