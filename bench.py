@@ -40,6 +40,7 @@ WORKLOAD_NAMES = {
     "C3b": "bias-add grad + dx output fp32 [65536,1024]",
     "C4": "transpose+bias+scale fp32 B32 S512 H16 D64",
     "C4b": "transpose+scale+bias fp32 B32 S512 H16 D64 (full bias)",
+    "C4t": "key transpose [B,S,H,D]->[B,H,D,S]+bias+scale fp32 B32 S512 H16 D64 (extra, innermost-moving)",
     "C5": "BERT-base encoder-layer non-MatMul graph, batch 64 seq 512",
 }
 
@@ -135,7 +136,8 @@ def reference_sample(config):
         # in the same byte proportions as b64 s512 (1/512 of it)
         return configs.c5_bert(B=1, S=512, Sq=64), "C5 query block: batch 1, 64 query rows x 512 keys (1/512 of b64 s512)"
     sizes = {"C1": dict(R=64, C=1024), "C2": dict(B=1, H=1, S=128, L=512), "C3": dict(N=512, C=1024),
-             "C3b": dict(N=512, C=1024), "C4": dict(B=1, S=128, H=16, D=64), "C4b": dict(B=1, S=128, H=16, D=64)}
+             "C3b": dict(N=512, C=1024), "C4": dict(B=1, S=128, H=16, D=64), "C4b": dict(B=1, S=128, H=16, D=64),
+             "C4t": dict(B=1, S=128, H=16, D=64)}
     return configs.build(config, **sizes[config]), f"{config} at {sizes[config]}"
 
 

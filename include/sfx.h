@@ -146,7 +146,7 @@ typedef struct sfx_compile_opts {
   int32_t rows_per_cta;  /* 0 = auto (row template) */
   int32_t threads_per_row; /* 0 = auto (row template) */
   int32_t items_per_thread; /* 0 = auto (map template: 128-bit vectors per thread) */
-  int32_t row_pipeline;     /* row template: 0 = auto, 1 = registers only, 2 = TMA-staged pipeline */
+  int32_t row_pipeline;     /* row template: 0/1 = register-resident rows, 2 = TMA-staged pipeline where applicable */
 } sfx_compile_opts;
 
 typedef struct sfx_ctx sfx_ctx;

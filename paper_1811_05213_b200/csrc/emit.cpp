@@ -206,6 +206,19 @@ std::string Emitter::load(int node, const std::vector<Ix>& comps) {
   auto pit = input_ptr.find(node);
   if (pit == input_ptr.end()) throw Error(SFX_ERR_EXEC, "missing external value " + n.id);
   const std::string& ptr = pit->second;
+  auto tt = tiled.find(node);
+  if (tt != tiled.end()) {  // transposed tile in shared memory
+    const Tile& t = tt->second;
+    std::string addr = t.arr + "[" + comps[t.jb].e + " - " + t.b0 + "][" + comps[t.ja].e + " - " + t.a0 + "]";
+    std::string key = "tld:" + addr;
+    std::string v = find(key);
+    if (v.empty()) {
+      v = fresh("v");
+      code->line(std::string("const ") + ctype(n.dtype) + " " + v + " = " + addr + ";");
+      bind(key, v);
+    }
+    return v;
+  }
   Ix L = linearize(comps, n.dims);
   auto st = staged.find(node);
   if (st != staged.end()) {  // row staged in shared memory by the TMA pipeline

@@ -61,6 +61,13 @@ class Emitter {
   // externals staged in shared memory for the current row: node ->
   // (const float* smem pointer variable, linear index of the row's first element)
   std::map<int, std::pair<std::string, std::string>> staged;
+  // externals staged as a transposed shared-memory tile: element at input comps
+  // c lives at arr[c[jb] - b0][c[ja] - a0]
+  struct Tile {
+    std::string arr, b0, a0;
+    int jb = 0, ja = 0;
+  };
+  std::map<int, Tile> tiled;
   // Strategy hook for member nodes: return a variable name to use instead of
   // evaluating the member's op, or "" to evaluate it inline.
   std::function<std::string(int node, const std::vector<Ix>& comps)> resolve;

@@ -440,6 +440,217 @@ KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
   return ks;
 }
 
+// ---- MAP with shared-memory-tiled transposes ---------------------------------------
+
+// Symbolic index walk from the root: every dimension of every reached node is
+// labelled with the root axis it is indexed by ("$k"), "0" for a broadcast
+// constant, or "?" when a reshape mixes axes.  Returns, per external, the set
+// of distinct label vectors it is read with.
+std::map<int, std::set<std::vector<std::string>>> index_labels(const Ctx& c, int root) {
+  std::map<int, std::set<std::vector<std::string>>> ext;
+  std::set<std::pair<int, std::vector<std::string>>> seen;
+  std::function<void(int, const std::vector<std::string>&)> walk = [&](int n, const std::vector<std::string>& t) {
+    if (!seen.insert({n, t}).second) return;
+    const Node& m = c.g.nodes[n];
+    if (!c.p.is_member(n)) {
+      if (!m.is_splat()) ext[n].insert(t);
+      return;
+    }
+    switch (m.op) {
+      case SFX_OP_ELEMENTWISE:
+        for (int o : m.operands) walk(o, t);
+        return;
+      case SFX_OP_TRANSPOSE: {
+        std::vector<std::string> in(t.size());
+        for (size_t i = 0; i < t.size(); ++i) in[m.perm[i]] = t[i];
+        walk(m.operands[0], in);
+        return;
+      }
+      case SFX_OP_BROADCAST: {
+        std::vector<std::string> in(m.dim_map.size());
+        for (size_t j = 0; j < m.dim_map.size(); ++j) in[j] = t[m.dim_map[j]];
+        walk(m.operands[0], in);
+        return;
+      }
+      case SFX_OP_RESHAPE:
+      case SFX_OP_BITCAST: {
+        const Node& in = c.g.nodes[m.operands[0]];
+        std::vector<std::string> nz_t;
+        std::vector<int64_t> nz_out, nz_in;
+        for (int i = 0; i < m.rank(); ++i)
+          if (m.dims[i] != 1) nz_t.push_back(t[i]), nz_out.push_back(m.dims[i]);
+        for (int i = 0; i < in.rank(); ++i)
+          if (in.dims[i] != 1) nz_in.push_back(in.dims[i]);
+        std::vector<std::string> r(in.rank(), "?");
+        if (nz_in == nz_out) {  // only unit dims added or removed
+          for (int i = 0, k = 0; i < in.rank(); ++i) r[i] = in.dims[i] == 1 ? "0" : nz_t[k++];
+        }
+        walk(m.operands[0], r);
+        return;
+      }
+      default: {
+        std::vector<std::string> q;
+        for (int o : m.operands) walk(o, std::vector<std::string>(c.g.nodes[o].rank(), "?"));
+        return;
+      }
+    }
+  };
+  std::vector<std::string> t;
+  for (int i = 0; i < c.g.nodes[root].rank(); ++i) t.push_back("$" + std::to_string(i));
+  walk(root, t);
+  return ext;
+}
+
+struct TilePlan {
+  int a = -1, b = -1;  // root axes: a = innermost (output-coalesced), b = input-innermost
+  std::map<int, std::pair<int, int>> inputs;  // external -> (jb, ja) input dims
+};
+
+// A map group whose (single-shape) roots read a streamed input whose innermost
+// dimension is indexed by a root axis other than the root's innermost: the
+// naive kLoop would read it with a stride.  Tile (a, b) through shared memory.
+bool analyze_tiled(const Ctx& c, TilePlan* tp) {
+  if (!c.reduces.empty()) return false;
+  const std::vector<int64_t>& dims = c.g.nodes[c.p.roots[0]].dims;
+  for (int r : c.p.roots)
+    if (c.g.nodes[r].dims != dims) return false;
+  const int n = static_cast<int>(dims.size());
+  if (n < 2) return false;
+  tp->a = n - 1;
+  std::map<int, int> votes;
+  std::map<int, std::pair<int, int>> cand;  // external -> (jb, ja), with b per external
+  std::map<int, int> bof;
+  std::map<int, std::set<std::vector<std::string>>> merged;
+  for (int r : c.p.roots)
+    for (auto& [e, ts] : index_labels(c, r)) merged[e].insert(ts.begin(), ts.end());
+  const std::string sa = "$" + std::to_string(tp->a);
+  for (auto& [e, ts] : merged) {
+    const Node& en = c.g.nodes[e];
+    if (ts.size() != 1 || en.rank() < 2 || en.numel() * 4 < (1 << 20)) continue;
+    const std::vector<std::string>& t = *ts.begin();
+    if (std::find(t.begin(), t.end(), "?") != t.end()) continue;
+    const std::string& last = t.back();
+    if (last == sa || last == "0") continue;
+    auto ja = std::find(t.begin(), t.end(), sa);
+    if (ja == t.end()) continue;
+    int b = std::stoi(last.substr(1));
+    cand[e] = {en.rank() - 1, static_cast<int>(ja - t.begin())};
+    bof[e] = b;
+    votes[b]++;
+  }
+  if (votes.empty()) return false;
+  tp->b = std::max_element(votes.begin(), votes.end(), [](auto& x, auto& y) { return x.second < y.second; })->first;
+  for (auto& [e, j] : cand)
+    if (bof[e] == tp->b) tp->inputs[e] = j;
+  return !tp->inputs.empty();
+}
+
+KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp) {
+  KernelSource ks;
+  ks.strategy = "map";
+  ks.entry = "sfx_mapt_" + c.name;
+  fill_common(c, ks);
+  const std::vector<int64_t>& dims = c.g.nodes[c.p.roots[0]].dims;
+  const int n = static_cast<int>(dims.size());
+  const int a = tp.a, b = tp.b;
+  const int64_t na = dims[a], nb = dims[b];
+  const int64_t nta = (na + 31) / 32, ntb = (nb + 31) / 32;
+  std::vector<int64_t> rest_dims;
+  std::vector<int> rest_axes;
+  for (int i = 0; i < n; ++i)
+    if (i != a && i != b) rest_dims.push_back(dims[i]), rest_axes.push_back(i);
+  const int64_t nrest = prod(rest_dims, 0, rest_dims.size());
+  Emitter em(c.g, c.p, 1, c.wide);
+  std::string sig = signature(c, em, ks.entry, 256);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;");
+  body.line(it + " tix = blockIdx.x;");
+  body.line("const " + it + " a0 = (tix % " + fmt_i(nta) + ") * 32; tix /= " + fmt_i(nta) + ";");
+  body.line("const " + it + " b0 = (tix % " + fmt_i(ntb) + ") * 32; tix /= " + fmt_i(ntb) + ";");
+  body.line("const " + it + " rest = tix;");
+  std::vector<Ix> rest = em.from_linear(em.uni("rest"), rest_dims);
+  auto root_comps = [&](const std::string& av, const std::string& bv) {
+    std::vector<Ix> comps(n);
+    comps[a] = em.uni(av);
+    comps[b] = em.uni(bv);
+    for (size_t k = 0; k < rest_axes.size(); ++k) comps[rest_axes[k]] = rest[k];
+    return comps;
+  };
+  // load phase: each tiled input read along its own innermost dim (root axis b)
+  int ti = 0;
+  for (auto& [e, j] : tp.inputs) {
+    const Node& en = c.g.nodes[e];
+    std::string arr = "tile" + std::to_string(ti++);
+    body.line(std::string("__shared__ ") + ctype(en.dtype) + " " + arr + "[32][33];");
+    em.tiled[e] = {arr, "b0", "a0", j.first, j.second};
+  }
+  // input comps for the load phase come from the label walk: rebuild them for
+  // (a = a0 + ty + 8k, b = b0 + tx)
+  std::map<int, std::vector<std::string>> labels;
+  for (int r : c.p.roots)
+    for (auto& [e, ts] : index_labels(c, r))
+      if (tp.inputs.count(e)) labels[e] = *ts.begin();
+  for (int k = 0; k < 4; ++k) {
+    std::string av = em.fresh("la"), bv = em.fresh("lb");
+    body.line("{");
+    body.indent++;
+    em.push();
+    body.line("const " + it + " " + av + " = a0 + ty + " + std::to_string(8 * k) + ";");
+    body.line("const " + it + " " + bv + " = b0 + tx;");
+    body.line("if (" + av + " < " + fmt_i(na) + " && " + bv + " < " + fmt_i(nb) + ") {");
+    body.indent++;
+    std::vector<Ix> rc = root_comps(av, bv);
+    for (auto& [e, j] : tp.inputs) {
+      const Node& en = c.g.nodes[e];
+      std::vector<Ix> ic(en.rank());
+      for (int d = 0; d < en.rank(); ++d) {
+        const std::string& l = labels[e][d];
+        ic[d] = l == "0" ? em.uni("0") : rc[std::stoi(l.substr(1))];
+      }
+      Ix L = em.linearize(ic, en.dims);
+      body.line(em.tiled[e].arr + "[tx][ty + " + std::to_string(8 * k) + "] = sfx_ld(" + em.input_ptr.at(e) +
+                " + " + L.e + ");");
+    }
+    body.indent--;
+    body.line("}");
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  body.line("__syncthreads();");
+  // compute phase: coalesced along the root's innermost axis a
+  for (int k = 0; k < 4; ++k) {
+    std::string av = em.fresh("ca"), bv = em.fresh("cb");
+    body.line("{");
+    body.indent++;
+    em.push();
+    body.line("const " + it + " " + av + " = a0 + tx;");
+    body.line("const " + it + " " + bv + " = b0 + ty + " + std::to_string(8 * k) + ";");
+    body.line("if (" + av + " < " + fmt_i(na) + " && " + bv + " < " + fmt_i(nb) + ") {");
+    body.indent++;
+    std::vector<Ix> rc = root_comps(av, bv);
+    for (int r : c.p.roots) {
+      std::string v = em.value(r, rc);
+      Ix L = em.linearize(rc, dims);
+      body.line("out" + std::to_string(root_slot(c, r)) + "[" + L.e + "] = " + v + ";");
+    }
+    body.indent--;
+    body.line("}");
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  ks.code = assemble(sig, body);
+  ks.block = 256;
+  ks.grid_x = nta * ntb * nrest;
+  ks.vector_width = 1;
+  ks.note = "kLoop with " + std::to_string(tp.inputs.size()) + " smem-tiled transposed input(s), tile 32x32 over root axes (" +
+            std::to_string(a) + "," + std::to_string(b) + ")";
+  return ks;
+}
+
 // ---- ROW ------------------------------------------------------------------------
 
 void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH);
@@ -1192,7 +1403,13 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   switch (strat) {
     case SFX_STRATEGY_MAP:
       if (!analyze_map(c, &why)) throw Error(SFX_ERR_UNSUPPORTED, "map template not applicable: " + why);
-      ks = lower_map(c, o);
+      {
+        TilePlan tp;
+        if (o.items_per_thread == 0 && analyze_tiled(c, &tp))
+          ks = lower_map_tiled(c, tp);
+        else
+          ks = lower_map(c, o);
+      }
       break;
     case SFX_STRATEGY_ROW: {
       RowPlan rp;
@@ -1206,8 +1423,6 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
       bool pipe_ok = !staged.empty() && rp.C % 128 == 0 && rp.C / 32 <= 64 &&
                      4 * 2 * rp.C * 4 * static_cast<int64_t>(staged.size()) <= 200 * 1024 &&
                      o.threads_per_row == 0 && o.rows_per_cta == 0;
-      if (o.row_pipeline == 2 && !pipe_ok)
-        throw Error(SFX_ERR_UNSUPPORTED, "TMA row pipeline not applicable to this group");
       if (pipe_ok && o.row_pipeline == 2)
         ks = lower_row_pipe(c, rp, staged);
       else

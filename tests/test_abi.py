@@ -47,7 +47,7 @@ WORKLOADS = sorted(f[:-5] for f in os.listdir(T.PLANS) if f.endswith(".json"))
 
 EXPECTED = {  # strategy the GroupAnalyzer must pick at full size
     ("C1", "y"): "row", ("C2", "y"): "row", ("C3", "db"): "col", ("C3b", "db"): "col",
-    ("C3b", "dx_out"): "map", ("C4", "y"): "map", ("C4b", "y"): "map", ("C5", "ctx_r"): "map",
+    ("C3b", "dx_out"): "map", ("C4", "y"): "map", ("C4b", "y"): "map", ("C4t", "y"): "map", ("C5", "ctx_r"): "map",
     ("C5", "gelu"): "map", ("C5", "h1"): "row", ("C5", "h2"): "row", ("C5", "probs_d"): "row",
 }
 
@@ -145,3 +145,13 @@ def test_parse_graph_lowers_mean_like_the_reference():
     assert [i.id for i in g.instructions] == [i.id for i in gb.instructions]
     assert g.at("ln.mean").op == "scale" and g.at("ln.mean").scalar == 1.0 / 8
     assert g.at("ln.mean.sum").op == "reduce"
+
+
+def test_innermost_moving_transpose_uses_smem_tiles():
+    """C4t (key transpose [B,S,H,D]->[B,H,D,S]) moves the innermost dimension:
+    the map template stages it through a padded 32x33 shared-memory tile."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C4t.full.json"))
+    src, cubin, note = H.codegen(g, rep.kernels[0].program)
+    assert "smem-tiled" in note and "[32][33]" in src
+    sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+    assert "STS" in sass and "LDS" in sass and "BAR.SYNC" in sass

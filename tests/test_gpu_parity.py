@@ -87,7 +87,7 @@ def test_random_graphs(ctx, stream, strategy):
 
 
 @pytest.mark.parametrize("strategy", ["auto", "literal"])
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C5"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t", "C5"])
 def test_configs_small(ctx, name, strategy):
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
     inputs = T.gen_inputs(g, 42, -1.0, 1.0)
@@ -98,7 +98,22 @@ def test_configs_small(ctx, name, strategy):
     assert not _check(g, outs, inputs, strict=True, literal=(strategy == "literal"))
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_tma_row_pipeline_small(ctx, name):
+    """The TMA-staged (cp.async.bulk + mbarrier) row template, where applicable."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
+    inputs = T.gen_inputs(g, 43, -1.0, 1.0)
+    cg = H.CompiledGraph(ctx, g, rep, row_pipeline=2)
+    try:
+        entries = [k.info["entry"] for k in cg.kernels]
+        outs = cg.run_host(inputs)
+    finally:
+        cg.close()
+    assert any(e.startswith("sfx_rowp_") for e in entries), entries
+    assert not _check(g, outs, inputs, strict=True)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t"])
 def test_configs_full_size(ctx, name):
     """BASELINE.json shapes with the reference's full-size plan."""
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, f"{name}.full.json"))

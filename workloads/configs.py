@@ -113,6 +113,20 @@ def c4_transpose(B=32, S=512, H=16, D=64):
     return g.doc(["y"])
 
 
+def c4t_transpose(B=32, S=512, H=16, D=64):
+    """Extra (not a BASELINE.json config): the attention key transpose
+    [B,S,H,D] -> [B,H,D,S], which moves the innermost dimension — exercises the
+    shared-memory-tiled transpose template at the C4 size."""
+    g = _G()
+    g.param("x", [B, S, H, D])
+    g.param("bias", [H, D])
+    g.add("bias_b", "broadcast", ["bias"], [B, S, H, D], broadcast_dim_map=[2, 3])
+    g.add("xb", "add", ["x", "bias_b"], [B, S, H, D])
+    g.add("xt", "transpose", ["xb"], [B, H, D, S], permutation=[0, 2, 3, 1])
+    g.add("y", "scale", ["xt"], [B, H, D, S], scalar=0.125)
+    return g.doc(["y"])
+
+
 def c4b_transpose(B=32, S=512, H=16, D=64):
     g = _G()
     g.param("q", [B, S, H, D])
@@ -188,6 +202,7 @@ BUILDERS = {
     "C3b": lambda **k: c3_biasgrad(with_dx=True, **k),
     "C4": c4_transpose,
     "C4b": c4b_transpose,
+    "C4t": c4t_transpose,
     "C5": c5_bert,
 }
 
@@ -200,6 +215,7 @@ FULL = {
     "C3b": dict(N=65536, C=1024),
     "C4": dict(B=32, S=512, H=16, D=64),
     "C4b": dict(B=32, S=512, H=16, D=64),
+    "C4t": dict(B=32, S=512, H=16, D=64),
     "C5": dict(B=64, S=512),
 }
 
@@ -210,6 +226,7 @@ SMALL = {
     "C3b": dict(N=2048, C=1024),
     "C4": dict(B=2, S=64, H=16, D=64),
     "C4b": dict(B=2, S=64, H=16, D=64),
+    "C4t": dict(B=2, S=64, H=16, D=64),
     "C5": dict(B=8, S=64),
 }
 
