@@ -425,7 +425,7 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dom["kernel"])
+            traffic = json.load(f).get(f"{args.config}/{dom['kernel']}")
     except Exception:
         pass
     cpu = None

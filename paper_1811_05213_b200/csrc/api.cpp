@@ -132,6 +132,9 @@ struct sfx_graph {
   std::map<int, CUdeviceptr> owned;  // intermediates + dense constants (device-resident)
   std::map<std::vector<uint64_t>, std::pair<CUgraph, CUgraphExec>> captured;
   std::vector<CUdeviceptr> host_bufs;  // staging for sfx_graph_run_host (params then outputs)
+  CUstream d2h = nullptr;              // host path: device->host copies overlap the next groups
+  std::vector<CUevent> events;
+  std::vector<int> host_order;
 };
 
 namespace {
@@ -244,6 +247,44 @@ std::vector<int> condensation_order(const sfx::Graph& g) {
       if (--indeg[s] == 0) ready.insert(std::lower_bound(ready.begin(), ready.end(), s), s);
   }
   if (processed != n) throw sfx::Error(SFX_ERR_EXEC, "condensation is cyclic");
+  return order;
+}
+
+// Launch order for the host-buffer path: any order respecting the groups'
+// dataflow gives identical values; groups returning the most bytes go first so
+// their device->host copies overlap the remaining host->device traffic.
+std::vector<int> host_order(const sfx_graph* G) {
+  const sfx::Graph& g = G->graph;
+  const int P = static_cast<int>(g.programs.size());
+  std::map<int, int> producer;
+  for (int p = 0; p < P; ++p)
+    for (int r : g.programs[p].roots) producer[r] = p;
+  std::set<int> outs(g.outputs.begin(), g.outputs.end());
+  std::vector<int64_t> d2h(P, 0);
+  std::vector<std::set<int>> succ(P);
+  std::vector<int> indeg(P, 0);
+  for (int p = 0; p < P; ++p) {
+    for (int r : g.programs[p].roots)
+      if (outs.count(r)) d2h[p] += g.nodes[r].numel() * 4;
+    for (int in : g.programs[p].inputs) {
+      auto it = producer.find(in);
+      if (it != producer.end() && it->second != p && succ[it->second].insert(p).second) ++indeg[p];
+    }
+  }
+  std::vector<int> order, ready;
+  for (int p = 0; p < P; ++p)
+    if (!indeg[p]) ready.push_back(p);
+  while (!ready.empty()) {
+    auto best = std::min_element(ready.begin(), ready.end(), [&](int a, int b) {
+      return d2h[a] != d2h[b] ? d2h[a] > d2h[b] : a < b;
+    });
+    int p = *best;
+    ready.erase(best);
+    order.push_back(p);
+    for (int q : succ[p])
+      if (--indeg[q] == 0) ready.push_back(q);
+  }
+  if (static_cast<int>(order.size()) != P) throw sfx::Error(SFX_ERR_EXEC, "group dependencies are cyclic");
   return order;
 }
 
@@ -597,14 +638,58 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
     }
     std::vector<uint64_t> dp(G->host_bufs.begin(), G->host_bufs.begin() + n_params);
     std::vector<uint64_t> dout(G->host_bufs.begin() + n_params, G->host_bufs.end());
-    for (int i = 0; i < n_params; ++i)
-      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[i], params[i], G->graph.nodes[G->params[i]].numel() * 4, s),
+    const sfx::Graph& g = G->graph;
+    if (!G->d2h) {
+      sfx::check_cu(d.cuStreamCreate(&G->d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      G->events.resize(G->kernels.size() + 1);
+      for (CUevent& e : G->events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      G->host_order = host_order(G);
+    }
+    // Overlapped host path: each group's params are copied in right before it
+    // runs and its graph outputs are copied back on a second stream while the
+    // next groups' inputs cross PCIe (full duplex).  Groups that return the
+    // most bytes go first (any dependency-respecting order gives the same values).
+    std::map<int, CUdeviceptr> where = G->owned;
+    std::map<int, int> param_slot, out_slot;
+    for (int i = 0; i < n_params; ++i) where[G->params[i]] = dp[i], param_slot[G->params[i]] = i;
+    for (int i = 0; i < n_outputs; ++i) where[g.outputs[i]] = dout[i], out_slot[g.outputs[i]] = i;
+    std::vector<bool> copied(n_params, false);
+    auto h2d = [&](int node) {
+      auto it = param_slot.find(node);
+      if (it == param_slot.end() || copied[it->second]) return;
+      copied[it->second] = true;
+      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[it->second], params[it->second], g.nodes[node].numel() * 4, s),
                     "cuMemcpyHtoDAsync");
-    graph_enqueue(G, dp.data(), dout.data(), s);
-    for (int i = 0; i < n_outputs; ++i)
-      sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], dout[i], G->graph.nodes[G->graph.outputs[i]].numel() * 4, s),
-                    "cuMemcpyDtoHAsync");
+    };
+    std::vector<bool> returned(n_outputs, false);
+    for (size_t q = 0; q < G->host_order.size(); ++q) {
+      sfx_kernel* k = G->kernels[G->host_order[q]];
+      for (int in : k->src.inputs) h2d(in);
+      launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), s);
+      bool any = false;
+      for (int r : k->src.outputs) any = any || out_slot.count(r);
+      if (!any) continue;
+      sfx::check_cu(d.cuEventRecord(G->events[q], s), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(G->d2h, G->events[q], 0), "cuStreamWaitEvent");
+      for (int r : k->src.outputs) {
+        auto it = out_slot.find(r);
+        if (it == out_slot.end() || returned[it->second]) continue;
+        returned[it->second] = true;
+        sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[it->second], dout[it->second], g.nodes[r].numel() * 4, G->d2h),
+                      "cuMemcpyDtoHAsync");
+      }
+    }
+    // graph outputs no group produces (a parameter or constant listed as output)
+    for (int i = 0; i < n_outputs; ++i) {
+      if (returned[i]) continue;
+      int o = g.outputs[i];
+      h2d(o);
+      CUdeviceptr src = param_slot.count(o) ? dp[param_slot[o]] : G->owned.count(o) ? G->owned.at(o) : 0;
+      if (!src) throw sfx::Error(SFX_ERR_EXEC, "no value for graph output " + g.nodes[o].id);
+      sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
+    }
     sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
+    sfx::check_cu(d.cuStreamSynchronize(G->d2h), "cuStreamSynchronize");
   });
 }
 
@@ -618,6 +703,8 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
         d.cuGraphExecDestroy(ge.second);
         d.cuGraphDestroy(ge.first);
       }
+      for (CUevent e : G->events) d.cuEventDestroy(e);
+      if (G->d2h) d.cuStreamDestroy(G->d2h);
     } catch (...) {
     }
     for (sfx_kernel* k : G->kernels) destroy_kernel(k);

@@ -50,6 +50,12 @@ const Driver& driver() {
     SFX_BIND(cuMemcpyDtoDAsync)
     SFX_BIND(cuMemsetD32Async)
     SFX_BIND(cuStreamSynchronize)
+    SFX_BIND(cuStreamCreate)
+    SFX_BIND(cuStreamDestroy)
+    SFX_BIND(cuStreamWaitEvent)
+    SFX_BIND(cuEventCreate)
+    SFX_BIND(cuEventDestroy)
+    SFX_BIND(cuEventRecord)
     SFX_BIND(cuModuleLoadData)
     SFX_BIND(cuModuleUnload)
     SFX_BIND(cuModuleGetFunction)

@@ -28,6 +28,12 @@ struct Driver {
   SFX_DRV(cuMemcpyDtoDAsync)
   SFX_DRV(cuMemsetD32Async)
   SFX_DRV(cuStreamSynchronize)
+  SFX_DRV(cuStreamCreate)
+  SFX_DRV(cuStreamDestroy)
+  SFX_DRV(cuStreamWaitEvent)
+  SFX_DRV(cuEventCreate)
+  SFX_DRV(cuEventDestroy)
+  SFX_DRV(cuEventRecord)
   SFX_DRV(cuModuleLoadData)
   SFX_DRV(cuModuleUnload)
   SFX_DRV(cuModuleGetFunction)

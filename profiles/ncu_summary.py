@@ -76,6 +76,7 @@ def main():
     ap.add_argument("launches", nargs="?")
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--algo", default=None, help="json {kernel: algorithmic bytes per launch}")
+    ap.add_argument("--config", required=True, help="workload name (keys of traffic.json are <config>/<kernel>)")
     args = ap.parse_args()
     algo = json.load(open(args.algo)) if args.algo else {}
     rows = raw_rows(args.rep)
@@ -94,7 +95,7 @@ def main():
                      f"{d.get('dram_wr', 0) / 1e6:.1f} | {ratio} | {d.get('dram_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                      f"{d.get('warps_active_pct', 0):.1f} | {int(d.get('regs', 0))} | {int(d.get('grid', 0))} | "
                      + ", ".join(f"{k} {v:.1f}" for k, v in d["stalls"]) + " |")
-        traffic[d["kernel"]] = t
+        traffic[f"{args.config}/{d['kernel']}"] = t
     with open(os.path.join(HERE, f"{args.tag}_kernels.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(traffic_path, "w") as f:
