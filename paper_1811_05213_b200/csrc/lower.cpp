@@ -655,6 +655,20 @@ KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp) {
 
 void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH);
 
+// Threads per row: the largest power of two <= 32 dividing the row into
+// V-vectors; rows longer than 32 threads x 32 elements span several warps (up
+// to a whole CTA) at ~32 elements per thread.
+int row_tpr(int64_t C, int V) {
+  int TPR = 1;
+  for (int t = 32; t >= 1; t /= 2)
+    if (C % (static_cast<int64_t>(t) * V) == 0) {
+      TPR = t;
+      break;
+    }
+  while (TPR >= 32 && TPR < 1024 && C / TPR > 32 && C % (static_cast<int64_t>(TPR) * 2 * V) == 0) TPR *= 2;
+  return TPR;
+}
+
 KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "row";
@@ -662,22 +676,17 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   fill_common(c, ks);
   const int64_t R = rp.R, C = rp.C;
   int V = (C % 4 == 0) ? 4 : 1;
-  int TPR = 1;
-  for (int t = 32; t >= 1; t /= 2)
-    if (C % (static_cast<int64_t>(t) * V) == 0) {
-      TPR = t;
-      break;
-    }
+  int TPR = row_tpr(C, V);
   if (o.threads_per_row > 0) {
     int t = o.threads_per_row;
-    if (t > 32 || (t & (t - 1)) || C % (static_cast<int64_t>(t) * V) != 0)
-      throw Error(SFX_ERR_INVALID, "threads_per_row must be a power of two <= 32 dividing the row");
+    if (t > 1024 || (t & (t - 1)) || C % (static_cast<int64_t>(t) * V) != 0)
+      throw Error(SFX_ERR_INVALID, "threads_per_row must be a power of two <= 1024 dividing the row");
     TPR = t;
   }
   const int64_t NCH = C / (static_cast<int64_t>(TPR) * V);
   if (NCH * V > 64) throw Error(SFX_ERR_UNSUPPORTED, "row of " + std::to_string(C) + " elements exceeds the register-resident row template");
   const int B = 256;
-  int RPC = B / TPR;
+  int RPC = std::max(1, B / TPR);
   if (o.rows_per_cta > 0 && o.rows_per_cta <= RPC) RPC = o.rows_per_cta;
   const int threads = RPC * TPR;
 
@@ -688,10 +697,21 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   const std::string& it = em.idx_t;
   body.line("const int tid = threadIdx.x;");
   body.line("const int lr = tid & " + std::to_string(TPR - 1) + ";");
-  body.line("const " + it + " row = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + (tid / " +
-            std::to_string(TPR) + ");");
-  body.line("if (row >= " + fmt_i(R) + ") return;");
-  if (TPR > 1) {
+  if (TPR > 32) {
+    body.line("const int rin = tid / " + std::to_string(TPR) + ", wir = (tid & " + std::to_string(TPR - 1) +
+              ") >> 5;");
+    body.line("const " + it + " row_u = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + rin;");
+    body.line("const bool rvalid = row_u < " + fmt_i(R) + ";");
+    body.line("const " + it + " row = rvalid ? row_u : " + fmt_i(R - 1) + ";");
+  } else {
+    body.line("const " + it + " row = (" + it + ")blockIdx.x * " + std::to_string(RPC) + " + (tid / " +
+              std::to_string(TPR) + ");");
+    body.line("if (row >= " + fmt_i(R) + ") return;");
+  }
+  if (TPR >= 32) {
+    body.line("const sfx_u32 gmask = 0xffffffffu;");
+    body.line("const int gleader = 0;");
+  } else if (TPR > 1) {
     if (TPR == 32)
       body.line("const sfx_u32 gmask = 0xffffffffu;");
     else
@@ -767,11 +787,42 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
       const Node& rn = c.g.nodes[red[k]];
       const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
                       : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
-      for (int m = TPR / 2; m >= 1; m /= 2)
+      for (int m = std::min(TPR, 32) / 2; m >= 1; m /= 2)
         body.line(acc[k] + " = " + f + "(" + acc[k] + ", sfx_shfl_xor(" + acc[k] + ", " +
                   std::to_string(m) + ", gmask));");
+    }
+    const int W = TPR > 32 ? TPR / 32 : 1;  // warps per row
+    std::vector<std::string> rsm(red.size()), rfm(red.size());
+    if (W > 1) {
+      // rows spanning several warps: per-warp partials through shared memory,
+      // folded by every thread in warp order (deterministic)
+      const int RPC = std::max(1, 256 / TPR);
+      for (size_t k = 0; k < red.size(); ++k) {
+        const Node& rn = c.g.nodes[red[k]];
+        rsm[k] = em.fresh("rsm");
+        body.line(std::string("__shared__ ") + ctype(rn.dtype) + " " + rsm[k] + "[" + std::to_string(RPC) + "][" +
+                  std::to_string(W) + "];");
+        body.line("if ((tid & 31) == 0) " + rsm[k] + "[rin][wir] = " + acc[k] + ";");
+        if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+          rfm[k] = em.fresh("rfm");
+          body.line(std::string("__shared__ float ") + rfm[k] + "[" + std::to_string(RPC) + "];");
+          body.line("if (lr == 0) " + rfm[k] + "[rin] = " + first[k] + ";");
+        }
+      }
+      body.line("__syncthreads();");
+      for (size_t k = 0; k < red.size(); ++k) {
+        const Node& rn = c.g.nodes[red[k]];
+        const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
+                        : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
+        body.line(acc[k] + " = " + rsm[k] + "[rin][0];");
+        for (int w = 1; w < W; ++w)
+          body.line(acc[k] + " = " + f + "(" + acc[k] + ", " + rsm[k] + "[rin][" + std::to_string(w) + "]);");
+      }
+    }
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
       if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
-        std::string f0 = TPR > 1 ? "sfx_shfl(" + first[k] + ", gleader, gmask)" : first[k];
+        std::string f0 = W > 1 ? rfm[k] + "[rin]" : TPR > 1 ? "sfx_shfl(" + first[k] + ", gleader, gmask)" : first[k];
         body.line(acc[k] + " = sfx_fold_first(" + f0 + ", " + acc[k] + ");");
       }
       reduced[red[k]] = acc[k];
@@ -790,18 +841,20 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
         vals[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rowix, col));
     }
     std::string addr = em.ivar(Emitter::iadd(rb, cb[j]));
+    // multi-warp rows keep out-of-range rows alive (clamped) for the barriers
+    const std::string guard = TPR > 32 ? "if (rvalid) " : "";
     for (size_t k = 0; k < full_roots.size(); ++k) {
       std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
       if (V == 4)
-        body.line("sfx_st4(" + out + " + " + addr + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
+        body.line(guard + "sfx_st4(" + out + " + " + addr + ", " + vals[k][0] + ", " + vals[k][1] + ", " +
                   vals[k][2] + ", " + vals[k][3] + ");");
       else
-        body.line(out + "[" + addr + "] = " + vals[k][0] + ";");
+        body.line(guard + out + "[" + addr + "] = " + vals[k][0] + ";");
     }
   }
   if (!row_roots.empty()) {
     em.lane = 0;
-    body.line("if (lr == 0) {");
+    body.line(TPR > 32 ? "if (lr == 0 && rvalid) {" : "if (lr == 0) {");
     body.indent++;
     em.push();
     for (int r : row_roots) {
@@ -1371,13 +1424,7 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   RowPlan rp;
   if (analyze_row(c, &rp, &w)) {
     int V = rp.C % 4 == 0 ? 4 : 1;
-    int TPR = 1;
-    for (int t = 32; t >= 1; t /= 2)
-      if (rp.C % (static_cast<int64_t>(t) * V) == 0) {
-        TPR = t;
-        break;
-      }
-    if (rp.C / TPR <= 64) return "row";
+    if (rp.C / row_tpr(rp.C, V) <= 64) return "row";
     w = "row too long for registers";
   }
   reasons += "; row: " + w;

@@ -189,6 +189,24 @@ def test_column_reduce_is_deterministic_and_relaunchable(ctx):
     cg.close()
 
 
+EXTRA = sorted(f[:-5] for f in os.listdir(os.path.join(T.GOLDEN, "plans_extra")))
+
+
+@pytest.mark.parametrize("name", EXTRA)
+def test_long_and_odd_rows(ctx, name):
+    """Rows spanning several warps (up to a CTA) and row counts that do not
+    fill the last CTA: the multi-warp row template, against the fp64 oracle;
+    the literal tier (reference fold order) against the fp32 oracle."""
+    g, rep, b = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 17, -1.0, 1.0)
+    outs, launched, strategies = _run(ctx, g, rep, inputs, "auto")
+    assert strategies == ["row"] and launched == 1
+    assert not _check(g, outs, inputs, strict=True)
+    outs, launched, strategies = _run(ctx, g, rep, inputs, "literal")
+    assert strategies == ["literal"]
+    assert not _check(g, outs, inputs, literal=True)
+
+
 DEVICE_PARITY = os.path.join(T.ROOT, "oracle", "_ref", "device_parity")
 
 
