@@ -658,14 +658,20 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
 // Threads per row: the largest power of two <= 32 dividing the row into
 // V-vectors; rows longer than 32 threads x 32 elements span several warps (up
 // to a whole CTA) at ~32 elements per thread.
-int row_tpr(int64_t C, int V) {
+// `streams` = number of [R, C] inputs read per element: rows are widened until
+// a thread holds <= 32 streamed values (measured on B200: BERT probs_d / h1
+// with 3 streamed inputs gain 4-6% at 2 warps per row; 1-input softmax rows
+// are best at one warp).
+int row_tpr(int64_t C, int V, int streams = 1) {
   int TPR = 1;
   for (int t = 32; t >= 1; t /= 2)
     if (C % (static_cast<int64_t>(t) * V) == 0) {
       TPR = t;
       break;
     }
-  while (TPR >= 32 && TPR < 1024 && C / TPR > 32 && C % (static_cast<int64_t>(TPR) * 2 * V) == 0) TPR *= 2;
+  streams = std::max(1, streams);
+  while (TPR >= 32 && TPR < 1024 && C / TPR * streams > 32 && C % (static_cast<int64_t>(TPR) * 2 * V) == 0)
+    TPR *= 2;
   return TPR;
 }
 
@@ -676,7 +682,10 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   fill_common(c, ks);
   const int64_t R = rp.R, C = rp.C;
   int V = (C % 4 == 0) ? 4 : 1;
-  int TPR = row_tpr(C, V);
+  int streams = 0;
+  for (int n : c.p.inputs)
+    if (c.g.nodes[n].numel() == R * C) ++streams;
+  int TPR = row_tpr(C, V, streams);
   if (o.threads_per_row > 0) {
     int t = o.threads_per_row;
     if (t > 1024 || (t & (t - 1)) || C % (static_cast<int64_t>(t) * V) != 0)
@@ -1012,7 +1021,7 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
 
 // ---- COL ------------------------------------------------------------------------
 
-KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
+KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "col";
   ks.entry = "sfx_col_" + c.name;
@@ -1022,7 +1031,9 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   const int WARPS = 8, B = WARPS * 32;
   const int64_t TC = 32 * V;
   const int64_t tiles = (C + TC - 1) / TC;
-  int64_t S = std::max<int64_t>(1, (kNumSMs * 4 + tiles - 1) / tiles);
+  // row stripes: ~4 CTAs per SM in one wave (col template reuses rows_per_cta
+  // as a stripe-count override and items_per_thread as rows per iteration)
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, (kNumSMs * 4 + tiles - 1) / tiles);
   S = std::min<int64_t>(S, std::max<int64_t>(1, R / 64));
   S = std::min<int64_t>(S, 65535);
   const int64_t RS = (R + S - 1) / S;
@@ -1105,7 +1116,7 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp) {
   };
   // UR rows per iteration, unguarded, so all their 128-bit loads are in flight
   // together; then the remainder one row at a time
-  const int UR = 4;
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
   body.line("if (cok) {");
   body.indent++;
   body.line(it + " r = r_begin + warp;");
@@ -1479,7 +1490,7 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
     case SFX_STRATEGY_COL: {
       ColPlan cp;
       if (!analyze_col(c, &cp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "col template not applicable: " + why);
-      ks = lower_col(c, cp);
+      ks = lower_col(c, cp, o);
       break;
     }
     case SFX_STRATEGY_LITERAL:
