@@ -287,6 +287,34 @@ int cmd_bench(int argc, char** argv) {
   return sink.load() > 0 ? 0 : 1;
 }
 
+// Loads a (measured) performance library with the reference's own parser
+// (PerfLibrary::load, tuning.cpp:41-90) and plans the graph with it.
+int cmd_perflib(int argc, char** argv) {
+  if (argc < 4) throw std::runtime_error("usage: perflib <graph> <perf.lib>");
+  TensorGraph g = load_any(argv[2]);
+  PerfLibrary lib = PerfLibrary::load(argv[3]);
+  size_t measured = 0;
+  for (const auto& [k, e] : lib.entries())
+    if (!e.synthetic) ++measured;
+  PipelineOptions o;
+  CostModelParams params;
+  CompileReport with = compile_graph(g, o, lib, params);
+  PerfLibrary empty;
+  CompileReport base = compile_graph(g, o, empty, params);
+  json line = {{"entries", lib.entries().size()}, {"measured_entries", measured}, {"hits", lib.hits()},
+               {"misses", lib.misses()}, {"fused_kernels", with.fused_kernels},
+               {"fused_kernels_default", base.fused_kernels}};
+  json kernels = json::array();
+  for (size_t i = 0; i < with.kernels.size(); ++i)
+    kernels.push_back({{"fusion_root", with.kernels[i].comp.fusion_root}, {"cost_us", with.kernels[i].cost_us},
+                       {"members", with.kernels[i].comp.members.size()},
+                       {"same_members_as_default", i < base.kernels.size() &&
+                                                       base.kernels[i].comp.members == with.kernels[i].comp.members}});
+  line["kernels"] = kernels;
+  std::cout << line.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -297,6 +325,7 @@ int main(int argc, char** argv) {
     if (cmd == "random") return cmd_random(argc, argv);
     if (cmd == "run") return cmd_run(argc, argv);
     if (cmd == "bench") return cmd_bench(argc, argv);
+    if (cmd == "perflib") return cmd_perflib(argc, argv);
     if (cmd == "fixture") {
       std::cout << fixture_graphs().at(argv[2]);
       return 0;
