@@ -191,15 +191,19 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup if os.path.exists(REF_TOOL) else 0):
-        pass  # the reference's executor has no warm-up state; warm-up steps are not repeated on CPU
-    times = []
-    cb = None
+    # W untimed samples, then K timed samples (each: one bounded sample of the
+    # workload as independent instances on every host thread)
+    for _ in range(args.warmup):
+        time_reference_cpu(args.config, threads)
+    times, values, cb = [], [], None
     for _ in range(args.steps):
         cb, secs = time_reference_cpu(args.config, threads)
         times.append(secs)
+        values.append(cb["value"])
     ms = 1000.0 * sum(times) / len(times)
-    value = sum(cb_["value"] for cb_ in [cb]) if cb else 0.0
+    # throughput over the timed samples: total bytes / total time
+    value = sum(v * t for v, t in zip(values, times)) / sum(times)
+    cb = dict(cb, value=value)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
