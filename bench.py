@@ -383,10 +383,27 @@ def run_ours(args):
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
         avg = sum(s.elapsed_time(e) for s, e in ev) / reps
+        # context: a device copy of the same byte count (half read, half
+        # written) as one launch — the achievable single-launch time at this size
+        half = k.info["algorithmic_bytes"] // 8
+        cps = [(torch.empty(half, device=dev), torch.empty(half, device=dev)) for _ in range(2)]
+        for i in range(2):
+            with torch.cuda.stream(stream):
+                cps[i % 2][1].copy_(cps[i % 2][0])
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        with torch.cuda.stream(stream):
+            for i in range(reps):
+                cev[i][0].record(stream)
+                cps[i % 2][1].copy_(cps[i % 2][0])
+                cev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        copy_ms = sum(s.elapsed_time(e) for s, e in cev) / reps
+        del cps
         per_kernel.append({"group": k.program.fusion_root, "kernel": k.info["entry"],
                            "strategy": k.info["strategy"], "ms": avg,
                            "bytes": k.info["algorithmic_bytes"],
                            "gbs": k.info["algorithmic_bytes"] / (avg * 1e-3) / 1e9,
+                           "same_size_copy_ms": copy_ms, "vs_same_size_copy": copy_ms / avg,
                            "grid": k.info["grid"], "block": k.info["block"], "regs": k.info["registers"]})
 
     # end-to-end through the reference-facing host-buffer call (TensorValue in/out)

@@ -931,7 +931,8 @@ std::set<int> row_local_inputs(const Ctx& c, const RowPlan& rp) {
 // per iteration; the row-local [R, C] inputs of the next NBUF rows are
 // streamed into shared memory by cp.async.bulk (the TMA engine) and tracked by
 // an mbarrier per stage, so HBM reads run continuously behind the arithmetic.
-KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs) {
+KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs,
+                            const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "row";
   ks.entry = "sfx_rowp_" + c.name;
@@ -939,13 +940,16 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
   const int64_t R = rp.R, C = rp.C;
   const int V = 4, TPR = 32;
   const int64_t NCH = C / (TPR * V);
-  const int WARPS = 4, NBUF = 2;
+  const int WARPS = o.pipe_warps > 0 ? std::min(o.pipe_warps, 32) : 4;
+  const int NBUF = o.pipe_stages > 0 ? std::min(o.pipe_stages, 8) : 2;
   std::vector<int> staged(staged_inputs.begin(), staged_inputs.end());
   const int64_t row_bytes = C * 4;
   const int64_t stage_bytes = row_bytes * static_cast<int64_t>(staged.size());
   const int64_t data_bytes = WARPS * NBUF * stage_bytes;
   const int smem = static_cast<int>(data_bytes + WARPS * NBUF * 8);
-  const int ctas_per_sm = std::max(1, std::min<int>(8, static_cast<int>((220 * 1024) / smem)));
+  if (smem > 227 * 1024) throw Error(SFX_ERR_UNSUPPORTED, "TMA row pipeline stages exceed shared memory");
+  int ctas_per_sm = std::max(1, std::min<int>(8, static_cast<int>((220 * 1024) / smem)));
+  if (o.pipe_ctas_per_sm > 0) ctas_per_sm = std::min(ctas_per_sm, o.pipe_ctas_per_sm);
   const int64_t grid = std::min<int64_t>((R + WARPS - 1) / WARPS, int64_t{kNumSMs} * ctas_per_sm);
 
   Emitter em(c.g, c.p, V, c.wide);
@@ -1482,7 +1486,7 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
                      4 * 2 * rp.C * 4 * static_cast<int64_t>(staged.size()) <= 200 * 1024 &&
                      o.threads_per_row == 0 && o.rows_per_cta == 0;
       if (pipe_ok && o.row_pipeline == 2)
-        ks = lower_row_pipe(c, rp, staged);
+        ks = lower_row_pipe(c, rp, staged, o);
       else
         ks = lower_row(c, rp, o);
       break;

@@ -91,7 +91,8 @@ class SfxGraphDesc(C.Structure):
 
 class SfxCompileOpts(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("debug_checks", C.c_int32), ("rows_per_cta", C.c_int32),
-                ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32), ("row_pipeline", C.c_int32)]
+                ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32), ("row_pipeline", C.c_int32),
+                ("pipe_warps", C.c_int32), ("pipe_stages", C.c_int32), ("pipe_ctas_per_sm", C.c_int32)]
 
 
 class SfxKernelInfo(C.Structure):
@@ -403,8 +404,10 @@ class GraphDesc:
         return C.byref(self.desc)
 
 
-def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0):
-    return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline)
+def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0,
+                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0):
+    return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline,
+                          pipe_warps, pipe_stages, pipe_ctas_per_sm)
 
 
 def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):

@@ -79,10 +79,27 @@ def main():
             ms = sorted(a.elapsed_time(b) for a, b in ev)
             med = ms[len(ms) // 2]
             gbs = k.info["algorithmic_bytes"] / (med * 1e-3) / 1e9
+            # same-size copy (torch copy_ of half the algorithmic bytes each way),
+            # the achievable single-launch bandwidth at this size
+            half = k.info["algorithmic_bytes"] // 8
+            cps = [(torch.empty(half, device=dev), torch.empty(half, device=dev)) for _ in range(nsets)]
+            for i in range(3):
+                cps[i % nsets][1].copy_(cps[i % nsets][0])
+            cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+            cs = torch.cuda.current_stream()
+            for i in range(reps):
+                cev[i][0].record(cs)
+                cps[i % nsets][1].copy_(cps[i % nsets][0])
+                cev[i][1].record(cs)
+            torch.cuda.synchronize()
+            cmed = sorted(a.elapsed_time(b) for a, b in cev)[reps // 2]
+            del cps
             print(json.dumps({"config": cfg, "variant": var, "group": kp.program.fusion_root,
                               "kernel": k.info["entry"], "regs": k.info["registers"], "grid": k.info["grid"],
                               "smem": k.info["smem_bytes"], "median_us": round(med * 1e3, 2),
-                              "gbs": round(gbs), "frac": round(gbs / peak, 3), "parity_ok": ok}), flush=True)
+                              "gbs": round(gbs), "frac": round(gbs / peak, 3),
+                              "same_size_copy_us": round(cmed * 1e3, 2),
+                              "vs_same_size_copy": round(cmed / med, 3), "parity_ok": ok}), flush=True)
             k.close()
             del sets
 
