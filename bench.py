@@ -231,8 +231,14 @@ def run_ours(args):
     from paper_1811_05213_b200 import host as H
 
     ws, rank, local = dist_env()
+    # one process per GPU; the modulo only matters for smoke-testing the
+    # multi-rank path with more ranks than GPUs (--dist-backend gloo)
+    local = local % max(1, torch.cuda.device_count())
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = H.Context(local)
@@ -349,7 +355,8 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    ms_t = torch.tensor([ms], device=dev)
+    red_dev = dev if args.dist_backend == "nccl" else "cpu"
+    ms_t = torch.tensor([ms], device=red_dev)
     if ws > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -429,7 +436,7 @@ def run_ours(args):
     for _ in range(e2e_steps):
         e2e_step()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_t = torch.tensor([e2e_s], device=dev)
+    e2e_t = torch.tensor([e2e_s], device=red_dev)
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
@@ -492,6 +499,8 @@ def main():
     ap.add_argument("--config", default="C5", choices=sorted(WORKLOAD_NAMES))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for the barrier / max-over-ranks timing (nccl on GPUs)")
     ap.add_argument("--inflight", type=int, default=0,
                     help="independent graph instances in flight per GPU (0 = auto)")
     args = ap.parse_args()
