@@ -189,6 +189,72 @@ def test_column_reduce_is_deterministic_and_relaunchable(ctx):
     cg.close()
 
 
+def _special_inputs(g, seed):
+    """Inputs with NaN / +-inf / -0.0 sprinkled in, including at element 0 of
+    rows and columns (the reference's max/min fold keeps a NaN first element and
+    skips later NaNs, exec.cpp:47-48,196-201)."""
+    inputs = T.gen_inputs(g, seed, -1.0, 1.0)
+    rng = np.random.default_rng(seed)
+    for k, a in inputs.items():
+        if a.dtype != np.float32:
+            continue
+        flat = a.reshape(-1)
+        n = flat.size
+        idx = rng.choice(n, size=max(1, n // 50), replace=False)
+        flat[idx[0::4]] = np.nan
+        flat[idx[1::4]] = np.inf
+        flat[idx[2::4]] = -np.inf
+        flat[idx[3::4]] = -0.0
+        flat[0] = np.nan
+    return inputs
+
+
+@pytest.mark.parametrize("strategy", ["auto", "literal"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_special_values(ctx, name, strategy):
+    """NaN / inf propagation and the reference's NaN-first max fold, on device."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
+    inputs = _special_inputs(g, 3)
+    outs, launched, _ = _run(ctx, g, rep, inputs, strategy)
+    ref = T.interpret(g, inputs, 0)
+    for o in g.outputs:
+        got, want = outs[o], ref[o]
+        # NaN / inf positions must agree exactly; finite values within tolerance
+        assert np.array_equal(np.isnan(got), np.isnan(want)), o
+        assert np.array_equal(np.isinf(got) & (got > 0), np.isinf(want) & (want > 0)), o
+        fin = np.isfinite(want)
+        ref64 = T.interpret(g, inputs, 1)[o]
+        assert T.values_close(got[fin], want[fin]) or T.values_close(got[fin], ref64[fin]), o
+
+
+def test_max_reduce_nan_first_rule(ctx):
+    """Row and column max folds: a NaN first element wins, later NaNs are skipped."""
+    doc = {"instructions": [
+        {"id": "p", "op": "parameter", "shape": [64, 128]},
+        {"id": "rmax", "op": "reduce", "operands": ["p"], "shape": [64], "reduce_dims": [1], "reducer": "max"},
+        {"id": "cmin", "op": "reduce", "operands": ["p"], "shape": [128], "reduce_dims": [0], "reducer": "min"},
+        {"id": "r2", "op": "scale", "operands": ["rmax"], "shape": [64], "scalar": 2.0},
+        {"id": "c2", "op": "scale", "operands": ["cmin"], "shape": [128], "scalar": 2.0},
+    ], "outputs": ["r2", "c2"]}
+    g = H.graph_from_json(doc)
+    p = T.gen_tensor(5, 0, 64 * 128, "f32", -1.0, 1.0).reshape(64, 128)
+    p[::3, 0] = np.nan      # NaN first in every third row -> row max is NaN
+    p[1::3, 5] = np.nan     # NaN later in the row -> ignored
+    p[0, 1::2] = np.nan     # NaN first in odd columns -> column min is NaN
+    p[7, ::2] = np.nan      # later NaNs in even columns -> ignored
+    want = T.interpret(g, {"p": p}, 0)
+    for members, roots, red in ((["rmax", "r2"], ["r2"], "rmax"), (["cmin", "c2"], ["c2"], "cmin")):
+        prog = H.KernelProgram(roots[0], members, roots, 1, 64, (4 * g.at(red).numel() + 7) // 8 * 8,
+                               [{"kind": "materialize", "instr": red, "schedule": [0, 1, "row"], "dest": "shared",
+                                 "offset": 0, "bytes": 4 * g.at(red).numel()}, {"kind": "barrier"},
+                                {"kind": "materialize", "instr": roots[0], "schedule": [0, 1, "row"], "dest": "output",
+                                 "root_index": 0}])
+        for strategy in ("auto", "literal"):
+            (got,) = H.run_program(prog, g, {"p": p}, strategy=strategy, ctx=ctx)
+            assert np.array_equal(np.isnan(got), np.isnan(want[roots[0]])), (roots, strategy)
+            assert T.values_close(got, want[roots[0]]), (roots, strategy)
+
+
 EXTRA = sorted(f[:-5] for f in os.listdir(os.path.join(T.GOLDEN, "plans_extra")))
 
 
