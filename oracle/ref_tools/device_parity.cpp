@@ -14,7 +14,9 @@
 //   device_parity shrink [--literal]
 //        test_exec.cpp:139-155: lowered smem limits (shrunk plans) keep outputs
 // Prints one JSON line; exit 0 iff every eligible case passed.
+#include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <iostream>
 #include <random>
 #include <sstream>
@@ -25,6 +27,10 @@
 #include "stitchfuse/fixtures.hpp"
 #include "stitchfuse/pipeline.hpp"
 #include "support.hpp"
+
+extern "C" {
+#include "../sfx_oracle.h"
+}
 
 using namespace stitchfuse;
 using json = nlohmann::json;
@@ -45,14 +51,103 @@ struct Tally {
   }
 };
 
-bool compare(const TensorGraph& g, const std::map<InstrId, TensorValue>& ref,
-             const std::map<InstrId, TensorValue>& dev, std::string* why) {
-  for (const InstrId& o : g.outputs())
-    if (!testsupport::values_close(dev.at(o), ref.at(o), 1e-5)) {
-      *why = "output " + o;
-      return false;
+// fp64 restatement of the graph (oracle/sfx_oracle.c, mode 1) for the
+// reduction-order tolerance policy.
+std::map<InstrId, TensorValue> interpret_fp64(const TensorGraph& g, const std::map<InstrId, TensorValue>& inputs) {
+  const auto& ins = g.instructions();
+  std::map<InstrId, int32_t> index;
+  for (size_t i = 0; i < ins.size(); ++i) index[ins[i].id] = static_cast<int32_t>(i);
+  std::vector<sfx_instr> d(ins.size());
+  std::vector<TensorValue> vals(ins.size());
+  std::vector<void*> ptrs(ins.size());
+  for (size_t i = 0; i < ins.size(); ++i) {
+    const Instruction& in = ins[i];
+    sfx_instr& s = d[i];
+    std::memset(&s, 0, sizeof s);
+    s.id = in.id.c_str();
+    s.opcode = static_cast<int32_t>(in.opcode);
+    s.kind = static_cast<int32_t>(in.kind);
+    s.dtype = in.shape.etype == ElementType::F32 ? SFX_F32 : SFX_I32;
+    s.rank = static_cast<int32_t>(in.shape.rank());
+    for (int k = 0; k < s.rank; ++k) s.dims[k] = in.shape.dims[k];
+    s.n_operands = static_cast<int32_t>(in.operands.size());
+    for (int k = 0; k < s.n_operands && k < 3; ++k) s.operands[k] = index.at(in.operands[k]);
+    for (size_t k = 0; k < in.permutation.size(); ++k) s.permutation[k] = in.permutation[k];
+    s.n_dim_map = static_cast<int32_t>(in.broadcast_dim_map.size());
+    for (size_t k = 0; k < in.broadcast_dim_map.size(); ++k) s.broadcast_dim_map[k] = in.broadcast_dim_map[k];
+    s.n_reduce_dims = static_cast<int32_t>(in.reduce_dims.size());
+    for (size_t k = 0; k < in.reduce_dims.size(); ++k) s.reduce_dims[k] = in.reduce_dims[k];
+    s.reducer = static_cast<int32_t>(in.reducer);
+    s.scalar = in.scalar;
+    s.n_literal = static_cast<int64_t>(in.literal.size());
+    s.literal = in.literal.empty() ? nullptr : in.literal.data();
+    vals[i] = in.opcode == Opcode::Parameter ? inputs.at(in.id) : TensorValue::zeros(in.shape);
+    ptrs[i] = in.shape.etype == ElementType::F32 ? static_cast<void*>(vals[i].f32.data())
+                                                 : static_cast<void*>(vals[i].i32.data());
+  }
+  sfx_graph_desc gd{};
+  gd.n_instrs = static_cast<int32_t>(d.size());
+  gd.instrs = d.data();
+  if (sfx_oracle_interpret(&gd, ptrs.data(), 1) != 0) throw std::runtime_error(sfx_oracle_error());
+  std::map<InstrId, TensorValue> out;
+  for (const InstrId& o : g.outputs()) out[o] = vals[index.at(o)];
+  return out;
+}
+
+bool reduce_dependent(const TensorGraph& g, const InstrId& id, std::map<InstrId, bool>& memo) {
+  auto it = memo.find(id);
+  if (it != memo.end()) return it->second;
+  bool r = g.at(id).opcode == Opcode::Reduce;
+  for (const InstrId& op : g.at(id).operands) r = r || reduce_dependent(g, op, memo);
+  return memo[id] = r;
+}
+
+int g_via_fp64 = 0;  // outputs accepted by the reduction-order policy
+
+// The reference's own criterion (values_close vs interpret, 1e-5); outputs
+// downstream of a reduction may instead meet it against the fp64 restatement
+// (reduction-order differences allowed, BASELINE.json north_star).
+bool compare(const TensorGraph& g, const std::map<InstrId, TensorValue>& ref, const std::map<InstrId, TensorValue>& dev,
+             const std::map<InstrId, TensorValue>& inputs, std::string* why) {
+  std::map<InstrId, bool> memo;
+  std::map<InstrId, TensorValue> exact;
+  for (const InstrId& o : g.outputs()) {
+    if (testsupport::values_close(dev.at(o), ref.at(o), 1e-5)) continue;
+    if (reduce_dependent(g, o, memo)) {
+      if (exact.empty()) exact = interpret_fp64(g, inputs);
+      if (testsupport::values_close(dev.at(o), exact.at(o), 1e-5)) {
+        ++g_via_fp64;
+        continue;
+      }
     }
+    *why = "output " + o;
+    return false;
+  }
   return true;
+}
+
+// On failure with SFX_DUMP_DIR set: the graph, its inputs (parameters in
+// instruction order) and both executors' outputs, for offline analysis.
+void dump_case(const std::string& name, const TensorGraph& g, const std::map<InstrId, TensorValue>& inputs,
+               const std::map<InstrId, TensorValue>& ref, const std::map<InstrId, TensorValue>& dev) {
+  const char* dir = std::getenv("SFX_DUMP_DIR");
+  if (!dir) return;
+  std::string base = std::string(dir) + "/" + name;
+  for (char& ch : base)
+    if (ch == ' ') ch = '_';
+  std::ofstream(base + ".graph.json") << serialize_graph(g);
+  auto put = [](std::ofstream& f, const TensorValue& v) {
+    if (v.shape.etype == ElementType::F32) f.write(reinterpret_cast<const char*>(v.f32.data()), v.f32.size() * 4);
+    else f.write(reinterpret_cast<const char*>(v.i32.data()), v.i32.size() * 4);
+  };
+  std::ofstream fi(base + ".inputs.bin", std::ios::binary);
+  for (const Instruction& i : g.instructions())
+    if (i.opcode == Opcode::Parameter) put(fi, inputs.at(i.id));
+  std::ofstream fr(base + ".ref.bin", std::ios::binary), fd(base + ".dev.bin", std::ios::binary);
+  for (const InstrId& o : g.outputs()) {
+    put(fr, ref.at(o));
+    if (dev.count(o)) put(fd, dev.at(o));
+  }
 }
 
 void run_case(const std::string& name, const TensorGraph& g, const CompileReport& report,
@@ -67,8 +162,9 @@ void run_case(const std::string& name, const TensorGraph& g, const CompileReport
     if (launched != static_cast<long long>(report.kernels.size())) {
       t.fail(name + ": launched " + std::to_string(launched) + " kernels for " +
              std::to_string(report.kernels.size()) + " fused groups");
-    } else if (!compare(g, ref, dev, &why)) {
+    } else if (!compare(g, ref, dev, inputs, &why)) {
       t.fail(name + ": " + why);
+      dump_case(name, g, inputs, ref, dev);
     } else {
       ++t.passed;
     }
@@ -79,7 +175,7 @@ void run_case(const std::string& name, const TensorGraph& g, const CompileReport
 
 int finish(const std::string& mode, const Tally& t, int extra_skipped) {
   json line = {{"mode", mode}, {"cases", t.cases}, {"passed", t.passed}, {"skipped_ineligible", extra_skipped},
-               {"failures", t.failures}};
+               {"outputs_accepted_vs_fp64", g_via_fp64}, {"failures", t.failures}};
   std::cout << line.dump() << std::endl;
   return t.cases > 0 && t.passed == t.cases ? 0 : 1;
 }
