@@ -255,6 +255,28 @@ def test_max_reduce_nan_first_rule(ctx):
             assert T.values_close(got, want[roots[0]]), (roots, strategy)
 
 
+def test_cli_run_device(tmp_path, capsys):
+    """`run --device` with the reference CLI's inputs file (random_seed tensors
+    drawn like the reference): printed checksums match the oracle's."""
+    from paper_1811_05213_b200 import cli
+    plan = os.path.join(T.PLANS, "C5.small.json")
+    g, rep, b = H.load_bundle(plan)
+    spec = {p.id: {"shape": p.shape, "random_seed": 100 + i} for i, p in enumerate(g.parameters())}
+    f = tmp_path / "inputs.json"
+    f.write_text(__import__("json").dumps(spec))
+    assert cli.main(["run", plan, "--inputs", str(f)]) == 0
+    lines = [l for l in capsys.readouterr().out.splitlines() if "checksum=" in l]
+    assert len(lines) == len(g.outputs)
+    inputs = cli.load_inputs(str(f), g)
+    ref = T.interpret(g, inputs, 1)
+    for line in lines:
+        o = line.split()[0]
+        got = float(line.split("checksum=")[1])
+        want = cli.value_checksum(ref[o])
+        scale = float(np.abs(ref[o]).astype(np.float64).sum()) + 1.0
+        assert abs(got - want) <= 1e-5 * scale, (o, got, want)
+
+
 EXTRA = sorted(f[:-5] for f in os.listdir(os.path.join(T.GOLDEN, "plans_extra")))
 
 
