@@ -276,7 +276,7 @@ bool analyze_row(const Ctx& c, RowPlan* rp, std::string* why) {
 // ---- COL analysis ------------------------------------------------------------
 
 struct ColPlan {
-  int64_t R = 0, C = 0;  // R = reduced extent (rows), C = output elements (columns)
+  int64_t O = 0, R = 0, I = 0;  // [outer | reduced | inner] of every reduce operand
 };
 
 bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
@@ -290,17 +290,18 @@ bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
     std::vector<int64_t> rd = n.reduce_dims;
     std::sort(rd.begin(), rd.end());
     for (size_t i = 0; i < rd.size(); ++i)
-      if (rd[i] != static_cast<int64_t>(i)) return *why = "reduce " + n.id + " is not over leading dims", false;
-    int k = static_cast<int>(rd.size());
-    int64_t R = prod(in.dims, 0, k), C = prod(in.dims, k, in.dims.size());
+      if (rd[i] != rd[0] + static_cast<int64_t>(i)) return *why = "reduce " + n.id + " dims are not contiguous", false;
+    const int k0 = static_cast<int>(rd[0]), k1 = static_cast<int>(rd.back()) + 1;
+    int64_t O = prod(in.dims, 0, k0), R = prod(in.dims, k0, k1), I = prod(in.dims, k1, in.dims.size());
     if (cp->R == 0) {
+      cp->O = O;
       cp->R = R;
-      cp->C = C;
-    } else if (cp->R != R || cp->C != C) {
+      cp->I = I;
+    } else if (cp->O != O || cp->R != R || cp->I != I) {
       return *why = "column reductions with different geometry", false;
     }
   }
-  const int64_t R = cp->R, C = cp->C;
+  const int64_t R = cp->R, C = cp->O * cp->I;
   if (R <= 1) return *why = "degenerate column length", false;
   for (int m : c.topo) {
     const Node& n = g.nodes[m];
@@ -1025,20 +1026,56 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
 
 // ---- COL ------------------------------------------------------------------------
 
+// Components of a node of `dims` at position (o, r, i) of an [O | R | I]
+// iteration space (o outer, r reduced, i inner), through a clean prefix split
+// of the dims when there is one, else through the linear index (o*R + r)*I + i.
+std::vector<Ix> orc_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t O, int64_t R, int64_t I,
+                          const Ix& o, const Ix& r, const Ix& i) {
+  int k0 = prefix_split(dims, O);
+  int k1 = k0 < 0 ? -1 : prefix_split(dims, O * R);
+  if (k0 >= 0 && k1 >= k0 && prod(dims, k1, dims.size()) == I && prod(dims, k0, k1) == R) {
+    std::vector<int64_t> d0(dims.begin(), dims.begin() + k0), d1(dims.begin() + k0, dims.begin() + k1),
+        d2(dims.begin() + k1, dims.end());
+    std::vector<Ix> a = em.from_linear(o, d0), b = em.from_linear(r, d1), c = em.from_linear(i, d2);
+    a.insert(a.end(), b.begin(), b.end());
+    a.insert(a.end(), c.begin(), c.end());
+    return a;
+  }
+  std::string ob = em.ivar(Emitter::imul(em.ivar(Emitter::iadd(Emitter::imul(o.e, R), r.e)), I));
+  Ix L;
+  if (i.kind == IX_PLUS) {
+    L = em.lane_plus(em.ivar(Emitter::iadd(ob, i.base)));
+  } else {
+    L = em.uni(em.ivar(Emitter::iadd(ob, i.e)));
+    L.kind = i.kind;
+  }
+  return em.from_linear(L, dims);
+}
+
+// Column template generalised to [outer | reduced | inner]: the reduce
+// operand's reduced dims are contiguous; "columns" are the O x I kept elements
+// (C3: O = 1).  A warp covers CL column vectors x RL rows (RL > 1 when there are
+// fewer than 32 column vectors, e.g. full reductions), 8 warps stride the rows
+// of a stripe, stripes combine in a single launch (last-CTA ticket).
 KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "col";
   ks.entry = "sfx_col_" + c.name;
   fill_common(c, ks);
-  const int64_t R = cp.R, C = cp.C;
-  const int V = (C % 4 == 0) ? 4 : 1;
+  const int64_t O = cp.O, R = cp.R, I = cp.I, C = cp.O * cp.I;
+  const int V = (I % 4 == 0) ? 4 : 1;
+  const int64_t cvec = (C + V - 1) / V;
+  int CL = 1;
+  while (CL < 32 && CL < cvec) CL *= 2;
+  const int RL = 32 / CL;
   const int WARPS = 8, B = WARPS * 32;
-  const int64_t TC = 32 * V;
+  const int RSUB = WARPS * RL;  // row sub-streams per CTA
+  const int64_t TC = static_cast<int64_t>(CL) * V;
   const int64_t tiles = (C + TC - 1) / TC;
   // row stripes: ~4 CTAs per SM in one wave (col template reuses rows_per_cta
   // as a stripe-count override and items_per_thread as rows per iteration)
   int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, (kNumSMs * 4 + tiles - 1) / tiles);
-  S = std::min<int64_t>(S, std::max<int64_t>(1, R / 64));
+  S = std::min<int64_t>(S, std::max<int64_t>(1, R / (8 * RSUB)));
   S = std::min<int64_t>(S, 65535);
   const int64_t RS = (R + S - 1) / S;
   const int NR = static_cast<int>(c.reduces.size());
@@ -1057,6 +1094,11 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     const Node& rn = c.g.nodes[c.reduces[k]];
     return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
   };
+  auto fold_fn = [&](int k) -> const char* {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum" : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax"
+                                                                                          : "sfx_fold_pmin";
+  };
   std::vector<int64_t> part_word(NR);
   int64_t words = ticket_words;
   for (int k = 0; k < NR; ++k) {
@@ -1067,10 +1109,15 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   ks.workspace_bytes = words * 4;
 
   body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
-  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + lane * " + std::to_string(V) + ";");
+  body.line("const int cl = lane & " + std::to_string(CL - 1) + ", rl = lane / " + std::to_string(CL) + ";");
+  body.line("const int rsub = warp * " + std::to_string(RL) + " + rl;");
+  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cl * " + std::to_string(V) + ";");
   body.line("const bool cok = c0 < " + fmt_i(C) + ";");
   body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
   body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
+  // the column vector's outer / inner coordinates (a vector never crosses an
+  // outer index: I % V == 0)
+  body.line("const " + it + " co = c0 / " + fmt_i(I) + ", ci = c0 % " + fmt_i(I) + ";");
   std::vector<std::vector<std::string>> acc(NR, std::vector<std::string>(V));
   for (int k = 0; k < NR; ++k) {
     const Node& rn = c.g.nodes[c.reduces[k]];
@@ -1085,37 +1132,41 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   }
   std::vector<int> full_roots, col_roots;
   for (int r : c.p.roots) (c.dep.at(r) || c.g.nodes[r].numel() != R * C ? col_roots : full_roots).push_back(r);
+  auto inner_ix = [&](int lane) {
+    em.lane = lane;
+    return V == 1 ? em.uni("ci") : em.lane_plus("ci");
+  };
 
   // one row of this thread's column vector: elementwise roots stored, reduce
   // operands folded into the per-lane accumulators
   auto emit_row = [&](const std::string& r) {
-    Ix rix = em.uni(r);
-    std::string rbase = em.ivar(Emitter::imul(r, C));
+    Ix rix = em.uni(r), oix = em.uni("co");
     std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+    std::vector<std::vector<std::string>> faddr(full_roots.size(), std::vector<std::string>(V));
+    std::vector<bool> fvec(full_roots.size(), V == 4);
     for (int lane = 0; lane < V; ++lane) {
-      em.lane = lane;
-      Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
-      for (size_t k = 0; k < full_roots.size(); ++k)
-        fv[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rix, col));
+      Ix iix = inner_ix(lane);
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::vector<Ix> comps = orc_comps(em, c.g.nodes[full_roots[k]].dims, O, R, I, oix, rix, iix);
+        fv[k][lane] = em.value(full_roots[k], comps);
+        Ix L = em.linearize(comps, c.g.nodes[full_roots[k]].dims);
+        faddr[k][lane] = lane == 0 && L.kind == IX_PLUS ? L.base : L.e;
+        if (lane == 0 && L.kind != IX_PLUS) fvec[k] = false;
+      }
       for (int k = 0; k < NR; ++k) {
         const Node& rn = c.g.nodes[c.reduces[k]];
         const Node& in = c.g.nodes[rn.operands[0]];
-        std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rix, col));
-        const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
-                        : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
-        body.line(acc[k][lane] + " = " + f + "(" + acc[k][lane] + ", " + v + ");");
+        std::string v = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, oix, rix, iix));
+        body.line(acc[k][lane] + " = " + fold_fn(k) + "(" + acc[k][lane] + ", " + v + ");");
       }
     }
-    if (!full_roots.empty()) {
-      std::string addr = em.ivar(Emitter::iadd(rbase, "c0"));
-      for (size_t k = 0; k < full_roots.size(); ++k) {
-        std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
-        if (V == 4)
-          body.line("sfx_st4(" + out + " + " + addr + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
-                    ", " + fv[k][3] + ");");
-        else
-          body.line(out + "[" + addr + "] = " + fv[k][0] + ";");
-      }
+    for (size_t k = 0; k < full_roots.size(); ++k) {
+      std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+      if (fvec[k])
+        body.line("sfx_st4(" + out + " + " + faddr[k][0] + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
+                  ", " + fv[k][3] + ");");
+      else
+        for (int l = 0; l < V; ++l) body.line(out + "[" + faddr[k][l] + "] = " + fv[k][l] + ";");
     }
   };
   // UR rows per iteration, unguarded, so all their 128-bit loads are in flight
@@ -1123,20 +1174,19 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
   body.line("if (cok) {");
   body.indent++;
-  body.line(it + " r = r_begin + warp;");
-  body.line("for (; r + " + std::to_string((UR - 1) * WARPS) + " < r_end; r += " + std::to_string(UR * WARPS) +
-            ") {");
+  body.line(it + " r = r_begin + rsub;");
+  body.line("for (; r + " + std::to_string((UR - 1) * RSUB) + " < r_end; r += " + std::to_string(UR * RSUB) + ") {");
   body.indent++;
   em.push();
   for (int u = 0; u < UR; ++u) {
     std::string ru = "r" + std::to_string(u);
-    body.line("const " + it + " " + ru + " = r + " + std::to_string(u * WARPS) + ";");
+    body.line("const " + it + " " + ru + " = r + " + std::to_string(u * RSUB) + ";");
     emit_row(ru);
   }
   em.pop();
   body.indent--;
   body.line("}");
-  body.line("for (; r < r_end; r += " + std::to_string(WARPS) + ") {");
+  body.line("for (; r < r_end; r += " + std::to_string(RSUB) + ") {");
   body.indent++;
   em.push();
   emit_row("r");
@@ -1146,32 +1196,29 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   body.indent--;
   body.line("}");
 
-  // CTA combine through shared memory (deterministic warp order)
+  // CTA combine through shared memory (deterministic row-substream order)
   for (int k = 0; k < NR; ++k) {
     const std::string T = acc_t(k);
-    body.line("__shared__ " + T + " sp" + std::to_string(k) + "[" + std::to_string(WARPS) + "][" +
-              fmt_i(TC) + "];");
+    body.line("__shared__ " + T + " sp" + std::to_string(k) + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
     for (int l = 0; l < V; ++l)
-      body.line("sp" + std::to_string(k) + "[warp][lane * " + std::to_string(V) + " + " + std::to_string(l) +
+      body.line("sp" + std::to_string(k) + "[rsub][cl * " + std::to_string(V) + " + " + std::to_string(l) +
                 "] = " + acc[k][l] + ";");
   }
   body.line("__syncthreads();");
   body.line("unsigned* tickets = ws;");
-  body.line("if (warp == 0 && cok) {");
+  body.line("const bool lead = warp == 0 && rl == 0 && cok;");
+  body.line("if (lead) {");
   body.indent++;
   for (int k = 0; k < NR; ++k) {
-    const Node& rn = c.g.nodes[c.reduces[k]];
     const std::string T = acc_t(k);
-    const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
-                    : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
     std::string part = "part" + std::to_string(k);
     body.line(T + "* " + part + " = (" + T + "*)(ws + " + fmt_i(part_word[k]) + ");");
     for (int l = 0; l < V; ++l) {
-      std::string sidx = "lane * " + std::to_string(V) + " + " + std::to_string(l);
+      std::string sidx = "cl * " + std::to_string(V) + " + " + std::to_string(l);
       std::string t = em.fresh("t");
       body.line(T + " " + t + " = sp" + std::to_string(k) + "[0][" + sidx + "];");
-      for (int w = 1; w < WARPS; ++w)
-        body.line(t + " = " + f + "(" + t + ", sp" + std::to_string(k) + "[" + std::to_string(w) + "][" + sidx + "]);");
+      body.line("for (int w = 1; w < " + std::to_string(RSUB) + "; ++w) " + t + " = " + fold_fn(k) + "(" + t +
+                ", sp" + std::to_string(k) + "[w][" + sidx + "]);");
       body.line(part + "[(" + it + ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + "] = " + t + ";");
     }
   }
@@ -1185,15 +1232,13 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   body.line("if (!s_last) return;");
   body.line("__threadfence();");
   // finisher: ordered combine over stripes, then the column roots
-  body.line("if (warp == 0 && cok) {");
+  body.line("if (lead) {");
   body.indent++;
   em.push();
   std::map<int, std::vector<std::string>> total;
   for (int k = 0; k < NR; ++k) {
     const Node& rn = c.g.nodes[c.reduces[k]];
     const std::string T = acc_t(k);
-    const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
-                    : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
     std::string part = "fp" + std::to_string(k);
     body.line("const " + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(part_word[k]) + ") + c0;");
     std::vector<std::string> tv(V);
@@ -1203,7 +1248,7 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     }
     body.line("for (" + it + " s = 1; s < " + fmt_i(S) + "; ++s) {");
     for (int l = 0; l < V; ++l)
-      body.line("  " + tv[l] + " = " + f + "(" + tv[l] + ", __ldcg(" + part + " + s * " + fmt_i(C) + " + " +
+      body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcg(" + part + " + s * " + fmt_i(C) + " + " +
                 std::to_string(l) + "));");
     body.line("}");
     if (T == "double")
@@ -1216,9 +1261,8 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
       // sequential std::max/min fold semantics: a NaN first element wins
       const Node& in = c.g.nodes[rn.operands[0]];
       for (int l = 0; l < V; ++l) {
-        em.lane = l;
-        Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
-        std::string f0 = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, em.uni("0"), col));
+        Ix iix = inner_ix(l);
+        std::string f0 = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
         body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
       }
     }
@@ -1251,8 +1295,9 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   ks.grid_x = tiles;
   ks.grid_y = S;
   ks.vector_width = V;
-  ks.note = "reduced=" + std::to_string(R) + " cols=" + std::to_string(C) + " tiles=" + std::to_string(tiles) +
-            " stripes=" + std::to_string(S);
+  ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
+            " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " lanes(col x row)=" +
+            std::to_string(CL) + "x" + std::to_string(RL);
   return ks;
 }
 

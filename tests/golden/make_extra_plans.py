@@ -23,6 +23,26 @@ EXTRA = {
     "ln_r37_c2048": configs.c1_layernorm(R=37, C=2048),
     "softmax_r16_c16384": configs.c2_softmax(B=1, H=2, S=8, L=16384),
     "softmax_r24_c4096": configs.c2_softmax(B=2, H=3, S=4, L=4096),
+    # middle-axis and full reductions: the [outer | reduced | inner] column template
+    "midsum_16x4096x64": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [16, 4096, 64]},
+        {"id": "e", "op": "exp", "operands": ["x"], "shape": [16, 4096, 64]},
+        {"id": "s", "op": "reduce", "operands": ["e"], "shape": [16, 64], "reduce_dims": [1], "reducer": "sum"},
+        {"id": "y", "op": "scale", "operands": ["s"], "shape": [16, 64], "scalar": 0.5}], "outputs": ["y"]},
+    "midmax_7x999x3_i32": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [7, 999, 3], "dtype": "i32"},
+        {"id": "n", "op": "neg", "operands": ["x"], "shape": [7, 999, 3], "dtype": "i32"},
+        {"id": "m", "op": "reduce", "operands": ["n"], "shape": [7, 3], "reduce_dims": [1], "reducer": "max",
+         "dtype": "i32"}], "outputs": ["m"]},
+    "fullmax_1024x1000": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [1024, 1000]},
+        {"id": "m", "op": "reduce", "operands": ["x"], "shape": [], "reduce_dims": [0, 1], "reducer": "max"},
+        {"id": "y", "op": "neg", "operands": ["m"], "shape": []}], "outputs": ["y"]},
+    "fullsum_3x5000x7": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [3, 5000, 7]},
+        {"id": "t", "op": "tanh", "operands": ["x"], "shape": [3, 5000, 7]},
+        {"id": "s", "op": "reduce", "operands": ["t"], "shape": [], "reduce_dims": [0, 1, 2], "reducer": "sum"}],
+        "outputs": ["s"]},
 }
 
 
