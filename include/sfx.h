@@ -54,7 +54,7 @@ typedef int32_t sfx_status; /* 0 = ok */
 enum {
   SFX_OK = 0,
   SFX_ERR_INVALID = 1,     /* malformed descriptor / argument (ParseError-like) */
-  SFX_ERR_UNSUPPORTED = 2, /* op outside the device path (BatchMatMul, LibraryCall) */
+  SFX_ERR_UNSUPPORTED = 2, /* template forced where it does not apply; group shape outside the lowering */
   SFX_ERR_COMPILE = 3,     /* NVRTC / module load failure */
   SFX_ERR_CUDA = 4,        /* driver error */
   SFX_ERR_EXEC = 5,        /* ExecError analogue (missing external, ...) */
@@ -73,6 +73,9 @@ enum {
   SFX_EW_SQRT, SFX_EW_RSQRT
 };
 enum { SFX_REDUCE_SUM = 0, SFX_REDUCE_MAX, SFX_REDUCE_MIN }; /* Reducer (ir.hpp:75) */
+/* LibraryCall callee (Instruction.callee, ir.hpp:97), carried in sfx_instr.kind:
+ * "matmul" is executable (exec.cpp:207-209), "opaque" is a barrier only. */
+enum { SFX_CALLEE_MATMUL = 0, SFX_CALLEE_OPAQUE = 1 };
 enum { SFX_F32 = 0, SFX_I32 = 1 };                          /* ElementType (ir.hpp:19) */
 enum { SFX_SCHED_ROW = 0, SFX_SCHED_COL = 1 };               /* SchedType (schedule.hpp:22) */
 enum { SFX_STMT_MATERIALIZE = 0, SFX_STMT_BARRIER = 1, SFX_STMT_INLINE = 2 };
@@ -81,7 +84,7 @@ enum { SFX_DEST_SHARED = 0, SFX_DEST_OUTPUT = 1 };
 typedef struct sfx_instr {
   const char* id;
   int32_t opcode;
-  int32_t kind;     /* elementwise kind */
+  int32_t kind;     /* elementwise kind; SFX_CALLEE_* for library calls */
   int32_t dtype;
   int32_t rank;
   int64_t dims[SFX_MAX_RANK];
@@ -158,7 +161,7 @@ typedef struct sfx_graph sfx_graph;
 
 /* Kernel facts for logging / measurement. */
 typedef struct sfx_kernel_info {
-  const char* strategy;      /* "map" | "row" | "col" | "literal" */
+  const char* strategy;      /* "map" | "row" | "col" | "literal" | "dot" */
   const char* entry;         /* kernel symbol */
   int32_t n_inputs;
   int32_t n_outputs;
@@ -192,7 +195,8 @@ int64_t sfx_launch_count(sfx_ctx* ctx);
 sfx_status sfx_program_compile(sfx_ctx* ctx, const sfx_graph_desc* graph, int32_t program_index,
                                const sfx_compile_opts* opts, sfx_kernel** out);
 /* Lower + compile to a cubin only (no device needed); writes the CUDA source to
- * `source_out` (may be NULL) and the cubin path to `cubin_path_out` (may be NULL). */
+ * `source_out` (may be NULL) and the cubin path to `cubin_path_out` (may be NULL).
+ * program_index >= n_programs selects the unfused instructions, as in sfx_graph_kernel. */
 sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_index,
                                const sfx_compile_opts* opts, char* source_out, uint64_t source_cap,
                                char* cubin_path_out, uint64_t path_cap, char* strategy_out,
@@ -211,10 +215,16 @@ sfx_status sfx_graph_compile(sfx_ctx* ctx, const sfx_graph_desc* graph, const sf
 /* Parameter slots: graph Parameters in ascending id order.  Output slots: graph.outputs order. */
 sfx_status sfx_graph_param_instrs(sfx_graph* g, int32_t* out, int32_t cap, int32_t* n);
 sfx_status sfx_graph_kernel(sfx_graph* g, int32_t program_index, sfx_kernel** out);
+/* Kernels per run: n_programs planned groups + unfused instructions (see sfx_graph_run). */
+sfx_status sfx_graph_kernel_count(sfx_graph* g, int32_t* n_kernels, int32_t* n_programs);
 /* Device-resident run: params and outputs are device pointers; intermediates
  * between groups stay in HBM (pooled).  Launches one kernel per group in the
- * reference's condensation (Kahn) order.  use_cuda_graph=1 replays a captured
- * CUDA graph for this exact pointer set (captured on first use). */
+ * reference's condensation (Kahn) order, plus one per instruction the planner
+ * left unfused (matmul barriers — BatchMatMul with fuse_dot off, LibraryCall
+ * "matmul" — and stray shape ops; the reference runs them through eval_dense,
+ * pipeline.cpp:124-127); those are the kernels program_index >= n_programs of
+ * sfx_graph_kernel.  use_cuda_graph=1 replays
+ * a captured CUDA graph for this exact pointer set (captured on first use). */
 sfx_status sfx_graph_run(sfx_graph* g, const uint64_t* params, int32_t n_params,
                          const uint64_t* outputs, int32_t n_outputs, void* stream,
                          int32_t use_cuda_graph);

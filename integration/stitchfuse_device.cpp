@@ -55,6 +55,8 @@ struct Desc {
       s.id = in.id.c_str();
       s.opcode = static_cast<int32_t>(in.opcode);  // same enumerator order (ir.hpp:41-52)
       s.kind = static_cast<int32_t>(in.kind);      // ir.hpp:54-73
+      if (in.opcode == Opcode::LibraryCall)
+        s.kind = in.callee == "matmul" ? SFX_CALLEE_MATMUL : in.callee == "opaque" ? SFX_CALLEE_OPAQUE : -1;
       s.dtype = in.shape.etype == ElementType::F32 ? SFX_F32 : SFX_I32;
       if (in.shape.rank() > SFX_MAX_RANK) throw ExecError("rank above SFX_MAX_RANK: " + in.id);
       s.rank = static_cast<int32_t>(in.shape.rank());

@@ -37,10 +37,19 @@ using json = nlohmann::json;
 
 namespace {
 
+// Everything the reference can execute: only "opaque" library calls are not
+// (exec.cpp:207-209).
 bool eligible(const TensorGraph& g) {
   for (const Instruction& i : g.instructions())
-    if (i.opcode == Opcode::BatchMatMul || i.opcode == Opcode::LibraryCall) return false;
+    if (i.opcode == Opcode::LibraryCall && i.callee != "matmul") return false;
   return true;
+}
+
+// Launches per run_compiled: one per planned group plus one per unfused
+// instruction (matmul barriers and stray shape ops, which the reference
+// evaluates densely, pipeline.cpp:124-127).
+long long expected_launches(const CompileReport& report) {
+  return static_cast<long long>(report.kernels.size() + report.fusion.unfused.size());
 }
 
 struct Tally {
@@ -67,6 +76,7 @@ std::map<InstrId, TensorValue> interpret_fp64(const TensorGraph& g, const std::m
     s.id = in.id.c_str();
     s.opcode = static_cast<int32_t>(in.opcode);
     s.kind = static_cast<int32_t>(in.kind);
+    if (in.opcode == Opcode::LibraryCall) s.kind = in.callee == "matmul" ? SFX_CALLEE_MATMUL : SFX_CALLEE_OPAQUE;
     s.dtype = in.shape.etype == ElementType::F32 ? SFX_F32 : SFX_I32;
     s.rank = static_cast<int32_t>(in.shape.rank());
     for (int k = 0; k < s.rank; ++k) s.dims[k] = in.shape.dims[k];
@@ -159,9 +169,10 @@ void run_case(const std::string& name, const TensorGraph& g, const CompileReport
     auto dev = stitchfuse_device::run_compiled(report, g, inputs);
     long long launched = stitchfuse_device::launches() - before;
     std::string why;
-    if (launched != static_cast<long long>(report.kernels.size())) {
+    if (launched != expected_launches(report)) {
       t.fail(name + ": launched " + std::to_string(launched) + " kernels for " +
-             std::to_string(report.kernels.size()) + " fused groups");
+             std::to_string(report.kernels.size()) + " fused groups + " +
+             std::to_string(report.fusion.unfused.size()) + " unfused instructions");
     } else if (!compare(g, ref, dev, inputs, &why)) {
       t.fail(name + ": " + why);
       dump_case(name, g, inputs, ref, dev);

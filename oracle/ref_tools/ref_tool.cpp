@@ -119,9 +119,10 @@ CompileReport compile(const TensorGraph& g, const PipelineOptions& o) {
 }
 
 bool device_eligible(const TensorGraph& g, const CompileReport& r) {
-  // the device executor covers the non-MatMul path only
+  // everything the reference can execute: "opaque" library calls are
+  // barriers only (exec.cpp:207-209)
   for (const Instruction& i : g.instructions())
-    if (i.opcode == Opcode::BatchMatMul || i.opcode == Opcode::LibraryCall) return false;
+    if (i.opcode == Opcode::LibraryCall && i.callee != "matmul") return false;
   (void)r;
   return true;
 }

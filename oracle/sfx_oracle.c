@@ -282,8 +282,8 @@ static int eval(Ctx* c, int k) {
     case SFX_OP_LIBRARY_CALL: { /* matmul_element, exec.cpp:84-100 */
       const sfx_instr* lhs = &g->instrs[s->operands[0]];
       const sfx_instr* rhs = &g->instrs[s->operands[1]];
-      if (s->opcode == SFX_OP_LIBRARY_CALL && s->n_operands != 2)
-        return fail("library call is not executable:", s->id);
+      if (s->opcode == SFX_OP_LIBRARY_CALL && (s->kind != SFX_CALLEE_MATMUL || s->n_operands != 2))
+        return fail("library call is not executable:", s->id); /* exec.cpp:207-209 */
       int r = s->rank;
       int64_t K = lhs->dims[lhs->rank - 1];
       for (int64_t e = 0; e < n; ++e) {

@@ -126,7 +126,8 @@ struct sfx_kernel {
 struct sfx_graph {
   sfx_ctx* ctx = nullptr;
   sfx::Graph graph;
-  std::vector<sfx_kernel*> kernels;  // per program
+  std::vector<sfx_kernel*> kernels;  // per program: planned groups, then matmul barriers
+  int n_planned = 0;                 // programs that came from the CompileReport
   std::vector<int> order;            // program launch order (condensation Kahn order)
   std::vector<int> params;           // Parameter nodes, ascending id = param slot order
   std::map<int, CUdeviceptr> owned;  // intermediates + dense constants (device-resident)
@@ -210,6 +211,23 @@ void destroy_kernel(sfx_kernel* k) {
   } catch (...) {
   }
   delete k;
+}
+
+// Unfused instructions (fusion.cpp:259-263): the fusion barriers and any
+// instruction no group took; run_compiled evaluates each densely
+// (pipeline.cpp:124-127).  Each becomes one kernel, appended after the planned
+// groups in instruction order.
+void add_barrier_programs(sfx::Graph& g) {
+  std::vector<bool> in_group(g.nodes.size(), false);
+  for (const sfx::Program& p : g.programs)
+    for (int m : p.members) in_group[m] = true;
+  for (size_t i = 0; i < g.nodes.size(); ++i) {
+    const sfx::Node& n = g.nodes[i];
+    if (in_group[i] || n.op == SFX_OP_PARAMETER || n.op == SFX_OP_CONSTANT) continue;
+    if (n.op == SFX_OP_LIBRARY_CALL && n.kind != SFX_CALLEE_MATMUL)
+      throw sfx::Error(SFX_ERR_EXEC, "library call 'opaque' is not executable");  // exec.cpp:209
+    g.programs.push_back(sfx::barrier_program(g, static_cast<int>(i)));
+  }
 }
 
 // run_compiled's condensation order (reference pipeline.cpp:67-131): one node
@@ -428,6 +446,7 @@ sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_inde
                                char* strategy_out, uint64_t strategy_cap) {
   return guard([&] {
     sfx::Graph g = sfx::graph_from_desc(graph);
+    if (program_index >= static_cast<int32_t>(g.programs.size())) add_barrier_programs(g);
     sfx_compile_opts o{};
     if (opts) o = *opts;
     sfx::KernelSource ks = sfx::lower_program(g, program_index, o);
@@ -490,23 +509,11 @@ sfx_status sfx_graph_compile(sfx_ctx* ctx, const sfx_graph_desc* desc, const sfx
     auto G = std::make_unique<sfx_graph>();
     G->ctx = ctx;
     G->graph = sfx::graph_from_desc(desc);
+    G->n_planned = static_cast<int>(G->graph.programs.size());
+    add_barrier_programs(G->graph);
+    for (size_t i = 0; i < G->graph.nodes.size(); ++i)
+      if (G->graph.nodes[i].op == SFX_OP_PARAMETER) G->params.push_back(static_cast<int>(i));
     const sfx::Graph& g = G->graph;
-    std::vector<bool> in_group(g.nodes.size(), false);
-    for (const sfx::Program& p : g.programs)
-      for (int m : p.members) in_group[m] = true;
-    for (size_t i = 0; i < g.nodes.size(); ++i) {
-      const sfx::Node& n = g.nodes[i];
-      if (in_group[i]) continue;
-      if (n.op == SFX_OP_PARAMETER) {
-        G->params.push_back(static_cast<int>(i));
-      } else if (n.op != SFX_OP_CONSTANT) {
-        throw sfx::Error(SFX_ERR_UNSUPPORTED, "instruction " + n.id + " (" +
-                                                  (n.op == SFX_OP_BATCH_MATMUL || n.op == SFX_OP_LIBRARY_CALL
-                                                       ? "matmul barrier"
-                                                       : "standalone op") +
-                                                  ") is outside the device non-MatMul path");
-      }
-    }
     std::sort(G->params.begin(), G->params.end(), [&](int a, int b) { return g.nodes[a].id < g.nodes[b].id; });
     G->order = condensation_order(g);
     try {
@@ -578,6 +585,14 @@ sfx_status sfx_graph_kernel(sfx_graph* G, int32_t program_index, sfx_kernel** ou
     if (program_index < 0 || program_index >= static_cast<int32_t>(G->kernels.size()))
       throw sfx::Error(SFX_ERR_INVALID, "program index out of range");
     *out = G->kernels[program_index];
+  });
+}
+
+sfx_status sfx_graph_kernel_count(sfx_graph* G, int32_t* n_kernels, int32_t* n_programs) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    if (n_kernels) *n_kernels = static_cast<int32_t>(G->kernels.size());
+    if (n_programs) *n_programs = G->n_planned;
   });
 }
 

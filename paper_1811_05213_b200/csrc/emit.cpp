@@ -354,6 +354,33 @@ std::string Emitter::reduce_loop(int node, const std::vector<Ix>& comps) {
   return acc;
 }
 
+// matmul_element (exec.cpp:84-100): acc starts at 0, then acc = acc + a*b over
+// the contraction index in ascending order (two roundings per step, no FMA).
+std::string Emitter::dot_loop(int node, const std::vector<Ix>& comps) {
+  const Node& n = g.nodes[node];
+  const Node& a = g.nodes[n.operands[0]];
+  const int r = n.rank();
+  const int64_t K = a.dims[r - 1];
+  std::string acc = fresh("a");
+  std::string q = fresh("k");
+  code->line(std::string(ctype(n.dtype)) + " " + acc + " = " + (n.dtype == SFX_F32 ? "0.0f" : "0") + ";");
+  code->line("for (" + idx_t + " " + q + " = 0; " + q + " < " + fmt_i(K) + "; ++" + q + ") {");
+  code->indent++;
+  push();
+  int saved_lane = lane;
+  std::vector<Ix> li(comps.begin(), comps.end()), ri(comps.begin(), comps.end());
+  li[r - 1] = uni(q);
+  ri[r - 2] = uni(q);
+  std::string x = value(n.operands[0], li);
+  std::string y = value(n.operands[1], ri);
+  lane = saved_lane;
+  code->line(acc + " = sfx_add(" + acc + ", sfx_mul(" + x + ", " + y + "));");
+  pop();
+  code->indent--;
+  code->line("}");
+  return acc;
+}
+
 std::string Emitter::value(int node, const std::vector<Ix>& comps) {
   const Node& n = g.nodes[node];
   if (n.is_splat()) return n.dtype == SFX_F32 ? fmt_f32(n.literal[0]) : fmt_i(static_cast<int32_t>(n.literal[0]));
@@ -414,9 +441,8 @@ std::string Emitter::value(int node, const std::vector<Ix>& comps) {
       result = reduce_loop(node, comps);
       break;
     case SFX_OP_BATCH_MATMUL:
-    case SFX_OP_LIBRARY_CALL:
-      throw Error(SFX_ERR_UNSUPPORTED, "instruction " + n.id +
-                                           " (matmul) is outside the device non-MatMul path");
+      result = dot_loop(node, comps);
+      break;
     default:
       throw Error(SFX_ERR_INVALID, "cannot evaluate " + n.id + " inside a group");
   }

@@ -105,6 +105,7 @@ class Emitter {
  private:
   std::string load(int node, const std::vector<Ix>& comps);
   std::string reduce_loop(int node, const std::vector<Ix>& comps);
+  std::string dot_loop(int node, const std::vector<Ix>& comps);
   std::vector<std::map<std::string, std::string>> scopes_;
   int next_ = 0;
 };

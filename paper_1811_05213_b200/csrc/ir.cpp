@@ -103,9 +103,27 @@ void validate_node(const Graph& g, const Node& n) {
       if (n.reducer < 0 || n.reducer > SFX_REDUCE_MIN) bad("instruction " + n.id + ": bad reducer");
       break;
     }
-    case SFX_OP_BATCH_MATMUL:
     case SFX_OP_LIBRARY_CALL:
-      break;  // representable; rejected when a program needs to execute it
+      if (n.kind == SFX_CALLEE_OPAQUE) break;  // a barrier only (ir.cpp:316-317)
+      if (n.kind != SFX_CALLEE_MATMUL) bad("instruction " + n.id + ": unknown library callee");
+      [[fallthrough]];
+    case SFX_OP_BATCH_MATMUL: {
+      // reference ir.cpp:288-315: [..., M, K] x [..., K, N] -> [..., M, N]
+      const int min_rank = n.op == SFX_OP_BATCH_MATMUL ? 3 : 2;
+      if (n.operands.size() != 2) bad("instruction " + n.id + ": matmul expects 2 operands");
+      const Node& a = in(0);
+      const Node& b = in(1);
+      const int r = a.rank();
+      if (r < min_rank || b.rank() != r || n.rank() != r)
+        bad("instruction " + n.id + ": operand ranks must be equal and >= " + std::to_string(min_rank));
+      for (int i = 0; i < r - 2; ++i)
+        if (a.dims[i] != b.dims[i] || a.dims[i] != n.dims[i]) bad("instruction " + n.id + ": batch dims mismatch");
+      if (a.dims[r - 1] != b.dims[r - 2]) bad("instruction " + n.id + ": contraction extents mismatch");
+      if (n.dims[r - 2] != a.dims[r - 2] || n.dims[r - 1] != b.dims[r - 1])
+        bad("instruction " + n.id + ": output dims mismatch");
+      if (a.dtype != n.dtype || b.dtype != n.dtype) bad("instruction " + n.id + ": element type mismatch");
+      break;
+    }
     default:
       bad("instruction " + n.id + ": unknown opcode");
   }

@@ -60,6 +60,9 @@ struct Program {
   std::vector<Stmt> stmts;
   std::vector<int> externals;  // operands outside the group, ascending id (splats included)
   std::vector<int> inputs;     // externals minus splat constants = kernel input slots
+  // an unfused matmul barrier run as its own kernel (not a planned group;
+  // members = roots = {the matmul}, no statements)
+  bool barrier = false;
   bool is_member(int n) const { return member_set.count(n) > 0; }
 };
 

@@ -22,6 +22,7 @@ struct Ctx {
   const Program& p;
   std::vector<int> topo;
   std::vector<int> reduces;
+  std::vector<int> dots;  // BatchMatMul members (fuse_dot groups): literal tier only
   std::map<int, bool> dep;
   bool wide = false;
   std::string name;
@@ -53,9 +54,9 @@ Ctx make_ctx(const Graph& g, const Program& p) {
   for (int m : p.members) visit(m);
   for (int m : c.topo) {
     const Node& n = g.nodes[m];
-    if (n.op == SFX_OP_BATCH_MATMUL || n.op == SFX_OP_LIBRARY_CALL)
-      throw Error(SFX_ERR_UNSUPPORTED, "group member " + n.id +
-                                           " is a matmul; the device path covers non-MatMul groups only");
+    if (n.op == SFX_OP_LIBRARY_CALL)  // always a fusion barrier (span.cpp:35)
+      throw Error(SFX_ERR_INVALID, "group member " + n.id + " is a library call");
+    if (n.op == SFX_OP_BATCH_MATMUL) c.dots.push_back(m);
     bool d = n.op == SFX_OP_REDUCE;
     for (int op : n.operands)
       if (p.is_member(op) && c.dep[op]) d = true;
@@ -76,8 +77,6 @@ std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int b
   std::ostringstream os;
   os << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << entry << "(";
   bool first = true;
-  int64_t biggest_root = 0;
-  for (int r : c.p.roots) biggest_root = std::max(biggest_root, c.g.nodes[r].numel());
   for (size_t k = 0; k < c.p.inputs.size(); ++k) {
     int n = c.p.inputs[k];
     std::string name = "in" + std::to_string(k);
@@ -185,6 +184,7 @@ struct RowPlan {
 
 bool analyze_row(const Ctx& c, RowPlan* rp, std::string* why) {
   const Graph& g = c.g;
+  if (!c.dots.empty()) return *why = "group contains a matmul", false;
   if (c.reduces.empty()) return *why = "no reduction", false;
   for (int r : c.reduces) {
     const Node& n = g.nodes[r];
@@ -281,6 +281,7 @@ struct ColPlan {
 
 bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
   const Graph& g = c.g;
+  if (!c.dots.empty()) return *why = "group contains a matmul", false;
   if (c.reduces.empty()) return *why = "no reduction", false;
   for (int r : c.reduces) {
     const Node& n = g.nodes[r];
@@ -336,6 +337,7 @@ bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
 // ---- MAP -----------------------------------------------------------------------
 
 bool analyze_map(const Ctx& c, std::string* why) {
+  if (!c.dots.empty()) return *why = "group contains a matmul", false;
   if (!c.reduces.empty()) return *why = "group has reductions", false;
   return true;
 }
@@ -1477,6 +1479,7 @@ KernelSource lower_literal(const Ctx& c) {
 
 std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   const Program& p = g.programs.at(pi);
+  if (dot_alone(g, p)) return "dot";
   Ctx c = make_ctx(g, p);
   std::string w;
   if (analyze_map(c, &w)) return "map";
@@ -1498,11 +1501,13 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
 KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   if (pi < 0 || pi >= static_cast<int>(g.programs.size())) throw Error(SFX_ERR_INVALID, "program index out of range");
   const Program& p = g.programs[pi];
+  if (p.barrier && dot_alone(g, p)) return lower_dot(g, p);  // no other lowering for LibraryCall
   Ctx c = make_ctx(g, p);
   std::string why;
   int strat = o.strategy;
   if (strat == SFX_STRATEGY_AUTO) {
     std::string s = choose_strategy(g, pi, &why);
+    if (s == "dot") return lower_dot(g, p);
     strat = s == "map" ? SFX_STRATEGY_MAP : s == "row" ? SFX_STRATEGY_ROW : s == "col" ? SFX_STRATEGY_COL
                                                                                         : SFX_STRATEGY_LITERAL;
   }

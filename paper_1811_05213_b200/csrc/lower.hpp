@@ -14,6 +14,12 @@
 //             stripes, shared-memory partials, single-launch deterministic
 //             cross-CTA combine (last-CTA ticket), elementwise roots written in
 //             the same pass.
+//   dot     — a lone matmul: an unfused barrier (BatchMatMul with fuse_dot
+//             off, LibraryCall "matmul") that the reference runs through
+//             eval_dense, or a fuse_dot group with nothing else in it:
+//             register-tiled SIMT kernel, bit-exact k order (dot.cpp).
+//             Groups that stitch other members to a BatchMatMul run on the
+//             literal tier.
 //   literal — any plan the reference emits: the KernelProgram executed as
 //             written (reference blocks/chunk_box/arena/barriers, reference
 //             fold order) with the arena in shared memory.  Correctness tier.
@@ -48,6 +54,17 @@ KernelSource lower_program(const Graph& g, int program_index, const sfx_compile_
 // Strategy the analyzer would pick (without generating code), with the reason
 // the faster templates were rejected.
 std::string choose_strategy(const Graph& g, int program_index, std::string* why);
+
+// The matmul barrier kernel (dot.cpp).
+KernelSource lower_dot(const Graph& g, const Program& p);
+
+// A program whose only member is a matmul: an unfused barrier, or a fuse_dot
+// group with nothing stitched to the BatchMatMul.  Runs the dot kernel.
+bool dot_alone(const Graph& g, const Program& p);
+
+// Synthetic one-member program for an instruction the planner left unfused
+// (Program::barrier set; includes a literal-tier plan).
+Program barrier_program(const Graph& g, int node);
 
 extern const char* kPrelude;
 

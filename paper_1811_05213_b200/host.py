@@ -108,7 +108,7 @@ EXPORTS = [
     "sfx_host_alloc", "sfx_host_free", "sfx_memcpy_h2d", "sfx_memcpy_d2h", "sfx_memset_d32",
     "sfx_stream_sync", "sfx_launch_count", "sfx_program_compile", "sfx_program_codegen",
     "sfx_kernel_get_info", "sfx_kernel_input_instrs", "sfx_program_launch", "sfx_kernel_destroy",
-    "sfx_graph_compile", "sfx_graph_param_instrs", "sfx_graph_kernel", "sfx_graph_run",
+    "sfx_graph_compile", "sfx_graph_param_instrs", "sfx_graph_kernel", "sfx_graph_kernel_count", "sfx_graph_run",
     "sfx_graph_run_host", "sfx_graph_destroy", "sfx_nccl_unique_id", "sfx_nccl_init",
     "sfx_allreduce_sum_f32",
 ]
@@ -149,6 +149,7 @@ def lib():
         "sfx_graph_compile": (i32, [vp, C.POINTER(SfxGraphDesc), C.POINTER(SfxCompileOpts), C.POINTER(vp)]),
         "sfx_graph_param_instrs": (i32, [vp, C.POINTER(i32), i32, C.POINTER(i32)]),
         "sfx_graph_kernel": (i32, [vp, i32, C.POINTER(vp)]),
+        "sfx_graph_kernel_count": (i32, [vp, C.POINTER(i32), C.POINTER(i32)]),
         "sfx_graph_run": (i32, [vp, C.POINTER(u64), i32, C.POINTER(u64), i32, vp, i32]),
         "sfx_graph_run_host": (i32, [vp, C.POINTER(vp), i32, C.POINTER(vp), i32, vp]),
         "sfx_graph_destroy": (i32, [vp]),
@@ -343,7 +344,10 @@ class GraphDesc:
             self._keep.append(bid)
             s.id = bid
             s.opcode = OPCODES[ins.opcode]
-            s.kind = EW_KINDS.index(ins.op) if ins.op in EW_KINDS else 0
+            if ins.op == "library_call":  # SFX_CALLEE_*
+                s.kind = {"matmul": 0, "opaque": 1}.get(ins.callee, -1)
+            else:
+                s.kind = EW_KINDS.index(ins.op) if ins.op in EW_KINDS else 0
             s.dtype = 0 if ins.dtype == "f32" else 1
             if len(ins.shape) > MAX_RANK:
                 raise ExecError(f"rank of {ins.id} exceeds {MAX_RANK}", 1)
@@ -419,6 +423,20 @@ def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):
     strat = C.create_string_buffer(1024)
     opts = compile_opts(strategy, **kw)
     _check(lib().sfx_program_codegen(gd.ref(), 0, C.byref(opts), src, len(src), path, len(path), strat, len(strat)))
+    return src.value.decode(), path.value.decode(), strat.value.decode()
+
+
+def codegen_barrier(graph: TensorGraph, report: "CompileReport", k: int):
+    """Like codegen() for the k-th unfused matmul barrier of a compiled module
+    (instruction order), which runs as its own kernel."""
+    programs = [kk.program for kk in report.kernels]
+    gd = GraphDesc(graph, programs)
+    src = C.create_string_buffer(1 << 22)
+    path = C.create_string_buffer(4096)
+    strat = C.create_string_buffer(1024)
+    opts = compile_opts()
+    _check(lib().sfx_program_codegen(gd.ref(), len(programs) + k, C.byref(opts), src, len(src), path, len(path),
+                                     strat, len(strat)))
     return src.value.decode(), path.value.decode(), strat.value.decode()
 
 
@@ -549,6 +567,18 @@ class CompiledGraph:
             kh = C.c_void_p()
             _check(lib().sfx_graph_kernel(h, i, C.byref(kh)))
             self.kernels.append(Kernel._borrow(ctx, graph, k.program, kh))
+        # unfused matmul barriers (one kernel each, after the planned groups)
+        nk, npl = C.c_int32(), C.c_int32()
+        _check(lib().sfx_graph_kernel_count(h, C.byref(nk), C.byref(npl)))
+        self.barrier_kernels = []
+        for i in range(npl.value, nk.value):
+            kh = C.c_void_p()
+            _check(lib().sfx_graph_kernel(h, i, C.byref(kh)))
+            self.barrier_kernels.append(Kernel._borrow(ctx, graph, None, kh))
+
+    @property
+    def launches_per_run(self) -> int:
+        return len(self.kernels) + len(self.barrier_kernels)
 
     def run(self, param_ptrs, out_ptrs, stream=0, cuda_graph=False):
         ps = (C.c_uint64 * max(len(param_ptrs), 1))(*[int(p) for p in param_ptrs])

@@ -95,20 +95,59 @@ def test_random_graph_groups_lower_and_compile():
     assert n > 40
 
 
-def test_matmul_group_is_rejected_as_unsupported():
-    """fuse_dot groups contain BatchMatMul: outside the non-MatMul device path."""
+def test_matmul_groups_lower():
+    """fuse_dot groups: a lone BatchMatMul uses the dot kernel, a BatchMatMul
+    stitched to other members the literal tier (dot_loop in reference k order)."""
     d = T.load_json(os.path.join(T.GOLDEN, "random_acceptance.json"))
+    seen = set()
     for case in d["cases"]:
-        if case["bundle"]["options"]["fuse_dot"]:
+        if not case["bundle"]["options"]["fuse_dot"]:
+            continue
+        g = H.graph_from_json(case["bundle"]["graph"])
+        rep = H.CompileReport.from_bundle(case["bundle"])
+        for k in rep.kernels:
+            if not any(g.at(m).op == "batch_matmul" for m in k.program.members):
+                continue
+            _, cubin, note = H.codegen(g, k.program)
+            kind = "dot" if len(k.program.members) == 1 else "literal"
+            assert note.split()[0] == kind, note
+            seen.add(kind)
+    assert seen == {"dot", "literal"}
+
+
+def test_unfused_instructions_lower():
+    """Instructions no group took (run by the reference through eval_dense)
+    compile to one kernel each; matmuls to the dot kernel, whose fp32 loop has
+    no FFMA (two roundings per step, as matmul_element, exec.cpp:84-100)."""
+    n = {"dot": 0, "other": 0}
+    for stream in ("pipeline", "acceptance"):
+        d = T.load_json(os.path.join(T.GOLDEN, f"random_{stream}.json"))
+        for case in d["cases"]:
             g = H.graph_from_json(case["bundle"]["graph"])
             rep = H.CompileReport.from_bundle(case["bundle"])
-            for k in rep.kernels:
-                if any(g.at(m).op == "batch_matmul" for m in k.program.members):
-                    with pytest.raises(H.ExecError) as e:
-                        H.codegen(g, k.program)
-                    assert e.value.status == 2
-                    return
-    pytest.skip("no fused matmul group in the stream")
+            for k, u in enumerate(T.unfused_kernels(g, rep)):
+                src, cubin, note = H.codegen_barrier(g, rep, k)
+                if g.at(u).op in ("batch_matmul", "library_call"):
+                    assert note.startswith("dot matmul barrier"), note
+                    if g.at(u).dtype == "f32" and n["dot"] < 8:
+                        sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+                        assert "FMUL" in sass and "FFMA" not in sass
+                    n["dot"] += 1
+                else:
+                    n["other"] += 1
+    assert n["dot"] >= 20 and n["other"] >= 1, n
+
+
+def test_opaque_library_call_is_not_executable():
+    g = H.graph_from_json({"instructions": [
+        {"id": "a", "op": "parameter", "shape": [4, 8]},
+        {"id": "b", "op": "parameter", "shape": [8, 2]},
+        {"id": "c", "op": "library_call", "callee": "opaque", "operands": ["a", "b"], "shape": [4, 2]}],
+        "outputs": ["c"]})
+    rep = H.CompileReport([], 0, 0, 1.0, ["c"])
+    with pytest.raises(H.ExecError) as e:  # exec.cpp:207-209
+        H.codegen_barrier(g, rep, 0)
+    assert e.value.status == 5 and "not executable" in str(e.value)
 
 
 def test_malformed_program_is_rejected():

@@ -70,14 +70,19 @@ def _eligible(stream):
 @pytest.mark.parametrize("stream", ["pipeline", "acceptance", "device"])
 def test_random_graphs(ctx, stream, strategy):
     """test_pipeline.cpp:106-123 / acceptance criterion 2 (test_acceptance.cpp:41-62),
-    restricted to device-eligible graphs, through the device executor."""
+    through the device executor: fused groups, fuse_dot groups and the
+    unfused matmul barriers (every graph the reference can execute)."""
     failures, n = [], 0
     for case in _eligible(stream):
         g = H.graph_from_json(case["bundle"]["graph"])
         rep = H.CompileReport.from_bundle(case["bundle"])
         inputs = T.gen_inputs(g, case["input_seed"])
         outs, launched, _ = _run(ctx, g, rep, inputs, strategy)
-        assert launched == len(rep.kernels) == rep.fused_kernels
+        unfused = T.unfused_kernels(g, rep)
+        # one launch per planned group + one per unfused instruction; the
+        # reference counts the latter as kernels too, except library calls
+        assert launched == len(rep.kernels) + len(unfused)
+        assert rep.fused_kernels == len(rep.kernels) + sum(g.at(u).op != "library_call" for u in unfused)
         bad = _check(g, outs, inputs, literal=(strategy == "literal"))
         if bad:
             failures.append((case["bundle"]["stream"]["index"], bad))
