@@ -209,7 +209,9 @@ std::string Emitter::load(int node, const std::vector<Ix>& comps) {
   auto tt = tiled.find(node);
   if (tt != tiled.end()) {  // transposed tile in shared memory
     const Tile& t = tt->second;
-    std::string addr = t.arr + "[" + comps[t.jb].e + " - " + t.b0 + "][" + comps[t.ja].e + " - " + t.a0 + "]";
+    std::string B = t.mb ? imod(comps[t.jb].e, t.mb) : comps[t.jb].e;
+    std::string A = t.ma ? imod(idiv(comps[t.ja].e, t.sa), t.ma) : comps[t.ja].e;
+    std::string addr = t.arr + "[" + B + " - " + t.b0 + "][" + A + " - " + t.a0 + "]";
     std::string key = "tld:" + addr;
     std::string v = find(key);
     if (v.empty()) {

@@ -62,10 +62,12 @@ class Emitter {
   // (const float* smem pointer variable, linear index of the row's first element)
   std::map<int, std::pair<std::string, std::string>> staged;
   // externals staged as a transposed shared-memory tile: element at input comps
-  // c lives at arr[c[jb] - b0][c[ja] - a0]
+  // c lives at arr[B - b0][A - a0], B = c[jb] (or c[jb] % mb when that dim
+  // merges several root axes), A = c[ja] (or c[ja] / sa % ma)
   struct Tile {
     std::string arr, b0, a0;
     int jb = 0, ja = 0;
+    int64_t mb = 0, sa = 1, ma = 0;
   };
   std::map<int, Tile> tiled;
   // Strategy hook for member nodes: return a variable name to use instead of

@@ -446,13 +446,28 @@ KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
 // ---- MAP with shared-memory-tiled transposes ---------------------------------------
 
 // Symbolic index walk from the root: every dimension of every reached node is
-// labelled with the root axis it is indexed by ("$k"), "0" for a broadcast
-// constant, or "?" when a reshape mixes axes.  Returns, per external, the set
-// of distinct label vectors it is read with.
-std::map<int, std::set<std::vector<std::string>>> index_labels(const Ctx& c, int root) {
-  std::map<int, std::set<std::vector<std::string>>> ext;
-  std::set<std::pair<int, std::vector<std::string>>> seen;
-  std::function<void(int, const std::vector<std::string>&)> walk = [&](int n, const std::vector<std::string>& t) {
+// labelled with the root axes it is indexed by, as row-major components
+// (axis, extent) — one component for a plain axis, several where a reshape
+// merged root axes into one dimension (BERT's [T, Hd] = [B*S, NH*D] feeding
+// a head transpose), none for a unit dimension — or kUnknown when a reshape
+// splits an axis or an op mixes indices.  Returns, per external, the set of
+// distinct labellings it is read with.
+constexpr int kUnknown = -2;
+using DimLabel = std::vector<std::pair<int, int64_t>>;
+using Labels = std::vector<DimLabel>;
+
+bool labels_known(const Labels& t) {
+  for (const DimLabel& d : t)
+    for (auto& c : d)
+      if (c.first == kUnknown) return false;
+  return true;
+}
+
+std::map<int, std::set<Labels>> index_labels(const Ctx& c, int root) {
+  std::map<int, std::set<Labels>> ext;
+  std::set<std::pair<int, Labels>> seen;
+  auto unknown = [](int rank) { return Labels(rank, DimLabel{{kUnknown, 0}}); };
+  std::function<void(int, const Labels&)> walk = [&](int n, const Labels& t) {
     if (!seen.insert({n, t}).second) return;
     const Node& m = c.g.nodes[n];
     if (!c.p.is_member(n)) {
@@ -464,56 +479,62 @@ std::map<int, std::set<std::vector<std::string>>> index_labels(const Ctx& c, int
         for (int o : m.operands) walk(o, t);
         return;
       case SFX_OP_TRANSPOSE: {
-        std::vector<std::string> in(t.size());
+        Labels in(t.size());
         for (size_t i = 0; i < t.size(); ++i) in[m.perm[i]] = t[i];
         walk(m.operands[0], in);
         return;
       }
       case SFX_OP_BROADCAST: {
-        std::vector<std::string> in(m.dim_map.size());
+        Labels in(m.dim_map.size());
         for (size_t j = 0; j < m.dim_map.size(); ++j) in[j] = t[m.dim_map[j]];
         walk(m.operands[0], in);
         return;
       }
       case SFX_OP_RESHAPE:
       case SFX_OP_BITCAST: {
+        // row-major: the flattened component sequence is shared; regroup it
+        // into the operand's dims without splitting a component
         const Node& in = c.g.nodes[m.operands[0]];
-        std::vector<std::string> nz_t;
-        std::vector<int64_t> nz_out, nz_in;
-        for (int i = 0; i < m.rank(); ++i)
-          if (m.dims[i] != 1) nz_t.push_back(t[i]), nz_out.push_back(m.dims[i]);
-        for (int i = 0; i < in.rank(); ++i)
-          if (in.dims[i] != 1) nz_in.push_back(in.dims[i]);
-        std::vector<std::string> r(in.rank(), "?");
-        if (nz_in == nz_out) {  // only unit dims added or removed
-          for (int i = 0, k = 0; i < in.rank(); ++i) r[i] = in.dims[i] == 1 ? "0" : nz_t[k++];
+        if (!labels_known(t)) return walk(m.operands[0], unknown(in.rank()));
+        DimLabel seq;
+        for (const DimLabel& d : t) seq.insert(seq.end(), d.begin(), d.end());
+        Labels r(in.rank());
+        size_t k = 0;
+        for (int i = 0; i < in.rank(); ++i) {
+          int64_t need = in.dims[i], have = 1;
+          while (have < need && k < seq.size()) {
+            have *= seq[k].second;
+            r[i].push_back(seq[k++]);
+          }
+          if (have != need) return walk(m.operands[0], unknown(in.rank()));
         }
         walk(m.operands[0], r);
         return;
       }
       default: {
-        std::vector<std::string> q;
-        for (int o : m.operands) walk(o, std::vector<std::string>(c.g.nodes[o].rank(), "?"));
+        for (int o : m.operands) walk(o, unknown(c.g.nodes[o].rank()));
         return;
       }
     }
   };
-  std::vector<std::string> t;
-  for (int i = 0; i < c.g.nodes[root].rank(); ++i) t.push_back("$" + std::to_string(i));
+  Labels t;
+  const Node& rn = c.g.nodes[root];
+  for (int i = 0; i < rn.rank(); ++i) t.push_back(rn.dims[i] == 1 ? DimLabel{} : DimLabel{{i, rn.dims[i]}});
   walk(root, t);
   return ext;
 }
 
 struct TilePlan {
   int a = -1, b = -1;  // root axes: a = innermost (output-coalesced), b = input-innermost
-  std::map<int, std::pair<int, int>> inputs;  // external -> (jb, ja) input dims
+  std::map<int, Emitter::Tile> inputs;  // external -> where axes a and b sit in its index
+  std::map<int, Labels> labels;         // external -> its labelling
 };
 
 // A map group whose (single-shape) roots read a streamed input whose innermost
 // dimension is indexed by a root axis other than the root's innermost: the
 // naive kLoop would read it with a stride.  Tile (a, b) through shared memory.
 bool analyze_tiled(const Ctx& c, TilePlan* tp) {
-  if (!c.reduces.empty()) return false;
+  if (!c.reduces.empty() || !c.dots.empty()) return false;
   const std::vector<int64_t>& dims = c.g.nodes[c.p.roots[0]].dims;
   for (int r : c.p.roots)
     if (c.g.nodes[r].dims != dims) return false;
@@ -521,30 +542,47 @@ bool analyze_tiled(const Ctx& c, TilePlan* tp) {
   if (n < 2) return false;
   tp->a = n - 1;
   std::map<int, int> votes;
-  std::map<int, std::pair<int, int>> cand;  // external -> (jb, ja), with b per external
+  std::map<int, Emitter::Tile> cand;
   std::map<int, int> bof;
-  std::map<int, std::set<std::vector<std::string>>> merged;
+  std::map<int, std::set<Labels>> merged;
   for (int r : c.p.roots)
     for (auto& [e, ts] : index_labels(c, r)) merged[e].insert(ts.begin(), ts.end());
-  const std::string sa = "$" + std::to_string(tp->a);
   for (auto& [e, ts] : merged) {
     const Node& en = c.g.nodes[e];
-    if (ts.size() != 1 || en.rank() < 2 || en.numel() * 4 < (1 << 20)) continue;
-    const std::vector<std::string>& t = *ts.begin();
-    if (std::find(t.begin(), t.end(), "?") != t.end()) continue;
-    const std::string& last = t.back();
-    if (last == sa || last == "0") continue;
-    auto ja = std::find(t.begin(), t.end(), sa);
-    if (ja == t.end()) continue;
-    int b = std::stoi(last.substr(1));
-    cand[e] = {en.rank() - 1, static_cast<int>(ja - t.begin())};
-    bof[e] = b;
-    votes[b]++;
+    if (ts.size() != 1 || en.rank() < 1 || en.numel() * 4 < (1 << 20)) continue;
+    const Labels& t = *ts.begin();
+    if (!labels_known(t) || t.back().empty()) continue;
+    const std::pair<int, int64_t>& fastest = t.back().back();
+    if (fastest.first == tp->a) continue;  // already coalesced along the root's innermost axis
+    Emitter::Tile tile;
+    tile.jb = en.rank() - 1;
+    tile.mb = t.back().size() > 1 ? fastest.second : 0;
+    bool found = false;
+    for (int d = 0; d < en.rank() && !found; ++d) {
+      int64_t stride = 1;
+      for (int q = static_cast<int>(t[d].size()) - 1; q >= 0; --q) {
+        if (t[d][q].first == tp->a) {
+          tile.ja = d;
+          tile.sa = stride;
+          tile.ma = t[d].size() > 1 ? t[d][q].second : 0;
+          found = true;
+          break;
+        }
+        stride *= t[d][q].second;
+      }
+    }
+    if (!found || tile.ja == tile.jb) continue;
+    cand[e] = tile;
+    bof[e] = fastest.first;
+    votes[fastest.first]++;
   }
   if (votes.empty()) return false;
   tp->b = std::max_element(votes.begin(), votes.end(), [](auto& x, auto& y) { return x.second < y.second; })->first;
-  for (auto& [e, j] : cand)
-    if (bof[e] == tp->b) tp->inputs[e] = j;
+  for (auto& [e, tile] : cand)
+    if (bof[e] == tp->b) {
+      tp->inputs[e] = tile;
+      tp->labels[e] = *merged[e].begin();
+    }
   return !tp->inputs.empty();
 }
 
@@ -583,18 +621,17 @@ KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp) {
   };
   // load phase: each tiled input read along its own innermost dim (root axis b)
   int ti = 0;
-  for (auto& [e, j] : tp.inputs) {
+  for (auto& [e, tile] : tp.inputs) {
     const Node& en = c.g.nodes[e];
-    std::string arr = "tile" + std::to_string(ti++);
-    body.line(std::string("__shared__ ") + ctype(en.dtype) + " " + arr + "[32][33];");
-    em.tiled[e] = {arr, "b0", "a0", j.first, j.second};
+    Emitter::Tile t = tile;
+    t.arr = "tile" + std::to_string(ti++);
+    t.b0 = "b0";
+    t.a0 = "a0";
+    body.line(std::string("__shared__ ") + ctype(en.dtype) + " " + t.arr + "[32][33];");
+    em.tiled[e] = t;
   }
   // input comps for the load phase come from the label walk: rebuild them for
   // (a = a0 + ty + 8k, b = b0 + tx)
-  std::map<int, std::vector<std::string>> labels;
-  for (int r : c.p.roots)
-    for (auto& [e, ts] : index_labels(c, r))
-      if (tp.inputs.count(e)) labels[e] = *ts.begin();
   for (int k = 0; k < 4; ++k) {
     std::string av = em.fresh("la"), bv = em.fresh("lb");
     body.line("{");
@@ -605,12 +642,14 @@ KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp) {
     body.line("if (" + av + " < " + fmt_i(na) + " && " + bv + " < " + fmt_i(nb) + ") {");
     body.indent++;
     std::vector<Ix> rc = root_comps(av, bv);
-    for (auto& [e, j] : tp.inputs) {
+    for (auto& [e, tile] : tp.inputs) {
       const Node& en = c.g.nodes[e];
+      const Labels& lab = tp.labels.at(e);
       std::vector<Ix> ic(en.rank());
       for (int d = 0; d < en.rank(); ++d) {
-        const std::string& l = labels[e][d];
-        ic[d] = l == "0" ? em.uni("0") : rc[std::stoi(l.substr(1))];
+        std::string v = "0";
+        for (auto& [axis, ext] : lab[d]) v = Emitter::iadd(Emitter::imul(v, ext), rc[axis].e);
+        ic[d] = em.uni(em.ivar(v));
       }
       Ix L = em.linearize(ic, en.dims);
       body.line(em.tiled[e].arr + "[tx][ty + " + std::to_string(8 * k) + "] = sfx_ld(" + em.input_ptr.at(e) +

@@ -515,12 +515,14 @@ class Kernel:
         _check(lib().sfx_program_compile(ctx.h, self._gd.ref(), 0, C.byref(opts), C.byref(h)))
         self.h = h
         self._owned = True
+        self.roots = list(program.roots)
         self._load_info()
 
     @classmethod
     def _borrow(cls, ctx, graph, program, handle):
         k = cls.__new__(cls)
         k.ctx, k.graph, k.program, k.h, k._owned, k._gd = ctx, graph, program, handle, False, None
+        k.roots = list(program.roots) if program is not None else []
         k._load_info()
         return k
 
@@ -570,11 +572,16 @@ class CompiledGraph:
         # unfused matmul barriers (one kernel each, after the planned groups)
         nk, npl = C.c_int32(), C.c_int32()
         _check(lib().sfx_graph_kernel_count(h, C.byref(nk), C.byref(npl)))
+        unfused = set(report.unfused)
+        self.unfused_ids = [i.id for i in graph.instructions if i.id in unfused]  # C-side order
+        assert len(self.unfused_ids) == nk.value - npl.value
         self.barrier_kernels = []
-        for i in range(npl.value, nk.value):
+        for i, u in zip(range(npl.value, nk.value), self.unfused_ids):
             kh = C.c_void_p()
             _check(lib().sfx_graph_kernel(h, i, C.byref(kh)))
-            self.barrier_kernels.append(Kernel._borrow(ctx, graph, None, kh))
+            k = Kernel._borrow(ctx, graph, None, kh)
+            k.roots = [u]
+            self.barrier_kernels.append(k)
 
     @property
     def launches_per_run(self) -> int:

@@ -49,6 +49,9 @@ EXPECTED = {  # strategy the GroupAnalyzer must pick at full size
     ("C1", "y"): "row", ("C2", "y"): "row", ("C3", "db"): "col", ("C3b", "db"): "col",
     ("C3b", "dx_out"): "map", ("C4", "y"): "map", ("C4b", "y"): "map", ("C4t", "y"): "map", ("C5", "ctx_r"): "map",
     ("C5", "gelu"): "map", ("C5", "h1"): "row", ("C5", "h2"): "row", ("C5", "probs_d"): "row",
+    ("C5L", "h2"): "row", ("C5L", "gelu"): "map", ("C5L", "h1"): "row", ("C5L", "ctx_r"): "map",
+    ("C5L", "probs_d"): "map", ("C5L", "v_t"): "map", ("C5L", "sm.e"): "row", ("C5L", "k_t"): "map",
+    ("C5L", "q_t"): "map",
 }
 
 
@@ -56,7 +59,8 @@ EXPECTED = {  # strategy the GroupAnalyzer must pick at full size
 def test_workload_plans_lower_and_compile_for_sm100a(wl):
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, wl + ".json"))
     name, size = wl.split(".")
-    assert len(rep.kernels) == b["fused_kernels"]
+    unfused = T.unfused_kernels(g, rep)
+    assert len(rep.kernels) + sum(g.at(u).op != "library_call" for u in unfused) == b["fused_kernels"]
     for k in rep.kernels:
         for strategy in ("auto", "literal"):
             src, cubin, note = H.codegen(g, k.program, strategy)
@@ -64,6 +68,11 @@ def test_workload_plans_lower_and_compile_for_sm100a(wl):
             assert "extern \"C\" __global__" in src
             if strategy == "auto" and size == "full":
                 assert note.split()[0] == EXPECTED[(name, k.program.fusion_root)], note
+    for i, u in enumerate(unfused):
+        src, cubin, note = H.codegen_barrier(g, rep, i)
+        assert os.path.getsize(cubin) > 0
+        if g.at(u).op in ("batch_matmul", "library_call"):
+            assert note.startswith("dot"), note
 
 
 def test_full_size_streams_are_128bit():

@@ -195,6 +195,76 @@ def c5_bert(B=64, S=512, Hd=768, NH=12, FF=3072, Sq=None):
     return g.doc(["probs_d", "ctx_r", "h1", "gelu", "h2"])
 
 
+def c5_layer(B=64, S=512, Hd=768, NH=12, FF=3072):
+    """Extra (not a BASELINE.json config): the whole BERT-base encoder layer
+    with its matmuls as instructions — LibraryCall "matmul" for the dense
+    projections, BatchMatMul for the attention products — so the reference
+    planner chains the C5 groups through matmul barriers.
+    The non-matmul part is C5's graph; inputs are the hidden states x and the
+    weights, plus C5's attention mask and dropout masks."""
+    D = Hd // NH
+    T = B * S
+    att = [B, NH, S, S]
+    g = _G()
+    g.param("x", [T, Hd])
+    for w in ("q", "k", "v"):
+        g.param("W" + w, [Hd, Hd])
+        g.param("b" + w, [Hd])
+        g.add(w + "_mm", "library_call", ["x", "W" + w], [T, Hd], callee="matmul")
+        g.add("b%s_b" % w, "broadcast", ["b" + w], [T, Hd], broadcast_dim_map=[1])
+        g.add(w + "_b", "add", [w + "_mm", "b%s_b" % w], [T, Hd])
+        g.add(w + "_r", "reshape", [w + "_b"], [B, S, NH, D])
+    g.add("q_t", "transpose", ["q_r"], [B, NH, S, D], permutation=[0, 2, 1, 3])
+    g.add("k_t", "transpose", ["k_r"], [B, NH, D, S], permutation=[0, 2, 3, 1])
+    g.add("v_t", "transpose", ["v_r"], [B, NH, S, D], permutation=[0, 2, 1, 3])
+    g.add("scores", "batch_matmul", ["q_t", "k_t"], att)
+    g.param("amask", att)
+    g.param("dmask_a", att)
+    g.add("scores_s", "scale", ["scores"], att, scalar=0.125)
+    g.add("scores_m", "add", ["scores_s", "amask"], att)
+    _softmax(g, "scores_m", att, "sm.", "probs")
+    g.add("probs_d", "mul", ["probs", "dmask_a"], att)
+    g.add("ctx", "batch_matmul", ["probs_d", "v_t"], [B, NH, S, D])
+    g.add("ctx_t", "transpose", ["ctx"], [B, S, NH, D], permutation=[0, 2, 1, 3])
+    g.add("ctx_r", "reshape", ["ctx_t"], [T, Hd])
+    g.param("Wo", [Hd, Hd])
+    g.add("attn_o", "library_call", ["ctx_r", "Wo"], [T, Hd], callee="matmul")
+    for p in ("b_o", "g1", "be1"):
+        g.param(p, [Hd])
+    g.param("dmask_o", [T, Hd])
+    g.add("b_o_b", "broadcast", ["b_o"], [T, Hd], broadcast_dim_map=[1])
+    g.add("attn_ob", "add", ["attn_o", "b_o_b"], [T, Hd])
+    g.add("attn_od", "mul", ["attn_ob", "dmask_o"], [T, Hd])
+    g.add("res1", "add", ["attn_od", "x"], [T, Hd])
+    _layernorm(g, "res1", "g1", "be1", T, Hd, "ln1.", "h1")
+    g.param("W1", [Hd, FF])
+    g.param("b_f1", [FF])
+    g.add("ff1", "library_call", ["h1", "W1"], [T, FF], callee="matmul")
+    g.add("b_f1_b", "broadcast", ["b_f1"], [T, FF], broadcast_dim_map=[1])
+    g.add("u", "add", ["ff1", "b_f1_b"], [T, FF])
+    g.add("u2", "mul", ["u", "u"], [T, FF])
+    g.add("u3", "mul", ["u2", "u"], [T, FF])
+    g.add("u3s", "scale", ["u3"], [T, FF], scalar=0.044715)
+    g.add("inner", "add", ["u", "u3s"], [T, FF])
+    g.add("inner_s", "scale", ["inner"], [T, FF], scalar=0.7978845608028654)
+    g.add("th", "tanh", ["inner_s"], [T, FF])
+    g.add("one", "constant", [], [T, FF], value=1.0)
+    g.add("th1", "add", ["th", "one"], [T, FF])
+    g.add("half_u", "scale", ["u"], [T, FF], scalar=0.5)
+    g.add("gelu", "mul", ["half_u", "th1"], [T, FF])
+    g.param("W2", [FF, Hd])
+    g.add("ff2", "library_call", ["gelu", "W2"], [T, Hd], callee="matmul")
+    for p in ("b_f2", "g2", "be2"):
+        g.param(p, [Hd])
+    g.param("dmask_f", [T, Hd])
+    g.add("b_f2_b", "broadcast", ["b_f2"], [T, Hd], broadcast_dim_map=[1])
+    g.add("ff2b", "add", ["ff2", "b_f2_b"], [T, Hd])
+    g.add("ff2d", "mul", ["ff2b", "dmask_f"], [T, Hd])
+    g.add("res2", "add", ["ff2d", "h1"], [T, Hd])
+    _layernorm(g, "res2", "g2", "be2", T, Hd, "ln2.", "h2")
+    return g.doc(["h2"])
+
+
 BUILDERS = {
     "C1": c1_layernorm,
     "C2": c2_softmax,
@@ -204,6 +274,7 @@ BUILDERS = {
     "C4b": c4b_transpose,
     "C4t": c4t_transpose,
     "C5": c5_bert,
+    "C5L": c5_layer,
 }
 
 # Full sizes = BASELINE.json configs.  The small sizes are the CPU-oracle-sized
@@ -217,6 +288,7 @@ FULL = {
     "C4b": dict(B=32, S=512, H=16, D=64),
     "C4t": dict(B=32, S=512, H=16, D=64),
     "C5": dict(B=64, S=512),
+    "C5L": dict(B=64, S=512),
 }
 
 SMALL = {
@@ -228,6 +300,7 @@ SMALL = {
     "C4b": dict(B=2, S=64, H=16, D=64),
     "C4t": dict(B=2, S=64, H=16, D=64),
     "C5": dict(B=8, S=64),
+    "C5L": dict(B=2, S=64),
 }
 
 
