@@ -2,7 +2,8 @@
 oracle, on the reference's own plans.
 
 * Plan parity at execution time: exactly one launch per reference
-  FusedComputation (kernel count == CompileReport.fused_kernels).
+  FusedComputation, plus one per instruction the planner left unfused (the
+  reference's fused_kernels counts those too, except library calls).
 * Outputs with no reduction upstream: values_close(rel=1e-5) against the
   reference-semantics oracle (the reference's own criterion,
   tests/support.cpp:300-316); on the named configs also |d| <= 1e-6 + 1e-5|ref|.
