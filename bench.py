@@ -216,11 +216,15 @@ def run_reference_arm(args):
     return 0
 
 
-def config_obj(config, n):
+def config_obj(config, n, combine="peer"):
+    if config not in ("C3", "C3b") or n == 1:
+        par = f"batch-sharded independent graph instances x{n} (no collective)"
+    elif combine == "peer":
+        par = f"batch-sharded x{n}; column sums combined across ranks inside the column kernel (peer memory)"
+    else:
+        par = f"batch-sharded x{n} + NCCL all-reduce of the column sums"
     return {"workload": f"{config}: {WORKLOAD_NAMES[config]}", "plan": f"workloads/plans/{config}.full.json "
-            "(reference compile_graph, default PipelineOptions)", "instances_per_gpu": 1,
-            "parallelism": f"batch-sharded independent graph instances x{n} (no collective)" if config not in
-            ("C3", "C3b") or n == 1 else f"batch-sharded x{n} + NCCL all-reduce of the column sums"}
+            "(reference compile_graph, default PipelineOptions)", "instances_per_gpu": 1, "parallelism": par}
 
 
 # --------------------------------------------------------------------------- our arm
@@ -243,7 +247,14 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     ctx = H.Context(local)
     g, rep, bundle = H.load_bundle(plan_path(args.config))
-    cg = H.CompiledGraph(ctx, g, rep)
+    # the one batch-crossing exchange on this path is a column reduction over
+    # the batch (C3's db).  Default: the column kernel combines the ranks'
+    # partials itself through peer memory (cross_rank); --combine nccl runs
+    # the unfused baseline (kernel, then ncclAllReduce of the column sums).
+    peer = ws > 1 and args.combine == "peer"
+    if peer:
+        ctx.peer_init(rank, ws, H.torch_all_gather)
+    cg = H.CompiledGraph(ctx, g, rep, cross_rank=int(peer))
     kinfo = [k.info for k in cg.kernels]
     n_kernels = len(cg.kernels)
 
@@ -265,7 +276,7 @@ def run_ours(args):
     # the one batch-crossing exchange on this path: column sums (C3's db) of
     # every rank's batch shard are combined with an NCCL all-reduce of C floats
     colsum_outputs = []
-    if ws > 1:
+    if ws > 1 and not peer:
         for k in cg.kernels:
             if k.info["strategy"] == "col":
                 for r in k.program.roots:
@@ -466,7 +477,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand U(-1,1) inputs resident in HBM)",
-        "config": dict(config_obj(args.config, ws), **{
+        "config": dict(config_obj(args.config, ws, args.combine), **{
             "l2_policy": f"{nsets} rotating input/output set(s) of {per_set / 1e6:.1f} MB (> L2 {l2 / 1e6:.0f} MB)",
             "groups": n_kernels, "launches_per_graph": n_kernels,
             "instances_in_flight": inflight}),
@@ -501,6 +512,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for the barrier / max-over-ranks timing (nccl on GPUs)")
+    ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
+                    help="cross-rank column sums: fused into the column kernel over peer memory, or NCCL after it")
     ap.add_argument("--inflight", type=int, default=0,
                     help="independent graph instances in flight per GPU (0 = auto)")
     args = ap.parse_args()

@@ -48,7 +48,7 @@ extern "C" {
 #endif
 
 #define SFX_MAX_RANK 8
-#define SFX_ABI_VERSION 1
+#define SFX_ABI_VERSION 2
 
 typedef int32_t sfx_status; /* 0 = ok */
 enum {
@@ -153,6 +153,9 @@ typedef struct sfx_compile_opts {
   int32_t pipe_warps;       /* TMA row pipeline: warps per CTA (0 = auto) */
   int32_t pipe_stages;      /* TMA row pipeline: row buffers per warp (0 = auto) */
   int32_t pipe_ctas_per_sm; /* TMA row pipeline: persistent CTAs per SM (0 = auto) */
+  int32_t cross_rank;       /* 1 = this graph is one rank's batch shard: reductions over dim 0 combine
+                               across the context's peer group inside the column kernel (peer memory,
+                               see sfx_peer_*); other reductions over dim 0 are SFX_ERR_UNSUPPORTED */
 } sfx_compile_opts;
 
 typedef struct sfx_ctx sfx_ctx;
@@ -239,6 +242,23 @@ sfx_status sfx_graph_destroy(sfx_graph* g);
 sfx_status sfx_nccl_unique_id(void* id_out /* SFX_NCCL_ID_BYTES */);
 sfx_status sfx_nccl_init(sfx_ctx* ctx, const void* id, int32_t nranks, int32_t rank);
 sfx_status sfx_allreduce_sum_f32(sfx_ctx* ctx, uint64_t buf, uint64_t count, void* stream);
+
+/* Peer-memory group: the fused alternative to compute-then-allreduce.  Every
+ * rank allocates a symmetric peer arena (same size on every rank), exchanges
+ * the IPC handles out of band (torch.distributed / MPI / files) and opens the
+ * others'.  Column kernels compiled afterwards with cross_rank=1 then push
+ * their per-column partials into every rank's arena over NVLink (plain
+ * stores + a release flag per column tile) and fold the ranks in rank order
+ * inside the same launch, so all ranks get bit-identical results with no
+ * separate collective.  Arena regions are assigned in kernel build order, so
+ * every rank must compile the same graphs in the same order.  Replaces the
+ * ncclAllReduce that would follow the reference's column reduce
+ * (SURVEY §8(e)); the reference itself is single-process. */
+#define SFX_PEER_HANDLE_BYTES 64
+#define SFX_PEER_MAX_RANKS 8
+sfx_status sfx_peer_create(sfx_ctx* ctx, uint64_t bytes, void* handle_out /* SFX_PEER_HANDLE_BYTES */);
+sfx_status sfx_peer_open(sfx_ctx* ctx, const void* handles /* nranks x SFX_PEER_HANDLE_BYTES, rank order */,
+                         int32_t nranks, int32_t rank);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -86,6 +86,12 @@ struct sfx_ctx {
   std::multimap<uint64_t, CUdeviceptr> pool;  // freed blocks by size (buffer manager)
   std::map<CUdeviceptr, uint64_t> live;
   nccl_comm_t comm = nullptr;
+  // peer-memory group (sfx_peer_create / sfx_peer_open)
+  CUdeviceptr peer_base = 0;       // this rank's symmetric arena
+  uint64_t peer_bytes = 0, peer_used = 0;
+  CUdeviceptr peer_table = 0;      // device array [pn] of every rank's arena, mapped here
+  std::vector<CUdeviceptr> peer_opened;
+  int pn = 0, prank = 0;
 
   void bind() const { sfx::check_cu(sfx::driver().cuCtxSetCurrent(cu), "cuCtxSetCurrent"); }
 
@@ -119,6 +125,7 @@ struct sfx_kernel {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
   CUdeviceptr ws = 0;
+  uint64_t peer_off = 0;  // this kernel's region of the symmetric peer arena
   int regs = 0;
   std::string cubin_path;
 };
@@ -156,6 +163,16 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   if (k->src.smem > 48 * 1024)
     sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->src.smem),
                   "cuFuncSetAttribute(smem)");
+  if (k->src.peer_bytes > 0) {
+    // regions are handed out in build order, identical on every rank
+    if (!ctx->peer_table)
+      throw sfx::Error(SFX_ERR_INVALID, "cross_rank kernel " + k->src.entry + " needs sfx_peer_open first");
+    if (ctx->peer_used + static_cast<uint64_t>(k->src.peer_bytes) > ctx->peer_bytes)
+      throw sfx::Error(SFX_ERR_INVALID, "peer arena too small: " + std::to_string(ctx->peer_bytes) + " bytes, need " +
+                                            std::to_string(ctx->peer_used + k->src.peer_bytes));
+    k->peer_off = ctx->peer_used;
+    ctx->peer_used += static_cast<uint64_t>(k->src.peer_bytes);
+  }
   if (k->src.workspace_bytes > 0) {
     k->ws = ctx->alloc(static_cast<uint64_t>(k->src.workspace_bytes));
     sfx::check_cu(d.cuMemsetD32Async(k->ws, 0, (k->src.workspace_bytes + 3) / 4, nullptr), "cuMemsetD32Async");
@@ -182,6 +199,15 @@ void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector
   vals.push_back(k->ws);
   std::vector<void*> args(vals.size());
   for (size_t i = 0; i < vals.size(); ++i) args[i] = &vals[i];
+  CUdeviceptr peers = k->ctx->peer_table;
+  unsigned long long poff = k->peer_off;
+  int prank = k->ctx->prank, pn = k->ctx->pn;
+  if (k->src.peer_bytes > 0) {
+    args.push_back(&peers);
+    args.push_back(&poff);
+    args.push_back(&prank);
+    args.push_back(&pn);
+  }
   // programmatic dependent launch (every generated kernel begins with
   // griddepcontrol.wait, so stream order is preserved)
   CUlaunchAttribute attr[1];
@@ -366,6 +392,9 @@ sfx_status sfx_ctx_destroy(sfx_ctx* ctx) {
       ctx->bind();
       for (auto& [sz, p] : ctx->pool) sfx::driver().cuMemFree(p);
       for (auto& [p, sz] : ctx->live) sfx::driver().cuMemFree(p);
+      for (CUdeviceptr p : ctx->peer_opened) sfx::driver().cuIpcCloseMemHandle(p);
+      if (ctx->peer_table) sfx::driver().cuMemFree(ctx->peer_table);
+      if (ctx->peer_base) sfx::driver().cuMemFree(ctx->peer_base);
     } catch (...) {
     }
     delete ctx;
@@ -755,6 +784,56 @@ sfx_status sfx_allreduce_sum_f32(sfx_ctx* ctx, uint64_t buf, uint64_t count, voi
     check_nccl(nccl().AllReduce(reinterpret_cast<const void*>(buf), reinterpret_cast<void*>(buf), count, 7, 0,
                                 ctx->comm, static_cast<CUstream>(stream)),
                "ncclAllReduce");
+  });
+}
+
+sfx_status sfx_peer_create(sfx_ctx* ctx, uint64_t bytes, void* handle_out) {
+  return guard([&] {
+    if (!ctx || !handle_out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    if (ctx->peer_base) throw sfx::Error(SFX_ERR_INVALID, "peer arena already created");
+    static_assert(sizeof(CUipcMemHandle) == SFX_PEER_HANDLE_BYTES, "IPC handle size");
+    ctx->bind();
+    const sfx::Driver& d = sfx::driver();
+    bytes = std::max<uint64_t>(4096, (bytes + 4095) / 4096 * 4096);
+    // a dedicated allocation (not pooled): IPC exports whole allocations
+    sfx::check_cu(d.cuMemAlloc(&ctx->peer_base, bytes), "cuMemAlloc(peer arena)");
+    sfx::check_cu(d.cuMemsetD32Async(ctx->peer_base, 0, bytes / 4, nullptr), "cuMemsetD32Async");
+    sfx::check_cu(d.cuStreamSynchronize(nullptr), "cuStreamSynchronize");
+    CUipcMemHandle h;
+    sfx::check_cu(d.cuIpcGetMemHandle(&h, ctx->peer_base), "cuIpcGetMemHandle");
+    std::memcpy(handle_out, &h, sizeof(h));
+    ctx->peer_bytes = bytes;
+  });
+}
+
+sfx_status sfx_peer_open(sfx_ctx* ctx, const void* handles, int32_t nranks, int32_t rank) {
+  return guard([&] {
+    if (!ctx || !handles) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    if (!ctx->peer_base) throw sfx::Error(SFX_ERR_INVALID, "sfx_peer_create first");
+    if (ctx->peer_table) throw sfx::Error(SFX_ERR_INVALID, "peer group already open");
+    if (nranks < 1 || nranks > SFX_PEER_MAX_RANKS || rank < 0 || rank >= nranks)
+      throw sfx::Error(SFX_ERR_INVALID, "peer group of " + std::to_string(nranks) + " ranks (max " +
+                                            std::to_string(SFX_PEER_MAX_RANKS) + "), rank " + std::to_string(rank));
+    ctx->bind();
+    const sfx::Driver& d = sfx::driver();
+    std::vector<uint64_t> table(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) {
+        table[r] = ctx->peer_base;
+        continue;
+      }
+      CUipcMemHandle h;
+      std::memcpy(&h, static_cast<const char*>(handles) + static_cast<size_t>(r) * SFX_PEER_HANDLE_BYTES, sizeof(h));
+      CUdeviceptr p = 0;
+      sfx::check_cu(d.cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS),
+                    ("cuIpcOpenMemHandle(rank " + std::to_string(r) + ")").c_str());
+      ctx->peer_opened.push_back(p);
+      table[r] = p;
+    }
+    sfx::check_cu(d.cuMemAlloc(&ctx->peer_table, nranks * sizeof(uint64_t)), "cuMemAlloc(peer table)");
+    sfx::check_cu(d.cuMemcpyHtoD(ctx->peer_table, table.data(), nranks * sizeof(uint64_t)), "cuMemcpyHtoD");
+    ctx->pn = nranks;
+    ctx->prank = rank;
   });
 }
 

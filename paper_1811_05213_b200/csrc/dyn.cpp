@@ -70,6 +70,10 @@ const Driver& driver() {
     SFX_BIND(cuGraphLaunch)
     SFX_BIND(cuGraphExecDestroy)
     SFX_BIND(cuGraphDestroy)
+    SFX_BIND(cuIpcGetMemHandle)
+    SFX_BIND(cuIpcOpenMemHandle)
+    SFX_BIND(cuIpcCloseMemHandle)
+    SFX_BIND(cuMemcpyHtoD)
 #undef SFX_BIND
     if (err.empty()) {
       CUresult r = d.cuInit(0);

@@ -48,6 +48,10 @@ struct Driver {
   SFX_DRV(cuGraphLaunch)
   SFX_DRV(cuGraphExecDestroy)
   SFX_DRV(cuGraphDestroy)
+  SFX_DRV(cuIpcGetMemHandle)
+  SFX_DRV(cuIpcOpenMemHandle)
+  SFX_DRV(cuIpcCloseMemHandle)
+  SFX_DRV(cuMemcpyHtoD)
 #undef SFX_DRV
 };
 

@@ -25,6 +25,7 @@ struct Ctx {
   std::vector<int> dots;  // BatchMatMul members (fuse_dot groups): literal tier only
   std::map<int, bool> dep;
   bool wide = false;
+  bool peer = false;  // column sums combine across ranks (opts.cross_rank)
   std::string name;
   Ctx(const Graph& g_, const Program& p_) : g(g_), p(p_) {}
 };
@@ -89,7 +90,10 @@ std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int b
     os << (first ? "" : ", ") << ctype(c.g.nodes[c.p.roots[r]].dtype) << "* __restrict__ out" << r;
     first = false;
   }
-  os << (first ? "" : ", ") << "unsigned* __restrict__ ws)";
+  os << (first ? "" : ", ") << "unsigned* __restrict__ ws";
+  if (c.peer)
+    os << ", const unsigned long long* __restrict__ peers, unsigned long long poff, int prank, int pn";
+  os << ")";
   return os.str();
 }
 
@@ -1147,6 +1151,12 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     words += S * C * (acc_t(k) == "double" ? 2 : 1);
     words = (words + 63) / 64 * 64;
   }
+  const int64_t seq_word = words;
+  if (c.peer) {
+    words += (tiles + 63) / 64 * 64;
+    ks.peer_bytes = ((2LL * SFX_PEER_MAX_RANKS * NR * C + 2LL * NR * C) * 8 + tiles * SFX_PEER_MAX_RANKS * 4 + 255) /
+                    256 * 256;
+  }
   ks.workspace_bytes = words * 4;
 
   body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
@@ -1272,13 +1282,10 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   body.line("__syncthreads();");
   body.line("if (!s_last) return;");
   body.line("__threadfence();");
-  // finisher: ordered combine over stripes, then the column roots
-  body.line("if (lead) {");
-  body.indent++;
-  em.push();
-  std::map<int, std::vector<std::string>> total;
-  for (int k = 0; k < NR; ++k) {
-    const Node& rn = c.g.nodes[c.reduces[k]];
+  // finisher: ordered combine over stripes (then, with cross_rank, over ranks
+  // in rank order through peer memory), then the column roots
+  const std::string Cs = fmt_i(C);
+  auto stripe_total = [&](int k) {
     const std::string T = acc_t(k);
     std::string part = "fp" + std::to_string(k);
     body.line("const " + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(part_word[k]) + ") + c0;");
@@ -1289,24 +1296,112 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     }
     body.line("for (" + it + " s = 1; s < " + fmt_i(S) + "; ++s) {");
     for (int l = 0; l < V; ++l)
-      body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcg(" + part + " + s * " + fmt_i(C) + " + " +
+      body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcg(" + part + " + s * " + Cs + " + " +
                 std::to_string(l) + "));");
     body.line("}");
+    return tv;
+  };
+  // the sequential fold's first element (row 0 of the column; with
+  // cross_rank, row 0 of rank 0's shard)
+  auto first_elem = [&](int k, int l) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const Node& in = c.g.nodes[rn.operands[0]];
+    Ix iix = inner_ix(l);
+    return em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
+  };
+  auto needs_first = [&](int k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32;
+  };
+  std::map<int, std::vector<std::string>> total;
+  // peer arena layout (8-byte slots): data[2][PMAX][NR][C], first[2][NR][C],
+  // then flags[tiles][PMAX] (u32); local ws keeps one sequence word per tile
+  const int PMAX = SFX_PEER_MAX_RANKS;
+  const int64_t first_slot = 2LL * PMAX * NR * C;
+  const int64_t flag_byte = (first_slot + 2LL * NR * C) * 8;
+  if (c.peer) {
+    body.line("__shared__ unsigned s_seq;");
+    body.line("if (threadIdx.x == 0) { const unsigned q = ws[" + fmt_i(seq_word) +
+              " + blockIdx.x] + 1u; ws[" + fmt_i(seq_word) + " + blockIdx.x] = q; s_seq = q; }");
+    body.line("__syncthreads();");
+    body.line("const unsigned seq = s_seq;");
+    body.line("const long long par = seq & 1u;");
+    body.line("if (lead) {");
+    body.indent++;
+    em.push();
+    for (int k = 0; k < NR; ++k) {
+      const std::string T = acc_t(k);
+      std::vector<std::string> tv = stripe_total(k);
+      body.line("for (int p = 0; p < pn; ++p) {");
+      body.line("  unsigned long long* slot = (unsigned long long*)(peers[p] + poff) + ((par * " +
+                std::to_string(PMAX) + " + prank) * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs +
+                " + c0;");
+      for (int l = 0; l < V; ++l) body.line("  *(" + T + "*)(slot + " + std::to_string(l) + ") = " + tv[l] + ";");
+      if (needs_first(k)) {
+        body.line("  if (prank == 0) {");
+        body.line("    float* f = (float*)((unsigned long long*)(peers[p] + poff) + " + fmt_i(first_slot) +
+                  " + (par * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs + " + c0);");
+        for (int l = 0; l < V; ++l) body.line("    f[" + std::to_string(2 * l) + "] = " + first_elem(k, l) + ";");
+        body.line("  }");
+      }
+      body.line("}");
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.line("__threadfence_system();");
+    body.line("__syncthreads();");
+    body.line("if (threadIdx.x < pn) {");
+    body.line("  sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
+              std::to_string(PMAX) + " + prank, seq);");
+    body.line("  sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
+              std::to_string(PMAX) + " + threadIdx.x, seq);");
+    body.line("}");
+    body.line("__syncthreads();");
+  }
+  body.line("if (lead) {");
+  body.indent++;
+  em.push();
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const std::string T = acc_t(k);
+    std::vector<std::string> tv;
+    if (c.peer) {
+      // every rank folds the same slots in rank order: bit-identical results
+      body.line("const unsigned long long* xs" + std::to_string(k) + " = (const unsigned long long*)(peers[prank] + poff) + (par * " +
+                std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs + " + c0;");
+      tv.resize(V);
+      for (int l = 0; l < V; ++l) {
+        tv[l] = em.fresh("tot");
+        body.line(T + " " + tv[l] + " = __ldcv((const " + T + "*)(xs" + std::to_string(k) + " + " + std::to_string(l) +
+                  "));");
+      }
+      body.line("for (int q = 1; q < pn; ++q) {");
+      for (int l = 0; l < V; ++l)
+        body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcv((const " + T + "*)(xs" +
+                  std::to_string(k) + " + (long long)q * " + std::to_string(NR) + " * " + Cs + " + " +
+                  std::to_string(l) + ")));");
+      body.line("}");
+    } else {
+      tv = stripe_total(k);
+    }
     if (T == "double")
       for (int l = 0; l < V; ++l) {
         std::string fv32 = em.fresh("tot");
         body.line("const float " + fv32 + " = (float)" + tv[l] + ";");
         tv[l] = fv32;
       }
-    if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+    if (needs_first(k)) {
       // sequential std::max/min fold semantics: a NaN first element wins
-      const Node& in = c.g.nodes[rn.operands[0]];
       for (int l = 0; l < V; ++l) {
-        Ix iix = inner_ix(l);
-        std::string f0 = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
+        std::string f0 = c.peer ? "__ldcv((const float*)((const unsigned long long*)(peers[prank] + poff) + " +
+                                      fmt_i(first_slot) + " + (par * " + std::to_string(NR) + " + " +
+                                      std::to_string(k) + ") * " + Cs + " + c0 + " + std::to_string(l) + "))"
+                                : first_elem(k, l);
         body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
       }
     }
+    (void)rn;
     total[c.reduces[k]] = tv;
   }
   em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
@@ -1544,6 +1639,21 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   Ctx c = make_ctx(g, p);
   std::string why;
   int strat = o.strategy;
+  if (o.cross_rank) {
+    // the graph is one rank's batch shard: a reduction over dim 0 crosses ranks
+    // and only the column template knows how to combine across the peer group
+    for (int r : c.reduces)
+      for (int64_t d : g.nodes[r].reduce_dims)
+        if (d == 0) c.peer = true;
+    if (c.peer) {
+      ColPlan cp;
+      if ((strat != SFX_STRATEGY_AUTO && strat != SFX_STRATEGY_COL) || !analyze_col(c, &cp, &why))
+        throw Error(SFX_ERR_UNSUPPORTED, "group " + c.name +
+                                             " reduces over the sharded dim 0 but cannot use the column template"
+                                             " (cross-rank combine): " + (why.empty() ? "strategy forced" : why));
+      strat = SFX_STRATEGY_COL;
+    }
+  }
   if (strat == SFX_STRATEGY_AUTO) {
     std::string s = choose_strategy(g, pi, &why);
     if (s == "dot") return lower_dot(g, p);

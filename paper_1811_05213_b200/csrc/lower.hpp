@@ -40,6 +40,10 @@ struct KernelSource {
   int block = 256;
   int smem = 0;              // dynamic shared memory bytes
   int64_t workspace_bytes = 0;
+  // cross-rank column combine (opts.cross_rank): bytes of the symmetric peer
+  // arena this kernel needs; the kernel then takes (peers, peer_off, rank,
+  // nranks) after ws
+  int64_t peer_bytes = 0;
   std::vector<int> inputs;   // node ids per input slot (Program::inputs)
   std::vector<int> outputs;  // node ids per output slot (Program::roots)
   int64_t algorithmic_bytes = 0;

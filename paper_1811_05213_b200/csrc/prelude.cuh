@@ -96,6 +96,31 @@ __device__ __forceinline__ sfx_i4 sfx_ld4s(const int* p) {
 }
 __device__ __forceinline__ sfx_f4 sfx_lds4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
 
+// ---- cross-rank flags in peer memory (column combine over NVLink) ----
+__device__ __forceinline__ void sfx_st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned sfx_ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long sfx_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until a peer has published sequence number `seq` (wrap-safe).  A rank
+// that never arrives (crashed process, mismatched graphs) traps after 20 s
+// instead of hanging the GPU.
+__device__ __forceinline__ void sfx_peer_wait(const unsigned* flag, unsigned seq) {
+  const unsigned long long t0 = sfx_globaltimer();
+  while ((int)(sfx_ld_acquire_sys(flag) - seq) < 0) {
+    if (sfx_globaltimer() - t0 > 20000000000ull) __trap();
+    __nanosleep(64);
+  }
+}
+
 // ---- TMA bulk copies + mbarrier (sm_90+/sm_100a), used by the pipelined row template ----
 __device__ __forceinline__ unsigned sfx_smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -92,7 +92,8 @@ class SfxGraphDesc(C.Structure):
 class SfxCompileOpts(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("debug_checks", C.c_int32), ("rows_per_cta", C.c_int32),
                 ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32), ("row_pipeline", C.c_int32),
-                ("pipe_warps", C.c_int32), ("pipe_stages", C.c_int32), ("pipe_ctas_per_sm", C.c_int32)]
+                ("pipe_warps", C.c_int32), ("pipe_stages", C.c_int32), ("pipe_ctas_per_sm", C.c_int32),
+                ("cross_rank", C.c_int32)]
 
 
 class SfxKernelInfo(C.Structure):
@@ -110,8 +111,11 @@ EXPORTS = [
     "sfx_kernel_get_info", "sfx_kernel_input_instrs", "sfx_program_launch", "sfx_kernel_destroy",
     "sfx_graph_compile", "sfx_graph_param_instrs", "sfx_graph_kernel", "sfx_graph_kernel_count", "sfx_graph_run",
     "sfx_graph_run_host", "sfx_graph_destroy", "sfx_nccl_unique_id", "sfx_nccl_init",
-    "sfx_allreduce_sum_f32",
+    "sfx_allreduce_sum_f32", "sfx_peer_create", "sfx_peer_open",
 ]
+ABI_VERSION = 2
+PEER_HANDLE_BYTES = 64
+PEER_MAX_RANKS = 8
 
 _lib = None
 
@@ -156,11 +160,15 @@ def lib():
         "sfx_nccl_unique_id": (i32, [vp]),
         "sfx_nccl_init": (i32, [vp, vp, i32, i32]),
         "sfx_allreduce_sum_f32": (i32, [vp, u64, u64, vp]),
+        "sfx_peer_create": (i32, [vp, u64, vp]),
+        "sfx_peer_open": (i32, [vp, vp, i32, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
+    if L.sfx_abi_version() != ABI_VERSION:
+        raise ExecError(f"libsfx.so ABI {L.sfx_abi_version()} != {ABI_VERSION}; rebuild it", 3)
     _lib = L
     return L
 
@@ -409,9 +417,9 @@ class GraphDesc:
 
 
 def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0,
-                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0):
+                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0, cross_rank=0):
     return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline,
-                          pipe_warps, pipe_stages, pipe_ctas_per_sm)
+                          pipe_warps, pipe_stages, pipe_ctas_per_sm, int(bool(cross_rank)))
 
 
 def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):
@@ -486,6 +494,41 @@ class Context:
 
     def allreduce_sum_f32(self, dptr: int, count: int, stream=0):
         _check(lib().sfx_allreduce_sum_f32(self.h, int(dptr), int(count), C.c_void_p(stream)))
+
+
+    # ---- peer-memory group: column sums combined across ranks inside the kernel ----
+    def peer_create(self, nbytes=1 << 24) -> bytes:
+        """Allocates this rank's symmetric peer arena; returns its IPC handle."""
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        _check(lib().sfx_peer_create(self.h, int(nbytes), buf))
+        return buf.raw
+
+    def peer_open(self, handles, rank: int):
+        """Opens every rank's arena (handles in rank order, as exchanged out of band)."""
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != PEER_HANDLE_BYTES * len(handles):
+            raise ExecError("peer handles must be 64 bytes each", 1)
+        buf = C.create_string_buffer(blob, len(blob))
+        _check(lib().sfx_peer_open(self.h, buf, len(handles), rank))
+
+    def peer_init(self, rank: int, world: int, all_gather, nbytes=1 << 24):
+        """peer_create + exchange + peer_open; `all_gather(obj) -> list` is the
+        out-of-band exchange (e.g. torch.distributed.all_gather_object)."""
+        if world > PEER_MAX_RANKS:
+            raise ExecError(f"peer group of {world} ranks exceeds {PEER_MAX_RANKS}", 1)
+        mine = self.peer_create(nbytes)
+        handles = all_gather(mine)
+        if len(handles) != world or bytes(handles[rank]) != mine:
+            raise ExecError("peer handle exchange returned an inconsistent list", 1)
+        self.peer_open(handles, rank)
+
+
+def torch_all_gather(obj):
+    """all_gather for Context.peer_init over the default torch.distributed group."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
 
 
 def nccl_unique_id() -> bytes:
@@ -615,11 +658,11 @@ def _to_device(ctx, arr):
     return p
 
 
-def run_program(program: KernelProgram, graph: TensorGraph, externals: dict, strategy="auto", ctx=None):
+def run_program(program: KernelProgram, graph: TensorGraph, externals: dict, strategy="auto", ctx=None, **kw):
     """Device twin of stitchfuse::run_program (exec.cpp:296-412): one stitched
     launch; returns one array per root in comp.roots order."""
     ctx = ctx or default_context()
-    k = Kernel(ctx, graph, program, strategy)
+    k = Kernel(ctx, graph, program, strategy, **kw)
     ptrs = []
     try:
         ins = []

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", H.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sfx_\w+)", out))
     assert set(names) <= exported
-    assert L.sfx_abi_version() == 1
+    assert L.sfx_abi_version() == H.ABI_VERSION == 2
 
 
 def test_ctx_create_without_gpu_fails_loudly():
@@ -203,3 +203,23 @@ def test_innermost_moving_transpose_uses_smem_tiles():
     assert "smem-tiled" in note and "[32][33]" in src
     sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
     assert "STS" in sass and "LDS" in sass and "BAR.SYNC" in sass
+
+
+def test_cross_rank_rejects_non_column_batch_reduce():
+    """A reduction over the sharded dim 0 that the column template cannot take
+    fails loudly at compile time instead of silently reducing one shard."""
+    doc = {"instructions": [
+        {"id": "p", "op": "parameter", "shape": [64, 128]},
+        {"id": "s", "op": "reduce", "operands": ["p"], "shape": [128], "reduce_dims": [0], "reducer": "sum"},
+        {"id": "sb", "op": "broadcast", "operands": ["s"], "shape": [64, 128], "broadcast_dim_map": [1]},
+        {"id": "y", "op": "sub", "operands": ["p", "sb"], "shape": [64, 128]},
+    ], "outputs": ["y"]}
+    g = H.graph_from_json(doc)
+    prog = H.KernelProgram("y", ["s", "sb", "y"], ["y"], 1, 64, 512,
+                           [{"kind": "materialize", "instr": "s", "schedule": [0, 1, "row"], "dest": "shared",
+                             "offset": 0, "bytes": 512}, {"kind": "barrier"},
+                            {"kind": "inline", "instr": "sb"},
+                            {"kind": "materialize", "instr": "y", "schedule": [0, 1, "row"], "dest": "output",
+                             "root_index": 0}])
+    with pytest.raises(H.ExecError, match="sharded dim 0"):
+        H.codegen(g, prog, cross_rank=1)

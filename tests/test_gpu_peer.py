@@ -1,0 +1,168 @@
+"""Cross-rank column combine through peer memory (opts.cross_rank), on GPU.
+
+The batch-sharded path's one exchange is a column reduction over the batch
+(C3's db).  With cross_rank=1 the column kernel itself pushes each column
+tile's partial to every rank's peer arena and folds the ranks in rank order
+inside the same launch (no NCCL call).  The box has one GPU, so the two ranks
+here are two processes sharing cuda:0 through CUDA IPC — the same
+cuIpcOpenMemHandle path that maps a peer GPU's arena over NVLink on a
+multi-GPU node.  Handles are exchanged over gloo (127.0.0.1).
+
+Checks: every rank's db equals the fp64 restatement of the UNSHARDED graph
+(rows of all ranks) within the north_star bounds and is bit-identical across
+ranks; element roots (C3b's dx) stay rank-local; repeated launches and CUDA
+graph replays (the per-tile sequence numbers / double-buffered slots) stay
+correct with fresh inputs each time; the min fold keeps the reference's "NaN
+first element wins" rule where the first element is row 0 of rank 0.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import sfx_testlib as T
+from paper_1811_05213_b200 import host as H
+from workloads import configs
+
+pytestmark = pytest.mark.gpu
+
+WS = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard(seed, idx, n_rows, cols, rank):
+    return T.gen_tensor(seed, idx, n_rows * cols, "f32", -1.0, 1.0, offset=rank * n_rows * cols).reshape(n_rows, cols)
+
+
+def _worker(rank, ws, port, case, q):
+    import sys
+    sys.path.insert(0, T.ROOT)
+    sys.path.insert(0, os.path.join(T.ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        ctx = H.Context(0)
+        ctx.peer_init(rank, ws, H.torch_all_gather, nbytes=1 << 22)
+        out = []
+        if case in ("C3", "C3b"):
+            g, rep, _ = H.load_bundle(os.path.join(T.PLANS, f"{case}.small.json"))
+            n, c = g.at("dy").shape
+            cg = H.CompiledGraph(ctx, g, rep, cross_rank=1)
+            assert [k.info["strategy"] for k in cg.kernels][0] == "col"
+            before = ctx.launch_count()
+            for it in range(4):  # fresh inputs per launch: slots / sequence numbers rotate
+                inputs = {"dy": _shard(100 + it, 0, n, c, rank), "x": _shard(100 + it, 1, n, c, rank)}
+                res = cg.run_host(inputs)
+                out.append({o: res[o] for o in g.outputs})
+            assert ctx.launch_count() - before == 4 * cg.launches_per_run
+            # device-resident runs with CUDA-graph replay on one buffer set
+            import torch
+            dev = torch.device("cuda", 0)
+            ins = [torch.from_numpy(_shard(200, i, n, c, rank)).to(dev) for i in range(2)]
+            outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+            st = torch.cuda.Stream(device=dev)
+            for _ in range(3):
+                cg.run([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], stream=st.cuda_stream,
+                       cuda_graph=True)
+            st.synchronize()
+            out.append({o: t.cpu().numpy() for o, t in zip(g.outputs, outs)})
+            cg.close()
+        elif case == "min_nan":
+            g, prog, p = _min_program(rank)
+            (got,) = H.run_program(prog, g, {"p": p}, ctx=ctx, cross_rank=1)
+            out.append({"c2": got})
+        q.put((rank, out, None))
+    except Exception as e:  # report, don't hang the parent
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _min_rows(rank):
+    p = _shard(5, 0, 64, 128, rank).copy()
+    p[0, 1::2] = np.nan     # row 0 of this shard: only rank 0's is the global first element
+    p[9, ::4] = np.nan      # later NaNs: skipped
+    return p
+
+
+def _min_program(rank):
+    doc = {"instructions": [
+        {"id": "p", "op": "parameter", "shape": [64, 128]},
+        {"id": "cmin", "op": "reduce", "operands": ["p"], "shape": [128], "reduce_dims": [0], "reducer": "min"},
+        {"id": "c2", "op": "scale", "operands": ["cmin"], "shape": [128], "scalar": 2.0},
+    ], "outputs": ["c2"]}
+    g = H.graph_from_json(doc)
+    prog = H.KernelProgram("c2", ["cmin", "c2"], ["c2"], 1, 64, 512,
+                           [{"kind": "materialize", "instr": "cmin", "schedule": [0, 1, "row"], "dest": "shared",
+                             "offset": 0, "bytes": 512}, {"kind": "barrier"},
+                            {"kind": "materialize", "instr": "c2", "schedule": [0, 1, "row"], "dest": "output",
+                             "root_index": 0}])
+    return g, prog, _min_rows(rank)
+
+
+def _spawn(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, WS, port, case, q)) for r in range(WS)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(WS)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    for rank, out, err in res:
+        assert err is None, f"rank {rank}: {err}"
+    for p in procs:
+        assert p.exitcode == 0
+    return [out for _, out, _ in res]
+
+
+@pytest.mark.parametrize("case", ["C3", "C3b"])
+def test_cross_rank_column_sum(case):
+    g, _, _ = H.load_bundle(os.path.join(T.PLANS, f"{case}.small.json"))
+    n, c = g.at("dy").shape
+    outs = _spawn(case)
+    full = H.parse_graph(configs.c3_biasgrad(N=n * WS, C=c))
+    seeds = [100, 101, 102, 103, 200]
+    for i, seed in enumerate(seeds):
+        dy = np.concatenate([_shard(seed, 0, n, c, r) for r in range(WS)])
+        x = np.concatenate([_shard(seed, 1, n, c, r) for r in range(WS)])
+        ref = T.interpret(full, {"dy": dy, "x": x}, mode=1)["db"]
+        for r in range(WS):
+            db = outs[r][i]["db"]
+            assert T.strict_close(db, ref), (seed, r, T.mismatch_report(db, ref))
+            assert np.array_equal(db.view(np.uint32), outs[0][i]["db"].view(np.uint32))  # identical on all ranks
+            for o in g.outputs:  # element roots (C3b's dx_out) are rank-local
+                if o != "db":
+                    want = T.interpret(g, {"dy": dy[r * n:(r + 1) * n], "x": x[r * n:(r + 1) * n]}, 0)[o]
+                    assert T.strict_close(outs[r][i][o], want), (o, seed, r)
+
+
+def test_cross_rank_min_nan_first_rule():
+    outs = _spawn("min_nan")
+    g, _, _ = _min_program(0)
+    full_doc = {"instructions": [
+        {"id": "p", "op": "parameter", "shape": [64 * WS, 128]},
+        {"id": "cmin", "op": "reduce", "operands": ["p"], "shape": [128], "reduce_dims": [0], "reducer": "min"},
+        {"id": "c2", "op": "scale", "operands": ["cmin"], "shape": [128], "scalar": 2.0},
+    ], "outputs": ["c2"]}
+    full = H.graph_from_json(full_doc)
+    p = np.concatenate([_min_rows(r) for r in range(WS)])
+    want = T.interpret(full, {"p": p}, 0)["c2"]
+    assert np.isnan(want[1::2]).all() and not np.isnan(want[::2]).any()
+    for r in range(WS):
+        got = outs[r][0]["c2"]
+        assert np.array_equal(np.isnan(got), np.isnan(want)), r
+        assert T.values_close(got, want), r
