@@ -74,9 +74,11 @@ Ctx make_ctx(const Graph& g, const Program& p) {
 
 // ---- kernel scaffolding ---------------------------------------------------
 
-std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block) {
+std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block, int min_blocks = 0) {
   std::ostringstream os;
-  os << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << entry << "(";
+  os << "extern \"C\" __global__ void __launch_bounds__(" << block;
+  if (min_blocks > 0) os << ", " << min_blocks;
+  os << ") " << entry << "(";
   bool first = true;
   for (size_t k = 0; k < c.p.inputs.size(); ++k) {
     int n = c.p.inputs[k];
@@ -1117,16 +1119,23 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   const int RSUB = WARPS * RL;  // row sub-streams per CTA
   const int64_t TC = static_cast<int64_t>(CL) * V;
   const int64_t tiles = (C + TC - 1) / TC;
-  // row stripes: ~4 CTAs per SM in one wave (col template reuses rows_per_cta
-  // as a stripe-count override and items_per_thread as rows per iteration)
-  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, (kNumSMs * 4 + tiles - 1) / tiles);
+  // row stripes: 2 CTAs per SM in exactly one wave, each thread keeping 16
+  // rows x (streamed inputs) 128-bit loads in flight under a 128-register cap
+  // (__launch_bounds__(256, 2)).  Measured on C3 (tools/gpu_ab_col.sh): 4 CTAs/SM
+  // x 4 rows 94.5 us, 4 x 8 rows 88.5 us, 2 x 16 rows 84.3 us (0.99 of the
+  // measured copy peak; a torch read-only sum of the same bytes takes 94.6 us).
+  // The col template reuses rows_per_cta as a stripe-count override,
+  // items_per_thread as rows per iteration and pipe_ctas_per_sm as the
+  // residency target.
+  const int ctas_per_sm = o.pipe_ctas_per_sm > 0 ? o.pipe_ctas_per_sm : 2;
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / tiles);
   S = std::min<int64_t>(S, std::max<int64_t>(1, R / (8 * RSUB)));
   S = std::min<int64_t>(S, 65535);
   const int64_t RS = (R + S - 1) / S;
   const int NR = static_cast<int>(c.reduces.size());
 
   Emitter em(c.g, c.p, V, c.wide);
-  std::string sig = signature(c, em, ks.entry, B);
+  std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
   Code body;
   em.code = &body;
   const std::string& it = em.idx_t;
@@ -1222,7 +1231,7 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   };
   // UR rows per iteration, unguarded, so all their 128-bit loads are in flight
   // together; then the remainder one row at a time
-  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 32) : 16;
   body.line("if (cok) {");
   body.indent++;
   body.line(it + " r = r_begin + rsub;");
