@@ -156,6 +156,9 @@ typedef struct sfx_compile_opts {
   int32_t cross_rank;       /* 1 = this graph is one rank's batch shard: reductions over dim 0 combine
                                across the context's peer group inside the column kernel (peer memory,
                                see sfx_peer_*); other reductions over dim 0 are SFX_ERR_UNSUPPORTED */
+  int32_t host_stream;      /* 1 = row / map kernels carry the host-streaming gate and completion code
+                               (sfx_graph_run_host compiles these variants itself on first use; the
+                               device-path kernels stay free of it) */
 } sfx_compile_opts;
 
 typedef struct sfx_ctx sfx_ctx;

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -130,10 +131,41 @@ struct sfx_kernel {
   std::string cubin_path;
 };
 
+// host streaming: per kernel gate[kMaxChunks] (set to 1 when chunk j's inputs
+// landed) then done[kMaxChunks] (CTAs of chunk j that stored their rows)
+constexpr int kMaxChunks = 64;
+constexpr int kFlagWords = 2 * kMaxChunks;
+
+// Streamed bytes per chunk on the host path (0 = the default policy below;
+// SFX_HOST_CHUNK_BYTES overrides it, e.g. to exercise many chunks on small
+// graphs in tests).
+// SFX_HOST_STREAM=0 turns the chunk-streamed host path off (whole copies
+// ordered by events; for A/B measurement).
+bool host_streaming() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFX_HOST_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+uint64_t host_chunk_bytes() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("SFX_HOST_CHUNK_BYTES");
+    long long x = e ? std::atoll(e) : 0;
+    return x > 0 ? static_cast<uint64_t>(x) : uint64_t{0};
+  }();
+  return v;
+}
+
 struct sfx_graph {
   sfx_ctx* ctx = nullptr;
   sfx::Graph graph;
   std::vector<sfx_kernel*> kernels;  // per program: planned groups, then matmul barriers
+  // host path: row / map kernels recompiled with the host-streaming gate code
+  // (opts.host_stream), built on the first sfx_graph_run_host; null = use kernels[p]
+  std::vector<sfx_kernel*> host_kernels;
+  sfx_compile_opts opts{};
   int n_planned = 0;                 // programs that came from the CompileReport
   std::vector<int> order;            // program launch order (condensation Kahn order)
   std::vector<int> params;           // Parameter nodes, ascending id = param slot order
@@ -141,6 +173,9 @@ struct sfx_graph {
   std::map<std::vector<uint64_t>, std::pair<CUgraph, CUgraphExec>> captured;
   std::vector<CUdeviceptr> host_bufs;  // staging for sfx_graph_run_host (params then outputs)
   CUstream d2h = nullptr;              // host path: device->host copies overlap the next groups
+  CUstream h2d = nullptr, h2d2 = nullptr;  // host path: host->device copies (chunks alternate)
+  CUstream d2h2 = nullptr;                 // second device->host stream (chunks alternate)
+  CUdeviceptr stream_flags = 0;        // per kernel: gate word + done[kFlagWords - 1]
   std::vector<CUevent> events;
   std::vector<int> host_order;
 };
@@ -181,7 +216,15 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   return k.release();
 }
 
-void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s) {
+// Host-streaming arguments of one launch (KernelSource::stream_R): null gate =
+// no streaming, the kernel runs on resident inputs as usual.
+struct StreamArgs {
+  CUdeviceptr gate = 0, done = 0;
+  long long chunk_elems = 0;
+};
+
+void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
+            const StreamArgs& sa = StreamArgs()) {
   if (in.size() != k->src.inputs.size())
     throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(k->src.inputs.size()) + " inputs");
   if (out.size() != k->src.outputs.size())
@@ -207,6 +250,15 @@ void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector
     args.push_back(&poff);
     args.push_back(&prank);
     args.push_back(&pn);
+  }
+  CUdeviceptr sgate = sa.gate, sdone = sa.done;
+  long long schunk = sa.chunk_elems;
+  if (k->src.stream_R > 0) {
+    args.push_back(&sgate);
+    args.push_back(&sdone);
+    args.push_back(&schunk);
+  } else if (sa.gate) {
+    throw sfx::Error(SFX_ERR_INVALID, "internal: stream gate for a non-streaming kernel");
   }
   // programmatic dependent launch (every generated kernel begins with
   // griddepcontrol.wait, so stream order is preserved)
@@ -537,6 +589,7 @@ sfx_status sfx_graph_compile(sfx_ctx* ctx, const sfx_graph_desc* desc, const sfx
     if (!ctx || !out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
     auto G = std::make_unique<sfx_graph>();
     G->ctx = ctx;
+    if (opts) G->opts = *opts;
     G->graph = sfx::graph_from_desc(desc);
     G->n_planned = static_cast<int>(G->graph.programs.size());
     add_barrier_programs(G->graph);
@@ -683,57 +736,181 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
     std::vector<uint64_t> dp(G->host_bufs.begin(), G->host_bufs.begin() + n_params);
     std::vector<uint64_t> dout(G->host_bufs.begin() + n_params, G->host_bufs.end());
     const sfx::Graph& g = G->graph;
+    const int K = static_cast<int>(G->kernels.size());
     if (!G->d2h) {
       sfx::check_cu(d.cuStreamCreate(&G->d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-      G->events.resize(G->kernels.size() + 1);
+      sfx::check_cu(d.cuStreamCreate(&G->h2d, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      sfx::check_cu(d.cuStreamCreate(&G->h2d2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      sfx::check_cu(d.cuStreamCreate(&G->d2h2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      G->events.resize(3 * K + 2);
       for (CUevent& e : G->events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
       G->host_order = host_order(G);
+      G->stream_flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
+      G->host_kernels.assign(K, nullptr);
+      if (host_streaming()) {
+        sfx_compile_opts ho = G->opts;
+        ho.host_stream = 1;
+        for (int p = 0; p < K; ++p) {
+          const std::string& st = G->kernels[p]->src.strategy;
+          if (st != "row" && st != "map") continue;
+          sfx_kernel* hk = build_kernel(G->ctx, g, p, &ho);
+          if (hk->src.stream_R > 0) G->host_kernels[p] = hk;
+          else destroy_kernel(hk);
+        }
+      }
     }
-    // Overlapped host path: each group's params are copied in right before it
-    // runs and its graph outputs are copied back on a second stream while the
-    // next groups' inputs cross PCIe (full duplex).  Groups that return the
-    // most bytes go first (any dependency-respecting order gives the same values).
+    // Overlapped host path.  Streams: host->device copies (h2d, h2d2), the
+    // launches (s), device->host copies (d2h, d2h2).  A group whose template
+    // works on an [R, C] row space (row / map, KernelSource::stream_R) is fed in
+    // row chunks: a copy stream lands chunk j of its row-local inputs and sets
+    // the group's gate[j] = 1 (cuStreamWriteValue32); the kernel's CTAs of chunk
+    // j wait on gate[j], and each bumps done[j] once its rows are stored; a
+    // copy-back stream waits for done[j] == the chunk's CTA count
+    // (cuStreamWaitValue32) and returns chunk j of the group's graph outputs.
+    // Chunks alternate between the two streams of each direction, so one
+    // stream's copy runs while the other waits on its stream memory operation
+    // (a memop drains the copy pipeline: ~20 us per chunk on one stream).
+    // So a group's launch starts when its first chunk lands and its results
+    // start crossing back while the rest of its inputs are still in flight —
+    // still ONE launch per group.  Other groups: whole copies, ordered by events.
+    // Groups that return the most bytes go first (any dependency-respecting
+    // order gives the same values).
+    sfx::check_cu(d.cuMemsetD32Async(G->stream_flags, 0, static_cast<size_t>(K) * kFlagWords, s), "cuMemsetD32Async");
+    CUevent ev_reset = G->events[3 * K];
+    sfx::check_cu(d.cuEventRecord(ev_reset, s), "cuEventRecord");
+    for (CUstream st : {G->h2d, G->h2d2, G->d2h, G->d2h2})
+      sfx::check_cu(d.cuStreamWaitEvent(st, ev_reset, 0), "cuStreamWaitEvent");
+
     std::map<int, CUdeviceptr> where = G->owned;
     std::map<int, int> param_slot, out_slot;
     for (int i = 0; i < n_params; ++i) where[G->params[i]] = dp[i], param_slot[G->params[i]] = i;
     for (int i = 0; i < n_outputs; ++i) where[g.outputs[i]] = dout[i], out_slot[g.outputs[i]] = i;
-    std::vector<bool> copied(n_params, false);
-    auto h2d = [&](int node) {
-      auto it = param_slot.find(node);
-      if (it == param_slot.end() || copied[it->second]) return;
-      copied[it->second] = true;
-      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[it->second], params[it->second], g.nodes[node].numel() * 4, s),
+    std::vector<bool> copied(n_params, false), returned(n_outputs, false);
+    // host->device copy of rows [r0, r1) of a node split into R rows (whole: 0, R, R)
+    auto h2d_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
+      const int slot = param_slot.at(node);
+      const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
+      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[slot] + r0 * row, static_cast<const char*>(params[slot]) + r0 * row,
+                                        (r1 - r0) * row, st),
                     "cuMemcpyHtoDAsync");
     };
-    std::vector<bool> returned(n_outputs, false);
+    auto d2h_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
+      const int slot = out_slot.at(node);
+      const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
+      sfx::check_cu(d.cuMemcpyDtoHAsync(static_cast<char*>(outputs[slot]) + r0 * row, dout[slot] + r0 * row,
+                                        (r1 - r0) * row, st),
+                    "cuMemcpyDtoHAsync");
+    };
+    auto is_host_param = [&](int n) {
+      auto it = param_slot.find(n);
+      return it != param_slot.end() && !copied[it->second];
+    };
     for (size_t q = 0; q < G->host_order.size(); ++q) {
-      sfx_kernel* k = G->kernels[G->host_order[q]];
-      for (int in : k->src.inputs) h2d(in);
-      launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), s);
-      bool any = false;
-      for (int r : k->src.outputs) any = any || out_slot.count(r);
-      if (!any) continue;
-      sfx::check_cu(d.cuEventRecord(G->events[q], s), "cuEventRecord");
-      sfx::check_cu(d.cuStreamWaitEvent(G->d2h, G->events[q], 0), "cuStreamWaitEvent");
-      for (int r : k->src.outputs) {
-        auto it = out_slot.find(r);
-        if (it == out_slot.end() || returned[it->second]) continue;
-        returned[it->second] = true;
-        sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[it->second], dout[it->second], g.nodes[r].numel() * 4, G->d2h),
-                      "cuMemcpyDtoHAsync");
+      const int pi = G->host_order[q];
+      sfx_kernel* k = G->host_kernels[pi] ? G->host_kernels[pi] : G->kernels[pi];
+      const sfx::KernelSource& ks = k->src;
+      std::vector<int> ret;  // graph outputs this group returns
+      for (int r : ks.outputs)
+        if (out_slot.count(r) && !returned[out_slot[r]]) ret.push_back(r);
+      std::set<int> chunked;
+      for (int in : ks.stream_inputs)
+        if (is_host_param(in)) chunked.insert(in);
+      const int64_t R = ks.stream_R;
+      bool streamed = R > 0 && host_streaming() && (!chunked.empty() || !ret.empty());
+      for (int r : ret)
+        if (streamed && g.nodes[r].numel() % R) streamed = false;
+      // chunk rows: ~16 MB of streamed bytes per chunk, a multiple of the CTA
+      // row unit, at most kFlagWords - 1 chunks
+      int64_t rpc = R, nch = 1;
+      if (streamed) {
+        uint64_t bytes = 0;
+        for (int in : chunked) bytes += g.nodes[in].numel() * 4;
+        for (int r : ret) bytes += g.nodes[r].numel() * 4;
+        // default: up to 32 chunks of >= 4 MB (measured: C1 67 MB best at 4-8 MB
+        // chunks, C2 537 MB at ~16 MB, C5's 3.2 GB probs_d flat from 16 to 100 MB)
+        const uint64_t cb = host_chunk_bytes() ? host_chunk_bytes() : std::max<uint64_t>(4 << 20, bytes / 32);
+        int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, static_cast<int64_t>(bytes / cb)));
+        const int64_t unit = std::max<int64_t>(1, ks.stream_unit);
+        rpc = ((R + want - 1) / want + unit - 1) / unit * unit;
+        nch = (R + rpc - 1) / rpc;
+        if (nch > kMaxChunks) streamed = false, rpc = R, nch = 1;
       }
+      // inputs: everything not chunked goes first, whole
+      for (int in : ks.inputs)
+        if (is_host_param(in) && !(streamed && chunked.count(in))) {
+          h2d_rows(in, 1, 0, 1, G->h2d);
+          copied[param_slot[in]] = true;
+        }
+      StreamArgs sa;
+      const CUdeviceptr gate = G->stream_flags + static_cast<uint64_t>(pi) * kFlagWords * 4;
+      if (streamed) {
+        // the whole inputs above precede every chunk gate on both streams
+        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d), "cuEventRecord");
+        sfx::check_cu(d.cuStreamWaitEvent(G->h2d2, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
+        for (int64_t j = 0; j < nch; ++j) {
+          CUstream st = (j & 1) ? G->h2d2 : G->h2d;
+          const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
+          for (int in : chunked) h2d_rows(in, R, r0, r1, st);
+          sfx::check_cu(d.cuStreamWriteValue32(st, gate + 4 * j, 1u, CU_STREAM_WRITE_VALUE_DEFAULT),
+                        "cuStreamWriteValue32");
+        }
+        for (int in : chunked) copied[param_slot[in]] = true;
+        sa.gate = gate;
+        sa.done = gate + 4 * kMaxChunks;
+        sa.chunk_elems = static_cast<long long>(rpc * ks.stream_C);
+      } else {
+        // whole copies: on the first copy stream, plus anything the second
+        // stream still has in flight for earlier groups
+        sfx::check_cu(d.cuEventRecord(G->events[3 * q], G->h2d), "cuEventRecord");
+        sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q], 0), "cuStreamWaitEvent");
+        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d2), "cuEventRecord");
+        sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
+      }
+      launch(k, gather_ptrs(G, ks.inputs, where), gather_ptrs(G, ks.outputs, where), s, sa);
+      if (ret.empty()) continue;
+      if (streamed) {
+        const int64_t E = ks.stream_cta_elems, C = ks.stream_C;
+        for (int64_t j = 0; j < nch; ++j) {
+          CUstream st = (j & 1) ? G->d2h2 : G->d2h;
+          const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
+          const int64_t ctas = (r1 * C + E - 1) / E - (r0 * C) / E;
+          sfx::check_cu(d.cuStreamWaitValue32(st, sa.done + 4 * j, static_cast<cuuint32_t>(ctas),
+                                              CU_STREAM_WAIT_VALUE_GEQ),
+                        "cuStreamWaitValue32");
+          for (int r : ret) d2h_rows(r, R, r0, r1, st);
+        }
+      } else {
+        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 1], s), "cuEventRecord");
+        sfx::check_cu(d.cuStreamWaitEvent(G->d2h, G->events[3 * q + 1], 0), "cuStreamWaitEvent");
+        for (int r : ret) d2h_rows(r, 1, 0, 1, G->d2h);
+      }
+      for (int r : ret) returned[out_slot[r]] = true;
     }
     // graph outputs no group produces (a parameter or constant listed as output)
+    bool tail = false;
     for (int i = 0; i < n_outputs; ++i) {
       if (returned[i]) continue;
       int o = g.outputs[i];
-      h2d(o);
-      CUdeviceptr src = param_slot.count(o) ? dp[param_slot[o]] : G->owned.count(o) ? G->owned.at(o) : 0;
-      if (!src) throw sfx::Error(SFX_ERR_EXEC, "no value for graph output " + g.nodes[o].id);
-      sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
+      if (is_host_param(o)) {
+        h2d_rows(o, 1, 0, 1, G->h2d);
+        copied[param_slot[o]] = true;
+      }
+      tail = true;
     }
-    sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
-    sfx::check_cu(d.cuStreamSynchronize(G->d2h), "cuStreamSynchronize");
+    if (tail) {
+      CUevent ev = G->events[3 * K + 1];
+      sfx::check_cu(d.cuEventRecord(ev, G->h2d), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(s, ev, 0), "cuStreamWaitEvent");
+      for (int i = 0; i < n_outputs; ++i) {
+        if (returned[i]) continue;
+        int o = g.outputs[i];
+        CUdeviceptr src = param_slot.count(o) ? dp[param_slot[o]] : G->owned.count(o) ? G->owned.at(o) : 0;
+        if (!src) throw sfx::Error(SFX_ERR_EXEC, "no value for graph output " + g.nodes[o].id);
+        sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
+      }
+    }
+    for (CUstream st : {G->h2d, G->h2d2, s, G->d2h, G->d2h2})
+      sfx::check_cu(d.cuStreamSynchronize(st), "cuStreamSynchronize");
   });
 }
 
@@ -749,9 +926,13 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
       }
       for (CUevent e : G->events) d.cuEventDestroy(e);
       if (G->d2h) d.cuStreamDestroy(G->d2h);
+      for (CUstream st : {G->h2d, G->h2d2, G->d2h2})
+        if (st) d.cuStreamDestroy(st);
     } catch (...) {
     }
+    if (G->stream_flags) G->ctx->release(G->stream_flags);
     for (sfx_kernel* k : G->kernels) destroy_kernel(k);
+    for (sfx_kernel* k : G->host_kernels) destroy_kernel(k);
     for (auto& [n, p] : G->owned) G->ctx->release(p);
     for (CUdeviceptr p : G->host_bufs) G->ctx->release(p);
     delete G;

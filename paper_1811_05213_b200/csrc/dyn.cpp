@@ -74,6 +74,8 @@ const Driver& driver() {
     SFX_BIND(cuIpcOpenMemHandle)
     SFX_BIND(cuIpcCloseMemHandle)
     SFX_BIND(cuMemcpyHtoD)
+    SFX_BIND(cuStreamWriteValue32)
+    SFX_BIND(cuStreamWaitValue32)
 #undef SFX_BIND
     if (err.empty()) {
       CUresult r = d.cuInit(0);

@@ -52,6 +52,8 @@ struct Driver {
   SFX_DRV(cuIpcOpenMemHandle)
   SFX_DRV(cuIpcCloseMemHandle)
   SFX_DRV(cuMemcpyHtoD)
+  SFX_DRV(cuStreamWriteValue32)
+  SFX_DRV(cuStreamWaitValue32)
 #undef SFX_DRV
 };
 

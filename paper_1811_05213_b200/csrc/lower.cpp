@@ -74,7 +74,8 @@ Ctx make_ctx(const Graph& g, const Program& p) {
 
 // ---- kernel scaffolding ---------------------------------------------------
 
-std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block, int min_blocks = 0) {
+std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block, int min_blocks = 0,
+                      bool stream = false) {
   std::ostringstream os;
   os << "extern \"C\" __global__ void __launch_bounds__(" << block;
   if (min_blocks > 0) os << ", " << min_blocks;
@@ -95,6 +96,7 @@ std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int b
   os << (first ? "" : ", ") << "unsigned* __restrict__ ws";
   if (c.peer)
     os << ", const unsigned long long* __restrict__ peers, unsigned long long poff, int prank, int pn";
+  if (stream) os << ", const unsigned* __restrict__ sgate, unsigned* __restrict__ sdone, long long schunk";
   os << ")";
   return os.str();
 }
@@ -121,6 +123,38 @@ std::string assemble(const std::string& sig, const Code& body) {
   s += body.text;
   s += "}\n";
   return s;
+}
+
+// Host-streaming gate (see KernelSource::stream_R): emitted first in the body.
+// `e0` = the CTA's first element of the [R, C] row space; a CTA never spans
+// two chunks, so it waits for its own chunk's copies (a copy stream sets
+// sgate[j] = 1 after chunk j).
+void emit_stream_gate(Code& body, const std::string& e0, int64_t cta_elems, int64_t total) {
+  // all of it behind the (uniform) null test: the device path pays one branch
+  body.line("if (sgate) {");
+  body.line("  const long long s_e1 = min(" + e0 + " + (long long)" + fmt_i(cta_elems) + ", (long long)" +
+            fmt_i(total) + ") - 1;");
+  body.line("  if (threadIdx.x == 0) sfx_gate_wait(sgate + s_e1 / schunk, 1u);");
+  body.line("  __syncthreads();");
+  body.line("}");
+}
+// ... and last: once every thread's stores are issued, one release-ordered
+// increment of the chunk's completion counter (the copy-back stream waits for
+// the chunk's CTA count with cuStreamWaitValue32).
+void emit_stream_done(Code& body, const std::string& e0) {
+  body.line("if (sdone) {");
+  body.line("  __syncthreads();");
+  body.line("  if (threadIdx.x == 0) { __threadfence(); atomicAdd(sdone + (" + e0 + ") / schunk, 1u); }");
+  body.line("}");
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
 }
 
 int root_slot(const Ctx& c, int node) {
@@ -348,6 +382,8 @@ bool analyze_map(const Ctx& c, std::string* why) {
   return true;
 }
 
+std::set<int> row_local_inputs(const Ctx& c, const RowPlan& rp);
+
 KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "map";
@@ -368,25 +404,43 @@ KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
     max_items = std::max(max_items, n / V);
   }
   Code body;
-  // one emitter per class (lane count differs)
-  std::string sig;
-  {
-    Emitter probe(c.g, c.p, 1, c.wide);
-    sig = signature(c, probe, ks.entry, B);
-  }
   // items (V-element vectors) per thread: several independent 128-bit loads in
   // flight per thread on large streams; consecutive threads stay consecutive
   int U = o.items_per_thread > 0 ? o.items_per_thread
           : max_items >= int64_t{kNumSMs} * 8 * B * 4 ? 4
           : max_items >= int64_t{kNumSMs} * 8 * B * 2 ? 2 : 1;
   U = std::max(1, std::min(U, 8));
+  // host streaming over the root's leading dim (one shape class only)
+  const bool stream = o.host_stream && classes.size() == 1 && !classes.begin()->first.empty() &&
+                      classes.begin()->first[0] > 1;
+  if (stream) {
+    const std::vector<int64_t>& dims = classes.begin()->first;
+    RowPlan sp;
+    sp.R = dims[0];
+    sp.C = prod(dims, 1, dims.size());
+    ks.stream_R = sp.R;
+    ks.stream_C = sp.C;
+    ks.stream_cta_elems = int64_t{B} * U * vw[0].first;
+    ks.stream_unit = ks.stream_cta_elems / gcd64(ks.stream_cta_elems, sp.C);
+    std::set<int> loc = row_local_inputs(c, sp);
+    ks.stream_inputs.assign(loc.begin(), loc.end());
+  }
+  // one emitter per class (lane count differs)
+  std::string sig;
+  {
+    Emitter probe(c.g, c.p, 1, c.wide);
+    sig = signature(c, probe, ks.entry, B, 0, stream);
+  }
   std::string idx_t = c.wide ? "long long" : "int";
+  if (stream)
+    emit_stream_gate(body, "(long long)blockIdx.x * " + fmt_i(ks.stream_cta_elems), ks.stream_cta_elems,
+                     ks.stream_R * ks.stream_C);
   body.line("const " + idx_t + " t0 = (" + idx_t + ")blockIdx.x * " + std::to_string(B * U) + " + threadIdx.x;");
   size_t ci = 0;
   for (auto& [dims, roots] : classes) {
     auto [V, items] = vw[ci++];
     Emitter em(c.g, c.p, V, c.wide);
-    signature(c, em, ks.entry, B);
+    signature(c, em, ks.entry, B, 0, stream);
     em.code = &body;
     auto emit_item = [&](const std::string& it) {
       em.push();
@@ -440,6 +494,7 @@ KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o) {
       body.line("}");
     }
   }
+  if (stream) emit_stream_done(body, "(long long)blockIdx.x * " + fmt_i(ks.stream_cta_elems));
   ks.code = assemble(sig, body);
   ks.block = B;
   ks.grid_x = (max_items + int64_t{B} * U - 1) / (int64_t{B} * U);
@@ -747,11 +802,23 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   if (o.rows_per_cta > 0 && o.rows_per_cta <= RPC) RPC = o.rows_per_cta;
   const int threads = RPC * TPR;
 
+  // host streaming by row chunks: only when no CTA has out-of-range rows (no
+  // thread leaves before the completion barrier)
+  const bool stream = o.host_stream && R % RPC == 0 && R > RPC;
+  if (stream) {
+    ks.stream_R = R;
+    ks.stream_C = C;
+    ks.stream_cta_elems = int64_t{RPC} * C;
+    ks.stream_unit = RPC;
+    std::set<int> loc = row_local_inputs(c, rp);
+    ks.stream_inputs.assign(loc.begin(), loc.end());
+  }
   Emitter em(c.g, c.p, V, c.wide);
-  std::string sig = signature(c, em, ks.entry, threads);
+  std::string sig = signature(c, em, ks.entry, threads, 0, stream);
   Code body;
   em.code = &body;
   const std::string& it = em.idx_t;
+  if (stream) emit_stream_gate(body, "(long long)blockIdx.x * " + fmt_i(ks.stream_cta_elems), ks.stream_cta_elems, R * C);
   body.line("const int tid = threadIdx.x;");
   body.line("const int lr = tid & " + std::to_string(TPR - 1) + ";");
   if (TPR > 32) {
@@ -777,6 +844,7 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
     body.line("const int gleader = (tid & 31) & " + std::to_string(32 - TPR) + ";");
   }
   emit_row_body(c, rp, em, body, TPR, V, NCH);
+  if (stream) emit_stream_done(body, "(long long)blockIdx.x * " + fmt_i(ks.stream_cta_elems));
   ks.code = assemble(sig, body);
   ks.block = threads;
   ks.grid_x = (R + RPC - 1) / RPC;

@@ -44,6 +44,16 @@ struct KernelSource {
   // arena this kernel needs; the kernel then takes (peers, peer_off, rank,
   // nranks) after ws
   int64_t peer_bytes = 0;
+  // host streaming (sfx_graph_run_host): the group's work is an [R, C] row
+  // space (stream_R > 0) that the kernel can consume in row chunks as the
+  // host->device copies land.  The kernel then takes (sgate, sdone, schunk)
+  // after ws / the peer params: a CTA waits until *sgate > its chunk (the copy
+  // stream bumps it after each chunk of `stream_inputs`), and bumps
+  // sdone[chunk] when its rows are stored (the copy-back stream waits on it).
+  // A CTA covers stream_cta_elems consecutive elements of the row space, so
+  // chunks of a multiple of stream_unit rows never share a CTA.
+  int64_t stream_R = 0, stream_C = 0, stream_cta_elems = 0, stream_unit = 0;
+  std::vector<int> stream_inputs;  // row-local inputs: chunk j = rows [j*rpc, (j+1)*rpc)
   std::vector<int> inputs;   // node ids per input slot (Program::inputs)
   std::vector<int> outputs;  // node ids per output slot (Program::roots)
   int64_t algorithmic_bytes = 0;

@@ -110,6 +110,15 @@ __device__ __forceinline__ unsigned long long sfx_globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Host-streaming gate: wait until the copy stream has published chunk count
+// `need` (cuStreamWriteValue32 after the chunk's host->device copies).
+__device__ __forceinline__ void sfx_gate_wait(const unsigned* gate, unsigned need) {
+  const unsigned long long t0 = sfx_globaltimer();
+  while (sfx_ld_acquire_sys(gate) < need) {
+    if (sfx_globaltimer() - t0 > 20000000000ull) __trap();
+    __nanosleep(128);
+  }
+}
 // Wait until a peer has published sequence number `seq` (wrap-safe).  A rank
 // that never arrives (crashed process, mismatched graphs) traps after 20 s
 // instead of hanging the GPU.

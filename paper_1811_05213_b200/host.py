@@ -93,7 +93,7 @@ class SfxCompileOpts(C.Structure):
     _fields_ = [("strategy", C.c_int32), ("debug_checks", C.c_int32), ("rows_per_cta", C.c_int32),
                 ("threads_per_row", C.c_int32), ("items_per_thread", C.c_int32), ("row_pipeline", C.c_int32),
                 ("pipe_warps", C.c_int32), ("pipe_stages", C.c_int32), ("pipe_ctas_per_sm", C.c_int32),
-                ("cross_rank", C.c_int32)]
+                ("cross_rank", C.c_int32), ("host_stream", C.c_int32)]
 
 
 class SfxKernelInfo(C.Structure):
@@ -417,9 +417,9 @@ class GraphDesc:
 
 
 def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0,
-                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0, cross_rank=0):
+                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0, cross_rank=0, host_stream=0):
     return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline,
-                          pipe_warps, pipe_stages, pipe_ctas_per_sm, int(bool(cross_rank)))
+                          pipe_warps, pipe_stages, pipe_ctas_per_sm, int(bool(cross_rank)), int(bool(host_stream)))
 
 
 def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):
