@@ -36,6 +36,9 @@ METRICS = {
     "l2_hit": "lts__t_sector_hit_rate.pct",
     "bank_conflicts_ld": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "bank_conflicts_st": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "smem_wavefronts_ld": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "smem_wavefronts_st": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+    "occ_theory": "sm__maximum_warps_per_active_cycle_pct",
 }
 
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "ms": 1e3, "ns": 1e-3, "s": 1e6}
@@ -83,17 +86,21 @@ def main():
     lines = [f"# ncu --set full summary ({args.tag})", "",
              f"source: `{os.path.basename(args.rep)}` (ncu --set full --clock-control none, cold cache, "
              "serialised replay; compare shares, not absolutes)", "",
-             "| kernel | dur us | DRAM rd MB | DRAM wr MB | traffic/algo | DRAM % | SM % | warps active % | regs | grid | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+             "| kernel | dur us | DRAM rd MB | DRAM wr MB | DRAM GB/s | traffic/algo | DRAM % | SM % | occupancy achieved / theoretical % | smem bank conflicts ld / st (wavefronts) | regs | grid | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(HERE, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for d in rows:
         t = d.get("dram_rd", 0) + d.get("dram_wr", 0)
         a = algo.get(d["kernel"])
         ratio = f"{t / a:.3f}" if a else "-"
+        gbs = t / (d["dur_us"] * 1e3) if d.get("dur_us") else 0.0
+        bc = (f"{int(d.get('bank_conflicts_ld', 0))} / {int(d.get('bank_conflicts_st', 0))} "
+              f"({int(d.get('smem_wavefronts_ld', 0))} / {int(d.get('smem_wavefronts_st', 0))})")
         lines.append(f"| {d['kernel']} | {d.get('dur_us', 0):.1f} | {d.get('dram_rd', 0) / 1e6:.1f} | "
-                     f"{d.get('dram_wr', 0) / 1e6:.1f} | {ratio} | {d.get('dram_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
-                     f"{d.get('warps_active_pct', 0):.1f} | {int(d.get('regs', 0))} | {int(d.get('grid', 0))} | "
+                     f"{d.get('dram_wr', 0) / 1e6:.1f} | {gbs:.0f} | {ratio} | {d.get('dram_pct', 0):.1f} | "
+                     f"{d.get('sm_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} / {d.get('occ_theory', 0):.1f} | {bc} | "
+                     f"{int(d.get('regs', 0))} | {int(d.get('grid', 0))} | "
                      + ", ".join(f"{k} {v:.1f}" for k, v in d["stalls"]) + " |")
         traffic[f"{args.config}/{d['kernel']}"] = t
     with open(os.path.join(HERE, f"{args.tag}_kernels.md"), "w") as f:
