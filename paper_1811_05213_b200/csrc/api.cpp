@@ -139,6 +139,17 @@ constexpr int kFlagWords = 2 * kMaxChunks;
 // Streamed bytes per chunk on the host path (0 = the default policy below;
 // SFX_HOST_CHUNK_BYTES overrides it, e.g. to exercise many chunks on small
 // graphs in tests).
+// Concurrent branches for independent groups in sfx_graph_run (SFX_GRAPH_BRANCHES=0
+// turns them off, for A/B measurement).
+constexpr int kBranches = 4;
+bool graph_branches() {
+  static const bool v = [] {
+    const char* e = std::getenv("SFX_GRAPH_BRANCHES");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // SFX_HOST_STREAM=0 turns the chunk-streamed host path off (whole copies
 // ordered by events; for A/B measurement).
 bool host_streaming() {
@@ -175,7 +186,9 @@ struct sfx_graph {
   CUstream d2h = nullptr;              // host path: device->host copies overlap the next groups
   CUstream h2d = nullptr, h2d2 = nullptr;  // host path: host->device copies (chunks alternate)
   CUstream d2h2 = nullptr;                 // second device->host stream (chunks alternate)
-  CUdeviceptr stream_flags = 0;        // per kernel: gate word + done[kFlagWords - 1]
+  CUdeviceptr stream_flags = 0;        // per kernel: gate[kMaxChunks] + done[kMaxChunks]
+  std::vector<CUstream> branch_streams;  // device path: independent groups run concurrently
+  std::vector<CUevent> branch_events;    // per kernel completion, then fork / join
   std::vector<CUevent> events;
   std::vector<int> host_order;
 };
@@ -411,9 +424,68 @@ void graph_enqueue(sfx_graph* G, const uint64_t* params, const uint64_t* outputs
         sfx::check_cu(d.cuMemcpyDtoDAsync(outputs[i], src, n.numel() * 4, s), "cuMemcpyDtoDAsync");
     }
   }
+  if (!graph_branches() || G->order.size() < 2) {
+    for (int p : G->order) {
+      sfx_kernel* k = G->kernels[p];
+      launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), s);
+    }
+    return;
+  }
+  // Independent groups on parallel branches (fork/join with events; captured
+  // as parallel CUDA-graph nodes), so one group's ramp and tail overlap
+  // another's body instead of leaving HBM idle between launches.  Edges are
+  // the groups' data dependencies (a group reads roots of earlier groups);
+  // roots, workspaces and inputs are otherwise disjoint, so nothing else orders
+  // them.  Within a branch, launches stay PDL-chained.
+  const int K = static_cast<int>(G->kernels.size());
+  if (G->branch_streams.empty()) {
+    G->branch_streams.resize(kBranches - 1, nullptr);
+    for (CUstream& st : G->branch_streams)
+      sfx::check_cu(d.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    G->branch_events.resize(K + kBranches, nullptr);
+    for (CUevent& e : G->branch_events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  }
+  std::map<int, int> producer;
+  for (int p = 0; p < K; ++p)
+    for (int r : G->kernels[p]->src.outputs) producer[r] = p;
+  std::vector<CUstream> streams{s};
+  streams.insert(streams.end(), G->branch_streams.begin(), G->branch_streams.end());
+  std::vector<bool> forked(streams.size(), false);
+  forked[0] = true;
+  CUevent ev_fork = G->branch_events[K];
+  sfx::check_cu(d.cuEventRecord(ev_fork, s), "cuEventRecord");
+  std::vector<int> stream_of(K, -1);
+  int next = 0;
   for (int p : G->order) {
     sfx_kernel* k = G->kernels[p];
-    launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), s);
+    std::set<int> deps;
+    for (int in : k->src.inputs) {
+      auto it = producer.find(in);
+      if (it != producer.end() && it->second != p) deps.insert(it->second);
+    }
+    int si;
+    if (deps.empty()) {
+      si = next;
+      next = (next + 1) % static_cast<int>(streams.size());
+    } else {
+      si = stream_of[*deps.begin()];
+    }
+    CUstream st = streams[si];
+    if (!forked[si]) {
+      sfx::check_cu(d.cuStreamWaitEvent(st, ev_fork, 0), "cuStreamWaitEvent");
+      forked[si] = true;
+    }
+    for (int q : deps)
+      if (stream_of[q] != si) sfx::check_cu(d.cuStreamWaitEvent(st, G->branch_events[q], 0), "cuStreamWaitEvent");
+    launch(k, gather_ptrs(G, k->src.inputs, where), gather_ptrs(G, k->src.outputs, where), st);
+    sfx::check_cu(d.cuEventRecord(G->branch_events[p], st), "cuEventRecord");
+    stream_of[p] = si;
+  }
+  for (size_t i = 1; i < streams.size(); ++i) {
+    if (!forked[i]) continue;
+    CUevent ev = G->branch_events[K + i];
+    sfx::check_cu(d.cuEventRecord(ev, streams[i]), "cuEventRecord");
+    sfx::check_cu(d.cuStreamWaitEvent(s, ev, 0), "cuStreamWaitEvent");
   }
 }
 
@@ -928,6 +1000,8 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
       if (G->d2h) d.cuStreamDestroy(G->d2h);
       for (CUstream st : {G->h2d, G->h2d2, G->d2h2})
         if (st) d.cuStreamDestroy(st);
+      for (CUstream st : G->branch_streams) d.cuStreamDestroy(st);
+      for (CUevent e : G->branch_events) d.cuEventDestroy(e);
     } catch (...) {
     }
     if (G->stream_flags) G->ctx->release(G->stream_flags);
