@@ -336,6 +336,11 @@ std::string Emitter::reduce_loop(int node, const std::vector<Ix>& comps) {
     if (rd.count(d)) red.push_back(in.dims[d]);
   int64_t nred = 1;
   for (int64_t d : red) nred *= d;
+  if (nred == 1) {  // a fold of one element is that element (exec.cpp:196-201)
+    std::vector<Ix> oc(in.rank());
+    for (int d = 0, o = 0; d < in.rank(); ++d) oc[d] = rd.count(d) ? uni("0") : comps[o++];
+    return value(n.operands[0], oc);
+  }
   std::string acc = fresh("a");
   std::string q = fresh("r");
   const char* T = ctype(n.dtype);

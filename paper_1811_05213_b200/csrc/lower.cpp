@@ -43,6 +43,13 @@ std::string sanitize(const std::string& s) {
   return o;
 }
 
+// A reduction over extent-1 dims folds one element: the element itself (the
+// reference's fold starts from the first element, exec.cpp:196-201), i.e. a
+// reshape.  Such reduces are index algebra, not reductions, for the analyzers.
+bool degenerate_reduce(const Graph& g, const Node& n) {
+  return n.op == SFX_OP_REDUCE && g.nodes[n.operands[0]].numel() == n.numel();
+}
+
 Ctx make_ctx(const Graph& g, const Program& p) {
   Ctx c(g, p);
   std::set<int> seen;
@@ -58,11 +65,12 @@ Ctx make_ctx(const Graph& g, const Program& p) {
     if (n.op == SFX_OP_LIBRARY_CALL)  // always a fusion barrier (span.cpp:35)
       throw Error(SFX_ERR_INVALID, "group member " + n.id + " is a library call");
     if (n.op == SFX_OP_BATCH_MATMUL) c.dots.push_back(m);
-    bool d = n.op == SFX_OP_REDUCE;
+    const bool real_reduce = n.op == SFX_OP_REDUCE && !degenerate_reduce(g, n);
+    bool d = real_reduce;
     for (int op : n.operands)
       if (p.is_member(op) && c.dep[op]) d = true;
     c.dep[m] = d;
-    if (n.op == SFX_OP_REDUCE) c.reduces.push_back(m);
+    if (real_reduce) c.reduces.push_back(m);
   }
   int64_t big = 0;
   for (int m : p.members) big = std::max(big, g.nodes[m].numel());
@@ -249,7 +257,7 @@ bool analyze_row(const Ctx& c, RowPlan* rp, std::string* why) {
     const Node& n = g.nodes[m];
     if (!c.dep.at(m)) continue;
     int cls = cls_of_numel(n.numel());
-    if (n.op == SFX_OP_REDUCE) {
+    if (n.op == SFX_OP_REDUCE && !degenerate_reduce(g, n)) {
       int op = n.operands[0];
       if (c.p.is_member(op) && c.dep.at(op) && rp->cls[op] != CLS_FULL)
         return *why = "reduce operand " + g.nodes[op].id + " is not row-shaped", false;
@@ -278,6 +286,7 @@ bool analyze_row(const Ctx& c, RowPlan* rp, std::string* why) {
         case SFX_OP_ELEMENTWISE:
         case SFX_OP_RESHAPE:
         case SFX_OP_BITCAST:
+        case SFX_OP_REDUCE:  // degenerate: a reshape
           if (oc != cls) return *why = "class mismatch at " + n.id, false;
           break;
         case SFX_OP_BROADCAST: {
@@ -875,7 +884,7 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
   };
   std::map<int, std::string> reduced;  // reduce node -> combined value
   em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
-    if (c.g.nodes[node].op != SFX_OP_REDUCE) return "";
+    if (c.g.nodes[node].op != SFX_OP_REDUCE || degenerate_reduce(c.g, c.g.nodes[node])) return "";
     auto f = reduced.find(node);
     if (f == reduced.end()) throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
     return f->second;
