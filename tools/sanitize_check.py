@@ -1,0 +1,31 @@
+"""Run every small config (and a slice of the reference's random graphs) once
+through the device executor — the workload for compute-sanitizer
+(tools/gpu_sanitize.sh: memcheck, racecheck, synccheck, initcheck)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import sfx_testlib as T  # noqa: E402
+from paper_1811_05213_b200 import host as H  # noqa: E402
+import test_gpu_parity as P  # noqa: E402
+
+ctx = H.Context(0)
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t", "C5"]
+for name in names:
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
+    inputs = T.gen_inputs(g, 42, -1.0, 1.0)
+    for strategy in ("auto", "literal"):
+        outs, _, strat = P._run(ctx, g, rep, inputs, strategy)
+        assert not P._check(g, outs, inputs, strict=True, literal=strategy == "literal"), (name, strategy)
+        print(name, strategy, strat, flush=True)
+n = 0
+for case in P._eligible("pipeline")[:12]:
+    g = H.graph_from_json(case["bundle"]["graph"])
+    rep = H.CompileReport.from_bundle(case["bundle"])
+    inputs = T.gen_inputs(g, case["input_seed"])
+    outs, _, _ = P._run(ctx, g, rep, inputs, "auto")
+    assert not P._check(g, outs, inputs)
+    n += 1
+print("random graphs", n, "ok")
