@@ -145,7 +145,12 @@ enum {
 };
 typedef struct sfx_compile_opts {
   int32_t strategy;      /* SFX_STRATEGY_* ; forcing an inapplicable one fails with SFX_ERR_UNSUPPORTED */
-  int32_t debug_checks;  /* reserved */
+  int32_t debug_checks;  /* 1 = coverage check after every launch (the device twin of the reference's
+                            coverage bitmap, exec.cpp:393-410): outputs are pre-filled with a canary,
+                            and any element the kernel left unwritten (canary still there after two
+                            launches with different canaries) fails the launch with SFX_ERR_EXEC
+                            "incomplete coverage"; synchronous, not inside CUDA-graph capture.
+                            2 = same, but the launch drops its last CTA (test hook: must be caught) */
   int32_t rows_per_cta;  /* 0 = auto (row template) */
   int32_t threads_per_row; /* 0 = auto (row template) */
   int32_t items_per_thread; /* 0 = auto (map template: 128-bit vectors per thread) */

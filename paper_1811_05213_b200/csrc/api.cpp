@@ -128,6 +128,8 @@ struct sfx_kernel {
   CUdeviceptr ws = 0;
   uint64_t peer_off = 0;  // this kernel's region of the symmetric peer arena
   int regs = 0;
+  int debug = 0;                    // sfx_compile_opts.debug_checks
+  std::vector<int64_t> out_elems;   // per output slot (coverage check)
   std::string cubin_path;
 };
 
@@ -201,6 +203,8 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   auto k = std::make_unique<sfx_kernel>();
   k->ctx = ctx;
   k->src = sfx::lower_program(g, pi, o);
+  k->debug = o.debug_checks;
+  for (int r : k->src.outputs) k->out_elems.push_back(g.nodes[r].numel());
   sfx::Cubin cb = sfx::compile_cubin(k->src.code, k->src.entry, k->src.nvrtc_options);
   k->cubin_path = cb.path;
   ctx->bind();
@@ -236,8 +240,59 @@ struct StreamArgs {
   long long chunk_elems = 0;
 };
 
+void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
+                const StreamArgs& sa, bool drop_last_cta);
+
+// One launch of a group's kernel.  With debug_checks, the coverage check of
+// the reference's executor (exec.cpp:393-410: every root element written
+// exactly once, "incomplete coverage" otherwise) runs around it.
 void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
             const StreamArgs& sa = StreamArgs()) {
+  if (!k->debug || sa.gate) {
+    launch_raw(k, in, out, s, sa, false);
+    return;
+  }
+  const sfx::Driver& d = sfx::driver();
+  CUstreamCaptureStatus cap = CU_STREAM_CAPTURE_STATUS_NONE;
+  sfx::check_cu(d.cuStreamIsCapturing(s, &cap), "cuStreamIsCapturing");
+  if (cap != CU_STREAM_CAPTURE_STATUS_NONE)
+    throw sfx::Error(SFX_ERR_INVALID, "debug_checks cannot run inside CUDA-graph capture");
+  // canary A; elements still equal to it are re-checked with canary B (a value
+  // the kernel legitimately computes cannot equal both)
+  const uint32_t canary[2] = {0x7fa5a5a5u, 0xffc3c3c3u};
+  std::vector<std::vector<uint32_t>> suspect(out.size());
+  for (int pass = 0; pass < 2; ++pass) {
+    for (size_t i = 0; i < out.size(); ++i)
+      sfx::check_cu(d.cuMemsetD32Async(out[i], canary[pass], k->out_elems[i], s), "cuMemsetD32Async");
+    launch_raw(k, in, out, s, sa, k->debug == 2);
+    sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
+    bool any = false;
+    for (size_t i = 0; i < out.size(); ++i) {
+      std::vector<uint32_t> host(k->out_elems[i]);
+      sfx::check_cu(d.cuMemcpyDtoH(host.data(), out[i], host.size() * 4), "cuMemcpyDtoH");
+      std::vector<uint32_t> still;
+      if (pass == 0) {
+        for (size_t e = 0; e < host.size(); ++e)
+          if (host[e] == canary[0]) still.push_back(static_cast<uint32_t>(e));
+      } else {
+        for (uint32_t e : suspect[i])
+          if (host[e] == canary[1]) still.push_back(e);
+      }
+      suspect[i] = still;
+      any = any || !still.empty();
+    }
+    if (!any) return;
+  }
+  for (size_t i = 0; i < out.size(); ++i)
+    if (!suspect[i].empty())
+      throw sfx::Error(SFX_ERR_EXEC, "incomplete coverage: " + k->src.entry + " left " +
+                                         std::to_string(suspect[i].size()) + " element(s) of output " +
+                                         std::to_string(i) + " unwritten (first: " + std::to_string(suspect[i][0]) +
+                                         ")");
+}
+
+void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
+                const StreamArgs& sa, bool drop_last_cta) {
   if (in.size() != k->src.inputs.size())
     throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(k->src.inputs.size()) + " inputs");
   if (out.size() != k->src.outputs.size())
@@ -281,6 +336,10 @@ void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector
   CUlaunchConfig cfg{};
   cfg.gridDimX = static_cast<unsigned>(k->src.grid_x);
   cfg.gridDimY = static_cast<unsigned>(k->src.grid_y);
+  if (drop_last_cta) {  // debug_checks=2 test hook
+    if (cfg.gridDimY > 1) --cfg.gridDimY;
+    else if (cfg.gridDimX > 1) --cfg.gridDimX;
+  }
   cfg.gridDimZ = 1;
   cfg.blockDimX = static_cast<unsigned>(k->src.block);
   cfg.blockDimY = 1;
@@ -819,7 +878,7 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
       G->host_order = host_order(G);
       G->stream_flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
       G->host_kernels.assign(K, nullptr);
-      if (host_streaming()) {
+      if (host_streaming() && !G->opts.debug_checks) {  // debug: every launch coverage-checked, whole copies
         sfx_compile_opts ho = G->opts;
         ho.host_stream = 1;
         for (int p = 0; p < K; ++p) {

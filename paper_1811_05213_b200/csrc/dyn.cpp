@@ -76,6 +76,8 @@ const Driver& driver() {
     SFX_BIND(cuMemcpyHtoD)
     SFX_BIND(cuStreamWriteValue32)
     SFX_BIND(cuStreamWaitValue32)
+    SFX_BIND(cuStreamIsCapturing)
+    SFX_BIND(cuMemcpyDtoH)
 #undef SFX_BIND
     if (err.empty()) {
       CUresult r = d.cuInit(0);

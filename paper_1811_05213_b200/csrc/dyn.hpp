@@ -54,6 +54,8 @@ struct Driver {
   SFX_DRV(cuMemcpyHtoD)
   SFX_DRV(cuStreamWriteValue32)
   SFX_DRV(cuStreamWaitValue32)
+  SFX_DRV(cuStreamIsCapturing)
+  SFX_DRV(cuMemcpyDtoH)
 #undef SFX_DRV
 };
 

@@ -417,8 +417,8 @@ class GraphDesc:
 
 
 def compile_opts(strategy="auto", rows_per_cta=0, threads_per_row=0, items_per_thread=0, row_pipeline=0,
-                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0, cross_rank=0, host_stream=0):
-    return SfxCompileOpts(STRATEGIES[strategy], 0, rows_per_cta, threads_per_row, items_per_thread, row_pipeline,
+                 pipe_warps=0, pipe_stages=0, pipe_ctas_per_sm=0, cross_rank=0, host_stream=0, debug_checks=0):
+    return SfxCompileOpts(STRATEGIES[strategy], int(debug_checks), rows_per_cta, threads_per_row, items_per_thread, row_pipeline,
                           pipe_warps, pipe_stages, pipe_ctas_per_sm, int(bool(cross_rank)), int(bool(host_stream)))
 
 

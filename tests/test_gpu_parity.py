@@ -368,3 +368,23 @@ def test_reference_suites_through_device_binding(args):
     r = subprocess.run([DEVICE_PARITY] + args, capture_output=True, text=True, timeout=1200)
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert r.returncode == 0 and line["passed"] == line["cases"] > 0, line
+
+
+@pytest.mark.parametrize("name", ["C1", "C4", "C5"])
+def test_debug_coverage_check(ctx, name):
+    """debug_checks=1: the reference executor's coverage check (exec.cpp:393-410)
+    around every launch passes on the real kernels; debug_checks=2 drops each
+    launch's last CTA and must fail with "incomplete coverage", like the
+    reference's test_exec.cpp:176-194 catches a plan that skips blocks."""
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
+    inputs = T.gen_inputs(g, 42, -1.0, 1.0)
+    cg = H.CompiledGraph(ctx, g, rep, debug_checks=1)
+    try:
+        outs = cg.run_host(inputs)
+    finally:
+        cg.close()
+    assert not _check(g, outs, inputs, strict=True)
+    prog = rep.kernels[0].program
+    ext = {e: inputs[e] for e in inputs}
+    with pytest.raises(H.ExecError, match="incomplete coverage"):
+        H.run_program(prog, g, ext, ctx=ctx, debug_checks=2)
