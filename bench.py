@@ -251,7 +251,9 @@ def run_ours(args):
     # the batch (C3's db).  Default: the column kernel combines the ranks'
     # partials itself through peer memory (cross_rank); --combine nccl runs
     # the unfused baseline (kernel, then ncclAllReduce of the column sums).
-    peer = ws > 1 and args.combine == "peer"
+    # (only graphs with a reduction over the batch dim need the peer group)
+    batch_reduce = any(i.op == "reduce" and 0 in i.reduce_dims for i in g.instructions)
+    peer = ws > 1 and args.combine == "peer" and batch_reduce
     if peer:
         ctx.peer_init(rank, ws, H.torch_all_gather)
     cg = H.CompiledGraph(ctx, g, rep, cross_rank=int(peer))
