@@ -1405,7 +1405,15 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   const int PMAX = SFX_PEER_MAX_RANKS;
   const int64_t first_slot = 2LL * PMAX * NR * C;
   const int64_t flag_byte = (first_slot + 2LL * NR * C) * 8;
+  // per reduce and lane: the column total in the accumulation type, declared
+  // at CTA scope so the cross-rank protocol can sit between its two halves
+  std::vector<std::vector<std::string>> ptot(NR, std::vector<std::string>(V));
   if (c.peer) {
+    for (int k = 0; k < NR; ++k)
+      for (int l = 0; l < V; ++l) {
+        ptot[k][l] = em.fresh("ptot");
+        body.line(acc_t(k) + " " + ptot[k][l] + " = 0;");
+      }
     body.line("__shared__ unsigned s_seq;");
     body.line("if (threadIdx.x == 0) { const unsigned q = ws[" + fmt_i(seq_word) +
               " + blockIdx.x] + 1u; ws[" + fmt_i(seq_word) + " + blockIdx.x] = q; s_seq = q; }");
@@ -1418,7 +1426,9 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     for (int k = 0; k < NR; ++k) {
       const std::string T = acc_t(k);
       std::vector<std::string> tv = stripe_total(k);
-      body.line("for (int p = 0; p < pn; ++p) {");
+      for (int l = 0; l < V; ++l) body.line(ptot[k][l] + " = " + tv[l] + ";");
+      // a single rank has nothing to exchange: the protocol only runs for pn > 1
+      body.line("for (int p = 0; p < pn && pn > 1; ++p) {");
       body.line("  unsigned long long* slot = (unsigned long long*)(peers[p] + poff) + ((par * " +
                 std::to_string(PMAX) + " + prank) * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs +
                 " + c0;");
@@ -1435,15 +1445,19 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     em.pop();
     body.indent--;
     body.line("}");
-    body.line("__threadfence_system();");
-    body.line("__syncthreads();");
-    body.line("if (threadIdx.x < pn) {");
-    body.line("  sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
-              std::to_string(PMAX) + " + prank, seq);");
-    body.line("  sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
+    // the lead lanes' stores reach thread p through the CTA barrier; its
+    // release store at system scope is cumulative over them (no separate
+    // __threadfence_system: it cost 2 us on the critical path)
+    body.line("if (pn > 1) {");
+    body.line("  __syncthreads();");
+    body.line("  if (threadIdx.x < pn) {");
+    body.line("    sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " + fmt_i(flag_byte) +
+              ") + blockIdx.x * " + std::to_string(PMAX) + " + prank, seq);");
+    body.line("    sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
               std::to_string(PMAX) + " + threadIdx.x, seq);");
+    body.line("  }");
+    body.line("  __syncthreads();");
     body.line("}");
-    body.line("__syncthreads();");
   }
   body.line("if (lead) {");
   body.indent++;
@@ -1452,22 +1466,21 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     const Node& rn = c.g.nodes[c.reduces[k]];
     const std::string T = acc_t(k);
     std::vector<std::string> tv;
+    std::string first_peer;  // pn > 1: rank 0's published first element (per lane, below)
     if (c.peer) {
       // every rank folds the same slots in rank order: bit-identical results
-      body.line("const unsigned long long* xs" + std::to_string(k) + " = (const unsigned long long*)(peers[prank] + poff) + (par * " +
+      body.line("if (pn > 1) {");
+      body.line("  const unsigned long long* xs = (const unsigned long long*)(peers[prank] + poff) + (par * " +
                 std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs + " + c0;");
-      tv.resize(V);
-      for (int l = 0; l < V; ++l) {
-        tv[l] = em.fresh("tot");
-        body.line(T + " " + tv[l] + " = __ldcv((const " + T + "*)(xs" + std::to_string(k) + " + " + std::to_string(l) +
-                  "));");
-      }
-      body.line("for (int q = 1; q < pn; ++q) {");
       for (int l = 0; l < V; ++l)
-        body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcv((const " + T + "*)(xs" +
-                  std::to_string(k) + " + (long long)q * " + std::to_string(NR) + " * " + Cs + " + " +
-                  std::to_string(l) + ")));");
+        body.line("  " + ptot[k][l] + " = __ldcv((const " + T + "*)(xs + " + std::to_string(l) + "));");
+      body.line("  for (int q = 1; q < pn; ++q) {");
+      for (int l = 0; l < V; ++l)
+        body.line("    " + ptot[k][l] + " = " + fold_fn(k) + "(" + ptot[k][l] + ", __ldcv((const " + T +
+                  "*)(xs + (long long)q * " + std::to_string(NR) + " * " + Cs + " + " + std::to_string(l) + ")));");
+      body.line("  }");
       body.line("}");
+      tv = ptot[k];
     } else {
       tv = stripe_total(k);
     }
@@ -1480,10 +1493,14 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
     if (needs_first(k)) {
       // sequential std::max/min fold semantics: a NaN first element wins
       for (int l = 0; l < V; ++l) {
-        std::string f0 = c.peer ? "__ldcv((const float*)((const unsigned long long*)(peers[prank] + poff) + " +
-                                      fmt_i(first_slot) + " + (par * " + std::to_string(NR) + " + " +
-                                      std::to_string(k) + ") * " + Cs + " + c0 + " + std::to_string(l) + "))"
-                                : first_elem(k, l);
+        std::string f0 = first_elem(k, l);
+        if (c.peer) {
+          std::string fp = em.fresh("f0");
+          body.line("const float " + fp + " = pn > 1 ? __ldcv((const float*)((const unsigned long long*)(peers[prank] + poff) + " +
+                    fmt_i(first_slot) + " + (par * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs +
+                    " + c0 + " + std::to_string(l) + ")) : " + f0 + ";");
+          f0 = fp;
+        }
         body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
       }
     }
