@@ -823,7 +823,8 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
     ks.stream_inputs.assign(loc.begin(), loc.end());
   }
   Emitter em(c.g, c.p, V, c.wide);
-  std::string sig = signature(c, em, ks.entry, threads, 0, stream);
+  // (pipe_ctas_per_sm doubles as a __launch_bounds__ residency target here)
+  std::string sig = signature(c, em, ks.entry, threads, o.pipe_ctas_per_sm, stream);
   Code body;
   em.code = &body;
   const std::string& it = em.idx_t;

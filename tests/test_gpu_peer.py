@@ -112,14 +112,14 @@ def _min_program(rank):
     return g, prog, _min_rows(rank)
 
 
-def _spawn(case):
+def _spawn(case, ws=WS):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, WS, port, case, q)) for r in range(WS)]
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, case, q)) for r in range(ws)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=600) for _ in range(WS)], key=lambda t: t[0])
+    res = sorted([q.get(timeout=600) for _ in range(ws)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=120)
     for rank, out, err in res:
@@ -129,18 +129,18 @@ def _spawn(case):
     return [out for _, out, _ in res]
 
 
-@pytest.mark.parametrize("case", ["C3", "C3b"])
-def test_cross_rank_column_sum(case):
+@pytest.mark.parametrize("case,ws", [("C3", 2), ("C3b", 2), ("C3", 4)])
+def test_cross_rank_column_sum(case, ws):
     g, _, _ = H.load_bundle(os.path.join(T.PLANS, f"{case}.small.json"))
     n, c = g.at("dy").shape
-    outs = _spawn(case)
-    full = H.parse_graph(configs.c3_biasgrad(N=n * WS, C=c))
+    outs = _spawn(case, ws)
+    full = H.parse_graph(configs.c3_biasgrad(N=n * ws, C=c))
     seeds = [100, 101, 102, 103, 200]
     for i, seed in enumerate(seeds):
-        dy = np.concatenate([_shard(seed, 0, n, c, r) for r in range(WS)])
-        x = np.concatenate([_shard(seed, 1, n, c, r) for r in range(WS)])
+        dy = np.concatenate([_shard(seed, 0, n, c, r) for r in range(ws)])
+        x = np.concatenate([_shard(seed, 1, n, c, r) for r in range(ws)])
         ref = T.interpret(full, {"dy": dy, "x": x}, mode=1)["db"]
-        for r in range(WS):
+        for r in range(ws):
             db = outs[r][i]["db"]
             assert T.strict_close(db, ref), (seed, r, T.mismatch_report(db, ref))
             assert np.array_equal(db.view(np.uint32), outs[0][i]["db"].view(np.uint32))  # identical on all ranks
