@@ -865,6 +865,180 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   return ks;
 }
 
+// Rows too long to hold in registers (more than 1024 threads x 64 elements,
+// e.g. softmax / LayerNorm over 128K columns): one CTA per row, one pass over
+// the row per reduction level plus a final pass for the roots.  The passes
+// re-read the row's inputs, which the first pass left in L2 (a 512 KB row per
+// CTA, 148 CTAs resident: well inside the 126 MB L2), so HBM traffic stays at
+// the compulsory bytes.  f32 sums accumulate in fp64 per thread (a thread
+// folds C / 1024 terms), then warp shuffles and a warp-ordered smem combine.
+KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "row";
+  ks.entry = "sfx_rowmp_" + c.name;
+  fill_common(c, ks);
+  const int64_t R = rp.R, C = rp.C;
+  const int V = (C % 4 == 0) ? 4 : 1;
+  int B = 1024;
+  if (o.threads_per_row > 0) {
+    if (o.threads_per_row % 32 || o.threads_per_row > 1024)
+      throw Error(SFX_ERR_INVALID, "threads_per_row must be a multiple of 32 <= 1024 for long rows");
+    B = o.threads_per_row;
+  }
+  const int W = B / 32;
+  const int64_t NV = C / V;
+  // vectors per thread per loop iteration (independent loads in flight)
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, B);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;");
+  body.line("const " + it + " row = (" + it + ")blockIdx.x;");
+  Ix rowix = em.uni("row");
+  std::map<int, std::string> reduced;
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    if (c.g.nodes[node].op != SFX_OP_REDUCE || degenerate_reduce(c.g, c.g.nodes[node])) return "";
+    auto f = reduced.find(node);
+    if (f == reduced.end()) throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
+    return f->second;
+  };
+  auto fold_of = [&](const Node& rn) {
+    return rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum" : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax"
+                                                                                         : "sfx_fold_pmin";
+  };
+  auto acc_type = [&](const Node& rn) -> std::string {
+    return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
+  };
+  // a loop over the row's vectors, UR per iteration; `emit(col_var)` emits one
+  // vector's work inside a scope
+  // (full tiles unguarded so all UR vectors' loads issue together, then the
+  // remainder one vector at a time)
+  auto row_loop = [&](const std::function<void(const std::string&)>& emit) {
+    const std::string j = em.fresh("j");
+    body.line(it + " " + j + " = tid;");
+    body.line("for (; " + j + " + " + std::to_string((UR - 1) * B) + " < " + fmt_i(NV) + "; " + j + " += " +
+              std::to_string(B * UR) + ") {");
+    body.indent++;
+    em.push();
+    for (int u = 0; u < UR; ++u) {
+      const std::string ju = em.fresh("ju");
+      body.line("const " + it + " " + ju + " = " + j + " + " + std::to_string(u * B) + ";");
+      emit(em.ivar(Emitter::imul(ju, V)));
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.line("for (; " + j + " < " + fmt_i(NV) + "; " + j + " += " + std::to_string(B) + ") {");
+    body.indent++;
+    em.push();
+    emit(em.ivar(Emitter::imul(j, V)));
+    em.pop();
+    body.indent--;
+    body.line("}");
+  };
+  for (int lv = 1; lv <= rp.max_level; ++lv) {
+    std::vector<int> red;
+    for (int r : c.reduces)
+      if (rp.level.at(r) == lv) red.push_back(r);
+    std::vector<std::string> acc(red.size());
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      acc[k] = em.fresh("acc");
+      std::string init = rn.reducer == SFX_REDUCE_SUM ? (rn.dtype == SFX_F32 ? "0.0" : "0")
+                         : rn.dtype == SFX_F32        ? "sfx_bits_f(0x7fc00000)"
+                         : rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+      body.line(acc_type(rn) + " " + acc[k] + " = " + init + ";");
+    }
+    row_loop([&](const std::string& cb) {
+      for (int lane = 0; lane < V; ++lane) {
+        em.lane = lane;
+        Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
+        for (size_t k = 0; k < red.size(); ++k) {
+          const Node& rn = c.g.nodes[red[k]];
+          const Node& in = c.g.nodes[rn.operands[0]];
+          std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, col));
+          body.line(acc[k] + " = " + fold_of(rn) + "(" + acc[k] + ", " + v + ");");
+        }
+      }
+    });
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      const std::string T = acc_type(rn);
+      for (int m = 16; m >= 1; m /= 2)
+        body.line(acc[k] + " = " + fold_of(rn) + "(" + acc[k] + ", __shfl_xor_sync(0xffffffffu, " + acc[k] + ", " +
+                  std::to_string(m) + "));");
+      const std::string sm = em.fresh("rsm");
+      body.line("__shared__ " + T + " " + sm + "[" + std::to_string(W) + "];");
+      body.line("if (lane == 0) " + sm + "[warp] = " + acc[k] + ";");
+      body.line("__syncthreads();");
+      body.line(acc[k] + " = " + sm + "[0];");
+      body.line("for (int w = 1; w < " + std::to_string(W) + "; ++w) " + acc[k] + " = " + fold_of(rn) + "(" + acc[k] +
+                ", " + sm + "[w]);");
+      std::string fin = acc[k];
+      if (T == "double") {
+        fin = em.fresh("red");
+        body.line("const float " + fin + " = (float)" + acc[k] + ";");
+      }
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+        // the sequential fold's first element: the row's element 0
+        em.push();
+        em.lane = 0;
+        const Node& in = c.g.nodes[rn.operands[0]];
+        std::string f0 = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, em.uni("0")));
+        body.line(fin + " = sfx_fold_first(" + f0 + ", " + fin + ");");
+        em.pop();
+      }
+      reduced[red[k]] = fin;
+    }
+  }
+  std::vector<int> full_roots, row_roots;
+  for (int r : c.p.roots) (c.g.nodes[r].numel() == R * C ? full_roots : row_roots).push_back(r);
+  if (!full_roots.empty())
+    row_loop([&](const std::string& cb) {
+      std::vector<std::vector<std::string>> vals(full_roots.size(), std::vector<std::string>(V));
+      for (int lane = 0; lane < V; ++lane) {
+        em.lane = lane;
+        Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
+        for (size_t k = 0; k < full_roots.size(); ++k)
+          vals[k][lane] = em.value(full_roots[k], rowcol_comps(em, c.g.nodes[full_roots[k]].dims, R, C, rowix, col));
+      }
+      const std::string addr = em.ivar(Emitter::iadd(em.ivar(Emitter::imul("row", C)), cb));
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+        if (V == 4)
+          body.line("sfx_st4(" + out + " + " + addr + ", " + vals[k][0] + ", " + vals[k][1] + ", " + vals[k][2] +
+                    ", " + vals[k][3] + ");");
+        else
+          body.line(out + "[" + addr + "] = " + vals[k][0] + ";");
+      }
+    });
+  if (!row_roots.empty()) {
+    em.lane = 0;
+    body.line("if (tid == 0) {");
+    body.indent++;
+    em.push();
+    for (int r : row_roots)
+      body.line("out" + std::to_string(root_slot(c, r)) + "[row] = " + em.value(r, em.from_linear(rowix, c.g.nodes[r].dims)) +
+                ";");
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = R;
+  ks.vector_width = V;
+  // residency cap through dynamic shared memory (the re-read rows of all
+  // resident CTAs must stay in L2): pipe_ctas_per_sm = CTAs per SM
+  if (o.pipe_ctas_per_sm > 0) ks.smem = 220 * 1024 / o.pipe_ctas_per_sm;
+  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
+            " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
+            " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
+  return ks;
+}
+
 // The row body shared by the register-resident and the TMA-pipelined row
 // templates: reduction phases (per-thread fold -> shuffle tree -> broadcast
 // back through registers) then the element and row roots.  Expects `row`,
@@ -1724,14 +1898,14 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   std::string reasons = "map: " + w;
   RowPlan rp;
   if (analyze_row(c, &rp, &w)) {
-    int V = rp.C % 4 == 0 ? 4 : 1;
-    if (rp.C / row_tpr(rp.C, V) <= 64) return "row";
+    if (rp.C / row_tpr(rp.C, rp.C % 4 == 0 ? 4 : 1) <= 64) return "row";
     w = "row too long for registers";
   }
   reasons += "; row: " + w;
   ColPlan cp;
   if (analyze_col(c, &cp, &w)) return "col";
   reasons += "; col: " + w;
+  if (analyze_row(c, &rp, &w)) return "row";  // long rows: one CTA per row, multi-pass
   if (why) *why = reasons;
   return "literal";
 }
@@ -1788,7 +1962,10 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
       bool pipe_ok = !staged.empty() && rp.C % 128 == 0 && rp.C / 32 <= 64 &&
                      4 * 2 * rp.C * 4 * static_cast<int64_t>(staged.size()) <= 200 * 1024 &&
                      o.threads_per_row == 0 && o.rows_per_cta == 0;
-      if (pipe_ok && o.row_pipeline == 2)
+      const int Vr = rp.C % 4 == 0 ? 4 : 1;
+      if (rp.C / row_tpr(rp.C, Vr) > 64)
+        ks = lower_row_mp(c, rp, o);  // longer than 1024 threads x 64 elements
+      else if (pipe_ok && o.row_pipeline == 2)
         ks = lower_row_pipe(c, rp, staged, o);
       else
         ks = lower_row(c, rp, o);

@@ -23,6 +23,10 @@ EXTRA = {
     "ln_r37_c2048": configs.c1_layernorm(R=37, C=2048),
     "softmax_r16_c16384": configs.c2_softmax(B=1, H=2, S=8, L=16384),
     "softmax_r24_c4096": configs.c2_softmax(B=2, H=3, S=4, L=4096),
+    # rows beyond the register-resident template: one CTA per row, multi-pass
+    "softmax_r4_c131072": configs.c2_softmax(B=1, H=1, S=4, L=131072),
+    "ln_r6_c98304": configs.c1_layernorm(R=6, C=98304),
+    "ln_r5_c70001": configs.c1_layernorm(R=5, C=70001),
     # middle-axis and full reductions: the [outer | reduced | inner] column template
     "midsum_16x4096x64": {"instructions": [
         {"id": "x", "op": "parameter", "shape": [16, 4096, 64]},

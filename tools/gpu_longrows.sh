@@ -1,0 +1,2 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -k "long_and_odd" 2>&1 | tail -3
+timeout 900 python tools/long_rows_bench.py --literal 2>&1 | grep -v Warn
