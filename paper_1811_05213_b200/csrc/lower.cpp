@@ -866,37 +866,96 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
 }
 
 // Rows too long to hold in registers (more than 1024 threads x 64 elements,
-// e.g. softmax / LayerNorm over 128K columns): one CTA per row, one pass over
-// the row per reduction level plus a final pass for the roots.  The passes
-// re-read the row's inputs, which the first pass left in L2 (a 512 KB row per
-// CTA, 148 CTAs resident: well inside the 126 MB L2), so HBM traffic stays at
-// the compulsory bytes.  f32 sums accumulate in fp64 per thread (a thread
-// folds C / 1024 terms), then warp shuffles and a warp-ordered smem combine.
+// e.g. softmax / LayerNorm over 128K columns).
+//
+// Cluster variant (default when the row's row-local f32 inputs fit the shared
+// memory of a thread-block cluster of <= 8 CTAs): one cluster per row, CTA q
+// of the cluster owns columns [q*SL, (q+1)*SL).  At entry each CTA has the TMA
+// engine copy its slice of every row-local input into shared memory
+// (cp.async.bulk + mbarrier); every reduction level is then a pass over shared
+// memory, a CTA combine, and a cluster combine through distributed shared
+// memory (each CTA publishes its partial, barrier.cluster, every CTA folds the
+// CS partials in rank order via ld.shared::cluster — identical results in all
+// CTAs); the final pass writes the roots.  HBM sees each input byte once.
+//
+// Plain variant (inputs too large for a cluster, odd widths): one CTA per row,
+// one pass over the row per level plus a final pass, re-reading the row's
+// inputs (mostly from L2).  f32 sums accumulate in fp64 per thread.
 KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "row";
-  ks.entry = "sfx_rowmp_" + c.name;
   fill_common(c, ks);
   const int64_t R = rp.R, C = rp.C;
   const int V = (C % 4 == 0) ? 4 : 1;
-  int B = 1024;
+  std::set<int> loc = row_local_inputs(c, rp);
+  std::vector<int> staged(loc.begin(), loc.end());
+  int CS = 1;
+  if (V == 4 && !staged.empty() && o.row_pipeline != 1) {  // row_pipeline=1: plain multi-pass (A/B)
+    const int64_t bytes = C * 4 * static_cast<int64_t>(staged.size());
+    int cs = 2;
+    while (cs < 8 && bytes / cs > 64 * 1024) cs *= 2;
+    // <= 64 KB of slices per CTA keeps 3 CTAs per SM, so one CTA's TMA load
+    // overlaps another's passes; measured: 128 KB slices (1 CTA/SM) lose to
+    // the plain multi-pass variant (softmax [256,262144]: 232 vs 185 us)
+    if (bytes / cs <= 64 * 1024 && C % (int64_t{cs} * V) == 0) CS = cs;
+  }
+  if (CS == 1) staged.clear();
+  ks.entry = (CS > 1 ? "sfx_rowcl_" : "sfx_rowmp_") + c.name;
+  int B = CS > 1 ? 512 : 1024;
   if (o.threads_per_row > 0) {
     if (o.threads_per_row % 32 || o.threads_per_row > 1024)
       throw Error(SFX_ERR_INVALID, "threads_per_row must be a multiple of 32 <= 1024 for long rows");
     B = o.threads_per_row;
   }
   const int W = B / 32;
-  const int64_t NV = C / V;
+  const int64_t SL = C / CS, SLV = SL / V;  // this CTA's columns / vectors
   // vectors per thread per loop iteration (independent loads in flight)
   const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
   Emitter em(c.g, c.p, V, c.wide);
   std::string sig = signature(c, em, ks.entry, B);
+  if (CS > 1) {
+    const std::string gv = "__global__ void ";
+    sig.insert(sig.find(gv) + gv.size(), "__cluster_dims__(" + std::to_string(CS) + ", 1, 1) ");
+  }
   Code body;
   em.code = &body;
   const std::string& it = em.idx_t;
   body.line("const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;");
-  body.line("const " + it + " row = (" + it + ")blockIdx.x;");
+  const int64_t slice_bytes = SL * 4;
+  if (CS > 1) {
+    body.line("const unsigned q = sfx_cluster_rank();");
+    body.line("const " + it + " row = (" + it + ")blockIdx.x / " + std::to_string(CS) + ";");
+    body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
+    const int64_t bar_off = slice_bytes * static_cast<int64_t>(staged.size());
+    body.line("unsigned long long* sbar = (unsigned long long*)(sfx_smem + " + fmt_i(bar_off) + ");");
+    body.line("if (tid == 0) {");
+    body.line("  sfx_mbar_init(sbar, 1);");
+    body.line("  sfx_fence_mbar_init();");
+    body.line("  sfx_mbar_expect_tx(sbar, " + fmt_i(bar_off) + "u);");
+    for (size_t k = 0; k < staged.size(); ++k)
+      body.line("  sfx_bulk_g2s(sfx_smem + " + fmt_i(static_cast<int64_t>(k) * slice_bytes) + ", " +
+                em.input_ptr.at(staged[k]) + " + row * " + fmt_i(C) + " + (" + it + ")q * " + fmt_i(SL) + ", " +
+                fmt_i(slice_bytes) + "u, sbar);");
+    body.line("}");
+    body.line("__syncthreads();");
+    body.line("sfx_mbar_wait(sbar, 0);");
+    ks.smem = static_cast<int>(bar_off + 16);
+  } else {
+    body.line("const " + it + " row = (" + it + ")blockIdx.x;");
+  }
   Ix rowix = em.uni("row");
+  // staged slices: element (row, col) of input k at sl_k[col - q*SL]
+  std::map<int, std::pair<std::string, std::string>> staged_map;
+  if (CS > 1) {
+    std::string rb = em.ivar(Emitter::iadd(em.ivar(Emitter::imul("row", C)), em.ivar(Emitter::imul("q", SL))));
+    for (size_t k = 0; k < staged.size(); ++k) {
+      std::string p = em.fresh("sl");
+      body.line("const float* " + p + " = (const float*)(sfx_smem + " + fmt_i(static_cast<int64_t>(k) * slice_bytes) +
+                ");");
+      staged_map[staged[k]] = {p, rb};
+    }
+    em.staged = staged_map;
+  }
   std::map<int, std::string> reduced;
   em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
     if (c.g.nodes[node].op != SFX_OP_REDUCE || degenerate_reduce(c.g, c.g.nodes[node])) return "";
@@ -911,29 +970,31 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   auto acc_type = [&](const Node& rn) -> std::string {
     return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
   };
-  // a loop over the row's vectors, UR per iteration; `emit(col_var)` emits one
-  // vector's work inside a scope
-  // (full tiles unguarded so all UR vectors' loads issue together, then the
-  // remainder one vector at a time)
+  // a loop over this CTA's vectors, UR per iteration (full tiles unguarded so
+  // all UR vectors' loads issue together, then the remainder one at a time);
+  // `emit(col_var)` emits one vector's work
+  const std::string vbase = CS > 1 ? "(" + it + ")q * " + fmt_i(SLV) + " + " : "";
   auto row_loop = [&](const std::function<void(const std::string&)>& emit) {
     const std::string j = em.fresh("j");
     body.line(it + " " + j + " = tid;");
-    body.line("for (; " + j + " + " + std::to_string((UR - 1) * B) + " < " + fmt_i(NV) + "; " + j + " += " +
+    body.line("for (; " + j + " + " + std::to_string((UR - 1) * B) + " < " + fmt_i(SLV) + "; " + j + " += " +
               std::to_string(B * UR) + ") {");
     body.indent++;
     em.push();
     for (int u = 0; u < UR; ++u) {
       const std::string ju = em.fresh("ju");
-      body.line("const " + it + " " + ju + " = " + j + " + " + std::to_string(u * B) + ";");
+      body.line("const " + it + " " + ju + " = " + vbase + j + " + " + std::to_string(u * B) + ";");
       emit(em.ivar(Emitter::imul(ju, V)));
     }
     em.pop();
     body.indent--;
     body.line("}");
-    body.line("for (; " + j + " < " + fmt_i(NV) + "; " + j + " += " + std::to_string(B) + ") {");
+    body.line("for (; " + j + " < " + fmt_i(SLV) + "; " + j + " += " + std::to_string(B) + ") {");
     body.indent++;
     em.push();
-    emit(em.ivar(Emitter::imul(j, V)));
+    const std::string jv = em.fresh("jv");
+    body.line("const " + it + " " + jv + " = " + vbase + j + ";");
+    emit(em.ivar(Emitter::imul(jv, V)));
     em.pop();
     body.indent--;
     body.line("}");
@@ -976,18 +1037,31 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
       body.line(acc[k] + " = " + sm + "[0];");
       body.line("for (int w = 1; w < " + std::to_string(W) + "; ++w) " + acc[k] + " = " + fold_of(rn) + "(" + acc[k] +
                 ", " + sm + "[w]);");
+      if (CS > 1) {
+        // cluster combine: every CTA folds the CS partials in rank order
+        const std::string xp = em.fresh("xp");
+        body.line("__shared__ " + T + " " + xp + ";");
+        body.line("if (tid == 0) " + xp + " = " + acc[k] + ";");
+        body.line("sfx_cluster_sync();");
+        body.line(acc[k] + " = sfx_dsmem_ld(&" + xp + ", 0u);");
+        body.line("for (unsigned r = 1; r < " + std::to_string(CS) + "u; ++r) " + acc[k] + " = " + fold_of(rn) + "(" +
+                  acc[k] + ", sfx_dsmem_ld(&" + xp + ", r));");
+      }
       std::string fin = acc[k];
       if (T == "double") {
         fin = em.fresh("red");
         body.line("const float " + fin + " = (float)" + acc[k] + ";");
       }
       if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
-        // the sequential fold's first element: the row's element 0
+        // the sequential fold's first element: the row's element 0, read from
+        // global memory (with a cluster it sits in rank 0's slice only)
         em.push();
+        em.staged.clear();
         em.lane = 0;
         const Node& in = c.g.nodes[rn.operands[0]];
         std::string f0 = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, em.uni("0")));
         body.line(fin + " = sfx_fold_first(" + f0 + ", " + fin + ");");
+        em.staged = staged_map;
         em.pop();
       }
       reduced[red[k]] = fin;
@@ -1016,7 +1090,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     });
   if (!row_roots.empty()) {
     em.lane = 0;
-    body.line("if (tid == 0) {");
+    em.staged.clear();
+    body.line(CS > 1 ? "if (tid == 0 && q == 0) {" : "if (tid == 0) {");
     body.indent++;
     em.push();
     for (int r : row_roots)
@@ -1026,16 +1101,23 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.indent--;
     body.line("}");
   }
+  em.staged.clear();
+  if (CS > 1) body.line("sfx_cluster_sync();  // no CTA leaves while a peer may still read its partials");
   ks.code = assemble(sig, body);
   ks.block = B;
-  ks.grid_x = R;
+  ks.grid_x = R * CS;
   ks.vector_width = V;
-  // residency cap through dynamic shared memory (the re-read rows of all
-  // resident CTAs must stay in L2): pipe_ctas_per_sm = CTAs per SM
-  if (o.pipe_ctas_per_sm > 0) ks.smem = 220 * 1024 / o.pipe_ctas_per_sm;
-  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
-            " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
-            " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
+  // residency cap through dynamic shared memory (plain variant, A/B knob)
+  if (CS == 1 && o.pipe_ctas_per_sm > 0) ks.smem = 220 * 1024 / o.pipe_ctas_per_sm;
+  if (CS > 1)
+    ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " cluster of " + std::to_string(CS) +
+              " CTAs x " + std::to_string(B) + " threads per row, " + std::to_string(staged.size()) +
+              " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), DSMEM combine, levels=" +
+              std::to_string(rp.max_level);
+  else
+    ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
+              " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
+              " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
   return ks;
 }
 

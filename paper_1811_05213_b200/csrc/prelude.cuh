@@ -160,6 +160,38 @@ __device__ __forceinline__ void sfx_mbar_wait(unsigned long long* bar, unsigned 
       "SFX_DONE:\n"
       "}\n" :: "r"(sfx_smem_u32(bar)), "r"(parity) : "memory");
 }
+// ---- thread-block clusters: distributed shared memory (long-row cluster template) ----
+__device__ __forceinline__ unsigned sfx_cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// every CTA of the cluster arrives (release) and waits (acquire): smem writes
+// before it are visible to DSMEM reads after it, cluster-wide
+__device__ __forceinline__ void sfx_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned sfx_dsmem_addr(const void* p, unsigned rank) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(sfx_smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ float sfx_dsmem_ld(const float* p, unsigned rank) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(sfx_dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ double sfx_dsmem_ld(const double* p, unsigned rank) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(sfx_dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ int sfx_dsmem_ld(const int* p, unsigned rank) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(sfx_dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+
 // Reused 128-bit loads (broadcast vectors): default caching.
 __device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
 __device__ __forceinline__ sfx_i4 sfx_ld4(const int* p) { return *reinterpret_cast<const sfx_i4*>(p); }

@@ -29,8 +29,7 @@ for name, doc in CASES.items():
     bpath = os.path.join(tempfile.gettempdir(), name + ".json")
     open(bpath, "w").write(out)
     g, rep, b = H.load_bundle(bpath)
-    variants = [{}] + [dict(items_per_thread=u, threads_per_row=t, pipe_ctas_per_sm=m)
-                       for u, t, m in ((8, 1024, 0), (4, 1024, 1), (8, 1024, 1), (8, 512, 2), (16, 512, 2), (8, 512, 1))]
+    variants = [{}, {"row_pipeline": 1}, {"threads_per_row": 256}, {"threads_per_row": 1024}]
     if "--literal" in sys.argv:
         variants.append({"strategy": "literal"})
     for kw in variants:
