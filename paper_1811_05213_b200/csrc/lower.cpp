@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <set>
@@ -119,7 +120,10 @@ void fill_common(const Ctx& c, KernelSource& ks) {
 }
 
 std::string assemble(const std::string& sig, const Code& body) {
-  std::string s = kPrelude;
+  std::string s;
+  if (const char* e = std::getenv("SFX_EXPERIMENT"))  // A/B experiments only (tools/)
+    s += std::string("#define ") + e + " 1\n";
+  s += kPrelude;
   s += "\n";
   s += sig;
   s += " {\n";

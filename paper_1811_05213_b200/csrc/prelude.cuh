@@ -197,13 +197,14 @@ __device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_
 __device__ __forceinline__ sfx_i4 sfx_ld4(const int* p) { return *reinterpret_cast<const sfx_i4*>(p); }
 __device__ __forceinline__ float sfx_ld(const float* p) { return __ldg(p); }
 __device__ __forceinline__ int sfx_ld(const int* p) { return __ldg(p); }
+// Root stores: streaming (st.global.cs, evict-first in L2) — a root is written
+// once and the inputs still streaming in keep the L2 (measured on B200:
+// probs_d 463 -> 449 us, ctx_r 37.2 -> 35.3 us, h1 66.0 -> 63.9 us).
 __device__ __forceinline__ void sfx_st4(float* p, float a, float b, float c, float d) {
-  sfx_f4 v; v.x = a; v.y = b; v.z = c; v.w = d;
-  *reinterpret_cast<sfx_f4*>(p) = v;
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 __device__ __forceinline__ void sfx_st4(int* p, int a, int b, int c, int d) {
-  sfx_i4 v; v.x = a; v.y = b; v.z = c; v.w = d;
-  *reinterpret_cast<sfx_i4*>(p) = v;
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 // ---- cross-thread combine ----
