@@ -141,7 +141,8 @@ enum {
   SFX_STRATEGY_LITERAL = 1, /* literal KernelProgram lowering (reference chunking and fold order) */
   SFX_STRATEGY_MAP = 2,
   SFX_STRATEGY_ROW = 3,
-  SFX_STRATEGY_COL = 4
+  SFX_STRATEGY_COL = 4,
+  SFX_STRATEGY_COLBC = 5    /* column reductions broadcast back (batch-norm): grid barriers, one launch */
 };
 typedef struct sfx_compile_opts {
   int32_t strategy;      /* SFX_STRATEGY_* ; forcing an inapplicable one fails with SFX_ERR_UNSUPPORTED */

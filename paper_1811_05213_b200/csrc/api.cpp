@@ -330,9 +330,15 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
   }
   // programmatic dependent launch (every generated kernel begins with
   // griddepcontrol.wait, so stream order is preserved)
-  CUlaunchAttribute attr[1];
+  CUlaunchAttribute attr[2];
   attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
   attr[0].value.programmaticStreamSerializationAllowed = 1;
+  unsigned n_attr = 1;
+  if (k->src.cooperative) {  // grid barriers: the driver refuses a grid that cannot be co-resident
+    attr[1].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+    attr[1].value.cooperative = 1;
+    n_attr = 2;
+  }
   CUlaunchConfig cfg{};
   cfg.gridDimX = static_cast<unsigned>(k->src.grid_x);
   cfg.gridDimY = static_cast<unsigned>(k->src.grid_y);
@@ -347,7 +353,7 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
   cfg.sharedMemBytes = static_cast<unsigned>(k->src.smem);
   cfg.hStream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n_attr;
   sfx::check_cu(sfx::driver().cuLaunchKernelEx(&cfg, k->fn, args.data(), nullptr), "cuLaunchKernelEx");
   k->ctx->launches.fetch_add(1);
 }

@@ -387,6 +387,115 @@ bool analyze_col(const Ctx& c, ColPlan* cp, std::string* why) {
   return true;
 }
 
+// ---- COL with broadcast-back analysis (batch-norm statistics) ------------------
+
+// Column reductions over one contiguous block of dims ([outer | reduced |
+// inner], like COL) whose results are broadcast back over the reduced dims and
+// combined with the elements again — batch-norm's mean / var / normalise, the
+// pattern the reference plans as one group with a Column schedule (one block
+// per column).  Classes: FULL ([O, R, I] elements) and COLV ([O, I] columns).
+struct ColBcPlan {
+  int64_t O = 0, R = 0, I = 0;
+  std::map<int, int> level;
+  int max_level = 0;
+};
+
+bool analyze_colbc(const Ctx& c, ColBcPlan* bp, std::string* why) {
+  const Graph& g = c.g;
+  if (!c.dots.empty()) return *why = "group contains a matmul", false;
+  if (c.reduces.empty()) return *why = "no reduction", false;
+  std::vector<int> kept;  // FULL-space axes that survive the reductions (of the reduce operands)
+  for (int r : c.reduces) {
+    const Node& n = g.nodes[r];
+    const Node& in = g.nodes[n.operands[0]];
+    std::vector<int64_t> rd = n.reduce_dims;
+    std::sort(rd.begin(), rd.end());
+    for (size_t i = 0; i < rd.size(); ++i)
+      if (rd[i] != rd[0] + static_cast<int64_t>(i)) return *why = "reduce " + n.id + " dims are not contiguous", false;
+    const int k0 = static_cast<int>(rd[0]), k1 = static_cast<int>(rd.back()) + 1;
+    const int64_t O = prod(in.dims, 0, k0), R = prod(in.dims, k0, k1), I = prod(in.dims, k1, in.dims.size());
+    if (bp->R == 0) {
+      bp->O = O, bp->R = R, bp->I = I;
+    } else if (bp->O != O || bp->R != R || bp->I != I) {
+      return *why = "column reductions with different geometry", false;
+    }
+  }
+  const int64_t O = bp->O, R = bp->R, I = bp->I, C = O * I;
+  if (R <= 1) return *why = "degenerate column length", false;
+  enum { FULL = 1, COLV = 2 };
+  std::map<int, int> cls;
+  auto cls_of = [&](int64_t n) { return n == O * R * I ? FULL : n == C ? COLV : 0; };
+  for (int m : c.topo) {
+    const Node& n = g.nodes[m];
+    if (!c.dep.at(m)) continue;
+    if (n.op == SFX_OP_REDUCE && !degenerate_reduce(g, n)) {
+      int op = n.operands[0];
+      if (c.p.is_member(op) && c.dep.at(op) && cls[op] != FULL)
+        return *why = "reduce operand " + g.nodes[op].id + " is not element-shaped", false;
+      cls[m] = COLV;
+      int lv = 1;
+      std::set<int> seen;
+      std::function<void(int)> walk = [&](int x) {
+        if (!c.p.is_member(x) || seen.count(x)) return;
+        seen.insert(x);
+        if (x != m && g.nodes[x].op == SFX_OP_REDUCE && !degenerate_reduce(g, g.nodes[x]))
+          lv = std::max(lv, bp->level[x] + 1);
+        else
+          for (int o : g.nodes[x].operands) walk(o);
+      };
+      for (int o : n.operands) walk(o);
+      bp->level[m] = lv;
+      bp->max_level = std::max(bp->max_level, lv);
+      continue;
+    }
+    int k = cls_of(n.numel());
+    if (!k) return *why = "member " + n.id + " is neither element- nor column-shaped", false;
+    for (int op : n.operands) {
+      if (!c.p.is_member(op) || !c.dep.at(op)) continue;
+      int oc = cls[op];
+      switch (n.op) {
+        case SFX_OP_ELEMENTWISE:
+        case SFX_OP_RESHAPE:
+        case SFX_OP_BITCAST:
+        case SFX_OP_REDUCE:  // degenerate
+          if (oc != k) return *why = "class mismatch at " + n.id, false;
+          break;
+        case SFX_OP_TRANSPOSE:
+          if (oc != k || !transpose_is_reshape(n)) return *why = "transpose of dependent data at " + n.id, false;
+          break;
+        case SFX_OP_BROADCAST: {
+          if (bcast_is_reshape(n) && oc == k) break;
+          // columns broadcast back over the reduced block: the output splits as
+          // [O dims | R dims | I dims] and the operand maps onto the O and I dims
+          int k0 = prefix_split(n.dims, O), k1 = k0 < 0 ? -1 : prefix_split(n.dims, O * R);
+          bool ok = k == FULL && oc == COLV && k0 >= 0 && k1 >= k0 && prod(n.dims, k1, n.dims.size()) == I;
+          std::vector<int64_t> want;
+          for (int d = 0; d < n.rank(); ++d)
+            if ((d < k0 || d >= k1) && n.dims[d] != 1) want.push_back(d);
+          std::vector<int64_t> have;
+          for (size_t j = 0; j < n.dim_map.size(); ++j)
+            if (g.nodes[op].dims[j] != 1) have.push_back(n.dim_map[j]);
+          if (!ok || want != have) return *why = "broadcast " + n.id + " does not map columns to columns", false;
+          break;
+        }
+        default:
+          return *why = "unsupported op at " + n.id, false;
+      }
+    }
+    cls[m] = k;
+  }
+  bool back = false;  // at least one reduction feeds an element again
+  for (int m : c.topo)
+    if (c.dep.at(m) && cls[m] == FULL) back = true;
+  if (!back) return *why = "no broadcast back (column template)", false;
+  for (int r : c.p.roots) {
+    int k = cls_of(c.g.nodes[r].numel());
+    if (!k) return *why = "root " + g.nodes[r].id + " is neither element- nor column-shaped", false;
+    if (c.dep.at(r) && cls[r] != k) return *why = "root class mismatch", false;
+  }
+  return true;
+}
+
 // ---- MAP -----------------------------------------------------------------------
 
 bool analyze_map(const Ctx& c, std::string* why) {
@@ -1801,6 +1910,288 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   return ks;
 }
 
+// Column reductions broadcast back (batch-norm): one launch, a co-resident
+// grid of column tiles x row stripes (2 CTAs/SM, one wave, cooperative
+// launch).  Per reduction level: every CTA folds its stripe (per-lane fp64
+// accumulators for f32 sums), combines its warps through shared memory and
+// writes a partial; a grid barrier; then every thread folds the S stripe
+// partials of its own columns in stripe order (identical totals in every CTA)
+// and keeps them in registers, where the broadcast-back reads them.  A final
+// pass writes the element roots.  Passes after the first re-read the stripe,
+// mostly from L2 (batch-norm [65536, 256]: 64 MB).
+KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "colbc";
+  ks.entry = "sfx_colbc_" + c.name;
+  fill_common(c, ks);
+  const int64_t O = bp.O, R = bp.R, I = bp.I, C = O * I;
+  const int V = (I % 4 == 0) ? 4 : 1;
+  const int64_t cvec = (C + V - 1) / V;
+  int CL = 1;
+  while (CL < 32 && CL < cvec) CL *= 2;
+  const int RL = 32 / CL;
+  const int WARPS = 8, B = WARPS * 32;
+  const int RSUB = WARPS * RL;
+  const int64_t TC = static_cast<int64_t>(CL) * V;
+  const int64_t tiles = (C + TC - 1) / TC;
+  const int ctas_per_sm = 2;
+  if (tiles > int64_t{kNumSMs} * ctas_per_sm)
+    throw Error(SFX_ERR_UNSUPPORTED, "colbc: " + std::to_string(tiles) + " column tiles exceed one co-resident wave");
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / tiles);
+  S = std::min<int64_t>(S, std::max<int64_t>(1, R / RSUB));
+  S = std::max<int64_t>(1, std::min<int64_t>(S, kNumSMs * ctas_per_sm / tiles));
+  const int64_t RS = (R + S - 1) / S;
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
+  const int NR = static_cast<int>(c.reduces.size());
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  auto acc_t = [&](int r) -> std::string {
+    const Node& rn = c.g.nodes[r];
+    return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
+  };
+  auto fold_fn = [&](int r) -> const char* {
+    const Node& rn = c.g.nodes[r];
+    return rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum" : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax"
+                                                                                         : "sfx_fold_pmin";
+  };
+  // workspace: barrier counters (64 words), then per reduce partials[S][C] and totals[C] (8-byte slots)
+  std::map<int, int64_t> part_word, tot_word;
+  int64_t words = 64;
+  for (int r : c.reduces) {
+    part_word[r] = words;
+    words += S * C * 2;
+    tot_word[r] = words;
+    words += C * 2 + 64;
+  }
+  ks.workspace_bytes = words * 4;
+  ks.cooperative = true;
+  body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const int cl = lane & " + std::to_string(CL - 1) + ", rl = lane / " + std::to_string(CL) + ";");
+  body.line("const int rsub = warp * " + std::to_string(RL) + " + rl;");
+  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cl * " + std::to_string(V) + ";");
+  body.line("const bool cok = c0 < " + fmt_i(C) + ";");
+  body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
+  body.line("const " + it + " co = cok ? c0 / " + fmt_i(I) + " : 0, ci = cok ? c0 % " + fmt_i(I) + " : 0;");
+  auto inner_ix = [&](int lane) {
+    em.lane = lane;
+    return V == 1 ? em.uni("ci") : em.lane_plus("ci");
+  };
+  // totals of every finished level, per lane, in registers
+  std::map<int, std::vector<std::string>> total;
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    auto f = total.find(node);
+    if (f == total.end()) {
+      if (c.g.nodes[node].op == SFX_OP_REDUCE && !degenerate_reduce(c.g, c.g.nodes[node]))
+        throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
+      return "";
+    }
+    return f->second[em.lane];
+  };
+  // a pass over this CTA's stripe: UR rows per iteration (unguarded, loads in
+  // flight together), then the remainder
+  auto stripe_pass = [&](const std::function<void(const std::string&)>& row) {
+    body.line("if (cok) {");
+    body.indent++;
+    const std::string r = em.fresh("r");
+    body.line(it + " " + r + " = r_begin + rsub;");
+    body.line("for (; " + r + " + " + std::to_string((UR - 1) * RSUB) + " < r_end; " + r + " += " +
+              std::to_string(UR * RSUB) + ") {");
+    body.indent++;
+    em.push();
+    for (int u = 0; u < UR; ++u) {
+      std::string ru = em.fresh("ru");
+      body.line("const " + it + " " + ru + " = " + r + " + " + std::to_string(u * RSUB) + ";");
+      row(ru);
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.line("for (; " + r + " < r_end; " + r + " += " + std::to_string(RSUB) + ") {");
+    body.indent++;
+    em.push();
+    row(r);
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.indent--;
+    body.line("}");
+  };
+  for (int lv = 1; lv <= bp.max_level; ++lv) {
+    std::vector<int> red;
+    for (int r : c.reduces)
+      if (bp.level.at(r) == lv) red.push_back(r);
+    std::vector<std::vector<std::string>> acc(red.size(), std::vector<std::string>(V));
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      std::string init = rn.reducer == SFX_REDUCE_SUM ? (rn.dtype == SFX_F32 ? "0.0" : "0")
+                         : rn.dtype == SFX_F32        ? "sfx_bits_f(0x7fc00000)"
+                         : rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+      for (int l = 0; l < V; ++l) {
+        acc[k][l] = em.fresh("acc");
+        body.line(acc_t(red[k]) + " " + acc[k][l] + " = " + init + ";");
+      }
+    }
+    stripe_pass([&](const std::string& ru) {
+      Ix rix = em.uni(ru), oix = em.uni("co");
+      for (int l = 0; l < V; ++l) {
+        Ix iix = inner_ix(l);
+        for (size_t k = 0; k < red.size(); ++k) {
+          const Node& rn = c.g.nodes[red[k]];
+          const Node& in = c.g.nodes[rn.operands[0]];
+          std::string v = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, oix, rix, iix));
+          body.line(acc[k][l] + " = " + fold_fn(red[k]) + "(" + acc[k][l] + ", " + v + ");");
+        }
+      }
+    });
+    // CTA combine over row sub-streams (deterministic order), partials out
+    for (size_t k = 0; k < red.size(); ++k) {
+      const std::string T = acc_t(red[k]);
+      const std::string sp = em.fresh("sp");
+      body.line("__shared__ " + T + " " + sp + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
+      for (int l = 0; l < V; ++l)
+        body.line(sp + "[rsub][cl * " + std::to_string(V) + " + " + std::to_string(l) + "] = " + acc[k][l] + ";");
+      body.line("__syncthreads();");
+      body.line("if (warp == 0 && rl == 0 && cok) {");
+      for (int l = 0; l < V; ++l) {
+        std::string sidx = "cl * " + std::to_string(V) + " + " + std::to_string(l);
+        std::string t = em.fresh("t");
+        body.line("  " + T + " " + t + " = " + sp + "[0][" + sidx + "];");
+        body.line("  for (int w = 1; w < " + std::to_string(RSUB) + "; ++w) " + t + " = " + fold_fn(red[k]) + "(" + t +
+                  ", " + sp + "[w][" + sidx + "]);");
+        body.line("  *(" + T + "*)((unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) + ") + (" + it +
+                  ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + ") = " + t + ";");
+      }
+      body.line("}");
+    }
+    body.line("sfx_grid_barrier(ws, " + std::to_string(2 * lv - 1) + "u);");
+    // the S stripe partials of each column are folded once, spread over the
+    // tile's S CTAs (CTA y takes columns y, y + S, ...; its 256 threads split
+    // the stripes and combine by a fixed shuffle / warp-order tree), into
+    // totals[C]; a second barrier; then every thread reads its columns'
+    // totals.  (Every CTA folding all S partials itself cost ~4x the data
+    // pass in L2 loads: batch-norm [65536,256] 208 us.)
+    for (size_t k = 0; k < red.size(); ++k) {
+      const std::string T = acc_t(red[k]);
+      const Node& rn = c.g.nodes[red[k]];
+      std::string ident = rn.reducer == SFX_REDUCE_SUM ? (T == "double" ? "0.0" : "0")
+                          : rn.dtype == SFX_F32        ? "sfx_bits_f(0x7fc00000)"
+                          : rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+      const std::string pt = "(const unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) + ")";
+      const std::string tt = "(unsigned long long*)(ws + " + fmt_i(tot_word[red[k]]) + ")";
+      const std::string fs = em.fresh("fs");
+      body.line("__shared__ " + T + " " + fs + "[" + std::to_string(WARPS) + "];");
+      body.line("for (" + it + " cc = blockIdx.y; cc < " + fmt_i(TC) + "; cc += " + fmt_i(S) + ") {");
+      body.line("  const " + it + " col = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cc;");
+      body.line("  if (col >= " + fmt_i(C) + ") break;");
+      body.line("  " + T + " a = " + ident + ";");
+      body.line("  for (" + it + " s = threadIdx.x; s < " + fmt_i(S) + "; s += " + std::to_string(B) + ") a = " +
+                fold_fn(red[k]) + "(a, __ldcg((const " + T + "*)(" + pt + " + s * " + fmt_i(C) + " + col)));");
+      body.line(std::string("  for (int m = 16; m >= 1; m /= 2) a = ") + fold_fn(red[k]) +
+                "(a, __shfl_xor_sync(0xffffffffu, a, m));");
+      body.line("  if (lane == 0) " + fs + "[warp] = a;");
+      body.line("  __syncthreads();");
+      body.line("  if (threadIdx.x == 0) {");
+      body.line("    " + T + " t = " + fs + "[0];");
+      body.line("    for (int w = 1; w < " + std::to_string(WARPS) + "; ++w) t = " + std::string(fold_fn(red[k])) + "(t, " +
+                fs + "[w]);");
+      body.line("    *(" + T + "*)(" + tt + " + col) = t;");
+      body.line("  }");
+      body.line("  __syncthreads();");
+      body.line("}");
+    }
+    body.line("sfx_grid_barrier(ws, " + std::to_string(2 * lv) + "u);");
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      const std::string T = acc_t(red[k]);
+      std::vector<std::string> tv(V);
+      for (int l = 0; l < V; ++l) {
+        tv[l] = em.fresh("tot");
+        body.line(T + " " + tv[l] + " = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
+                  fmt_i(tot_word[red[k]]) + ") + (cok ? c0 : 0) + " + std::to_string(l) + "));");
+      }
+      if (T == "double")
+        for (int l = 0; l < V; ++l) {
+          std::string f = em.fresh("tot");
+          body.line("const float " + f + " = (float)" + tv[l] + ";");
+          tv[l] = f;
+        }
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+        const Node& in = c.g.nodes[rn.operands[0]];
+        for (int l = 0; l < V; ++l) {
+          em.push();
+          Ix iix = inner_ix(l);
+          std::string f0 = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
+          body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
+          em.pop();
+        }
+      }
+      total[red[k]] = tv;
+    }
+  }
+  // final pass: element roots; column roots from stripe 0
+  std::vector<int> full_roots, col_roots;
+  for (int r : c.p.roots) (c.g.nodes[r].numel() == O * R * I ? full_roots : col_roots).push_back(r);
+  if (!full_roots.empty())
+    stripe_pass([&](const std::string& ru) {
+      Ix rix = em.uni(ru), oix = em.uni("co");
+      std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+      std::vector<std::string> faddr(full_roots.size());
+      std::vector<bool> fvec(full_roots.size(), V == 4);
+      std::vector<std::vector<std::string>> fad(full_roots.size(), std::vector<std::string>(V));
+      for (int l = 0; l < V; ++l) {
+        Ix iix = inner_ix(l);
+        for (size_t k = 0; k < full_roots.size(); ++k) {
+          std::vector<Ix> comps = orc_comps(em, c.g.nodes[full_roots[k]].dims, O, R, I, oix, rix, iix);
+          fv[k][l] = em.value(full_roots[k], comps);
+          Ix L = em.linearize(comps, c.g.nodes[full_roots[k]].dims);
+          fad[k][l] = L.e;
+          if (l == 0) {
+            if (L.kind == IX_PLUS) faddr[k] = L.base;
+            else fvec[k] = false;
+          }
+        }
+      }
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+        if (fvec[k])
+          body.line("sfx_st4(" + out + " + " + faddr[k] + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] + ", " +
+                    fv[k][3] + ");");
+        else
+          for (int l = 0; l < V; ++l) body.line(out + "[" + fad[k][l] + "] = " + fv[k][l] + ";");
+      }
+    });
+  if (!col_roots.empty()) {
+    body.line("if (blockIdx.y == 0 && warp == 0 && rl == 0 && cok) {");
+    body.indent++;
+    em.push();
+    for (int r : col_roots) {
+      for (int l = 0; l < V; ++l) {
+        em.lane = l;
+        Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+        std::string v = em.value(r, em.from_linear(col, c.g.nodes[r].dims));
+        body.line("out" + std::to_string(root_slot(c, r)) + "[c0 + " + std::to_string(l) + "] = " + v + ";");
+      }
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  body.line("sfx_grid_exit(ws);");
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = tiles;
+  ks.grid_y = S;
+  ks.vector_width = V;
+  ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
+            " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " levels=" +
+            std::to_string(bp.max_level) + " (grid barriers, cooperative launch)";
+  return ks;
+}
+
 // ---- LITERAL --------------------------------------------------------------------
 
 // chunk_box geometry (reference schedule.cpp:52-76) for a materialised member
@@ -1991,7 +2382,12 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   ColPlan cp;
   if (analyze_col(c, &cp, &w)) return "col";
   reasons += "; col: " + w;
-  if (analyze_row(c, &rp, &w)) return "row";  // long rows: one CTA per row, multi-pass
+  if (analyze_row(c, &rp, &w)) return "row";  // long rows: clusters / multi-pass (before colbc: measured 7x faster)
+  ColBcPlan bp;
+  if (analyze_colbc(c, &bp, &w) &&
+      (bp.O * bp.I + 127) / 128 <= int64_t{kNumSMs} * 2)  // column tiles fit one co-resident wave
+    return "colbc";
+  reasons += "; colbc: " + w;
   if (why) *why = reasons;
   return "literal";
 }
@@ -2022,7 +2418,7 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
     std::string s = choose_strategy(g, pi, &why);
     if (s == "dot") return lower_dot(g, p);
     strat = s == "map" ? SFX_STRATEGY_MAP : s == "row" ? SFX_STRATEGY_ROW : s == "col" ? SFX_STRATEGY_COL
-                                                                                        : SFX_STRATEGY_LITERAL;
+            : s == "colbc" ? SFX_STRATEGY_COLBC : SFX_STRATEGY_LITERAL;
   }
   KernelSource ks;
   switch (strat) {
@@ -2061,6 +2457,12 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
       ColPlan cp;
       if (!analyze_col(c, &cp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "col template not applicable: " + why);
       ks = lower_col(c, cp, o);
+      break;
+    }
+    case SFX_STRATEGY_COLBC: {
+      ColBcPlan bp;
+      if (!analyze_colbc(c, &bp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "colbc template not applicable: " + why);
+      ks = lower_colbc(c, bp, o);
       break;
     }
     case SFX_STRATEGY_LITERAL:

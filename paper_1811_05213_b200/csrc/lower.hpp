@@ -40,6 +40,7 @@ struct KernelSource {
   int block = 256;
   int smem = 0;              // dynamic shared memory bytes
   int64_t workspace_bytes = 0;
+  bool cooperative = false;  // grid-wide barriers: launched cooperatively (co-residency checked)
   // cross-rank column combine (opts.cross_rank): bytes of the symmetric peer
   // arena this kernel needs; the kernel then takes (peers, peer_off, rank,
   // nranks) after ws

@@ -110,6 +110,35 @@ __device__ __forceinline__ unsigned long long sfx_globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+__device__ __forceinline__ unsigned sfx_ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Grid-wide barrier of a co-resident grid (one wave, cooperative launch):
+// arrival counter ctr[0] grows by gridDim.x*gridDim.y per barrier; barrier k
+// (1-based) waits for k*G arrivals.  sfx_grid_exit resets the counters once
+// every CTA has passed its last barrier, so the next launch starts from zero.
+__device__ __forceinline__ void sfx_grid_barrier(unsigned* ctr, unsigned k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned target = k * gridDim.x * gridDim.y;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned long long t0 = sfx_globaltimer();
+    while (sfx_ld_acquire_gpu(ctr) < target) {
+      if (sfx_globaltimer() - t0 > 20000000000ull) __trap();
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void sfx_grid_exit(unsigned* ctr) {
+  if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x * gridDim.y - 1u) {
+    ctr[0] = 0u;
+    ctr[1] = 0u;
+  }
+}
 // Host-streaming gate: wait until the copy stream has published chunk count
 // `need` (cuStreamWriteValue32 after the chunk's host->device copies).
 __device__ __forceinline__ void sfx_gate_wait(const unsigned* gate, unsigned need) {

@@ -36,7 +36,7 @@ OPCODES = {
 EW_KINDS = ["add", "sub", "mul", "max", "min", "neg", "compare", "select", "scale",
             "exp", "log", "div", "pow", "tanh", "sqrt", "rsqrt"]
 REDUCERS = {"sum": 0, "max": 1, "min": 2}
-STRATEGIES = {"auto": 0, "literal": 1, "map": 2, "row": 3, "col": 4}
+STRATEGIES = {"auto": 0, "literal": 1, "map": 2, "row": 3, "col": 4, "colbc": 5}
 EXPENSIVE = {"exp", "log", "div", "pow", "tanh", "sqrt", "rsqrt"}
 
 

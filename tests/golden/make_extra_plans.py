@@ -17,6 +17,35 @@ sys.path.insert(0, ROOT)
 
 from workloads import configs  # noqa: E402
 
+def bn_graph(shape, rdims, with_stats=False):
+    """Batch-norm statistics + normalise over `rdims` (contiguous), gamma/beta on the kept dims."""
+    kept = [d for d in range(len(shape)) if d not in rdims]
+    cshape = [shape[d] for d in kept]
+    ins = [
+        {"id": "x", "op": "parameter", "shape": shape},
+        {"id": "g", "op": "parameter", "shape": cshape},
+        {"id": "b", "op": "parameter", "shape": cshape},
+        {"id": "mean", "op": "reduce", "operands": ["x"], "shape": cshape, "reduce_dims": rdims, "reducer": "mean"},
+        {"id": "mean_b", "op": "broadcast", "operands": ["mean"], "shape": shape, "broadcast_dim_map": kept},
+        {"id": "d", "op": "sub", "operands": ["x", "mean_b"], "shape": shape},
+        {"id": "d2", "op": "mul", "operands": ["d", "d"], "shape": shape},
+        {"id": "var", "op": "reduce", "operands": ["d2"], "shape": cshape, "reduce_dims": rdims, "reducer": "mean"},
+        {"id": "eps", "op": "constant", "shape": cshape, "value": 1e-5},
+        {"id": "ve", "op": "add", "operands": ["var", "eps"], "shape": cshape},
+        {"id": "rstd", "op": "rsqrt", "operands": ["ve"], "shape": cshape},
+        {"id": "rstd_b", "op": "broadcast", "operands": ["rstd"], "shape": shape, "broadcast_dim_map": kept},
+        {"id": "n", "op": "mul", "operands": ["d", "rstd_b"], "shape": shape},
+        {"id": "g_b", "op": "broadcast", "operands": ["g"], "shape": shape, "broadcast_dim_map": kept},
+        {"id": "b_b", "op": "broadcast", "operands": ["b"], "shape": shape, "broadcast_dim_map": kept},
+        {"id": "ng", "op": "mul", "operands": ["n", "g_b"], "shape": shape},
+        {"id": "y", "op": "add", "operands": ["ng", "b_b"], "shape": shape}]
+    outs = ["y"]
+    if with_stats:
+        ins.append({"id": "rstd_out", "op": "scale", "operands": ["rstd"], "shape": cshape, "scalar": 1.0})
+        outs.append("rstd_out")
+    return {"instructions": ins, "outputs": outs}
+
+
 EXTRA = {
     "ln_r64_c8192": configs.c1_layernorm(R=64, C=8192),
     "ln_r100_c3072": configs.c1_layernorm(R=100, C=3072),
@@ -27,6 +56,16 @@ EXTRA = {
     "softmax_r4_c131072": configs.c2_softmax(B=1, H=1, S=4, L=131072),
     "ln_r6_c98304": configs.c1_layernorm(R=6, C=98304),
     "ln_r5_c70001": configs.c1_layernorm(R=5, C=70001),
+    # column statistics broadcast back (batch-norm): the colbc template
+    "bn_4096x256": bn_graph([4096, 256], [0]),
+    "bn_mid_8x512x64": bn_graph([8, 512, 64], [1]),
+    "bn_nhwc_16x16x8x128": bn_graph([16, 16, 8, 128], [0, 1, 2], with_stats=True),
+    "bnmax_3000x37": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [3000, 37]},
+        {"id": "m", "op": "reduce", "operands": ["x"], "shape": [37], "reduce_dims": [0], "reducer": "max"},
+        {"id": "mb", "op": "broadcast", "operands": ["m"], "shape": [3000, 37], "broadcast_dim_map": [1]},
+        {"id": "z", "op": "sub", "operands": ["x", "mb"], "shape": [3000, 37]},
+        {"id": "e", "op": "exp", "operands": ["z"], "shape": [3000, 37]}], "outputs": ["e"]},
     # middle-axis and full reductions: the [outer | reduced | inner] column template
     "midsum_16x4096x64": {"instructions": [
         {"id": "x", "op": "parameter", "shape": [16, 4096, 64]},

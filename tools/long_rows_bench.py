@@ -1,5 +1,6 @@
-"""Throughput of the multi-pass long-row template (rows beyond 1024 threads x
-64 elements): softmax and LayerNorm with 128K-wide rows, planned by the
+"""Throughput of the templates for long rows (rows beyond 1024 threads x 64
+elements: softmax / LayerNorm with 128K-262K-wide rows) and for batch-norm
+statistics broadcast back (colbc), planned by the
 reference's compile_graph (oracle/_ref/ref_tool) at run time, timed with CUDA
 events over rotating buffers (> L2), GB/s of compulsory bytes."""
 import json
@@ -14,12 +15,21 @@ import torch  # noqa: E402
 from paper_1811_05213_b200 import host as H  # noqa: E402
 from workloads import configs  # noqa: E402
 
-CASES = {"softmax_1024x131072": configs.c2_softmax(B=1, H=1, S=1024, L=131072),
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+from make_extra_plans import bn_graph  # noqa: E402
+
+ONLY = [a for a in sys.argv[1:] if not a.startswith("--")]
+CASES = {"batchnorm_65536x256": bn_graph([65536, 256], [0]),
+         "batchnorm_262144x1024": bn_graph([262144, 1024], [0]),
+         "batchnorm_nhwc_64x56x56x256": bn_graph([64, 56, 56, 256], [0, 1, 2]),
+         "softmax_1024x131072": configs.c2_softmax(B=1, H=1, S=1024, L=131072),
          "layernorm_1024x131072": configs.c1_layernorm(R=1024, C=131072),
          "softmax_256x262144": configs.c2_softmax(B=1, H=1, S=256, L=262144)}
 dev = torch.device("cuda", 0)
 ctx = H.Context(0)
 for name, doc in CASES.items():
+    if ONLY and not any(name.startswith(o) for o in ONLY):
+        continue
     with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
         f.write(configs.dumps(doc))
         path = f.name
@@ -29,7 +39,7 @@ for name, doc in CASES.items():
     bpath = os.path.join(tempfile.gettempdir(), name + ".json")
     open(bpath, "w").write(out)
     g, rep, b = H.load_bundle(bpath)
-    variants = [{}, {"row_pipeline": 1}, {"threads_per_row": 256}, {"threads_per_row": 1024}]
+    variants = [{}] + ([{"rows_per_cta": 16}, {"rows_per_cta": 37}, {"items_per_thread": 4}] if name.startswith("batchnorm") else [{"row_pipeline": 1}])
     if "--literal" in sys.argv:
         variants.append({"strategy": "literal"})
     for kw in variants:
