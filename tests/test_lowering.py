@@ -1,0 +1,85 @@
+"""GroupAnalyzer / lowering decisions, on CPU (codegen + NVRTC to sm_100a, no
+GPU): which template each reference plan gets, and properties of the
+generated kernels that the GPU suite relies on."""
+
+import os
+import subprocess
+
+import pytest
+
+import sfx_testlib as T
+from paper_1811_05213_b200 import host as H
+
+EXTRA = os.path.join(T.GOLDEN, "plans_extra")
+
+
+def _note(path, k=0, **kw):
+    g, rep, _ = H.load_bundle(path)
+    src, cubin, note = H.codegen(g, rep.kernels[k].program, **kw)
+    return src, cubin, note
+
+
+@pytest.mark.parametrize("name,entry,strategy", [
+    ("softmax_r4_c131072", "sfx_rowcl_", "row"),      # cluster + DSMEM long rows
+    ("ln_r6_c98304", "sfx_rowcl_", "row"),
+    ("ln_r5_c70001", "sfx_rowmp_", "row"),            # odd width: multi-pass
+    ("softmax_r16_c16384", "sfx_row_", "row"),        # register-resident, multi-warp
+    ("bn_4096x256", "sfx_colbc_", "colbc"),           # batch-norm statistics broadcast back
+    ("bn_mid_8x512x64", "sfx_colbc_", "colbc"),
+    ("bnmax_3000x37", "sfx_colbc_", "colbc"),
+    ("midsum_16x4096x64", "sfx_col_", "col"),
+    ("fullmax_1024x1000", "sfx_col_", "col"),
+])
+def test_template_choice(name, entry, strategy):
+    src, _, note = _note(os.path.join(EXTRA, name + ".json"))
+    assert note.startswith(strategy), note
+    assert (" " + entry) in src, (name, note)
+
+
+def test_cluster_kernel_uses_tma_and_dsmem():
+    src, cubin, note = _note(os.path.join(EXTRA, "softmax_r4_c131072.json"))
+    assert "__cluster_dims__(8, 1, 1)" in src and "cluster of 8 CTAs" in note
+    sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass, "cp.async.bulk (TMA bulk copy) missing"
+    assert "SYNCS" in sass, "mbarrier wait missing"
+    assert "CGAERRBAR" in sass, "cluster barrier missing"
+
+
+def test_colbc_is_cooperative_with_grid_barriers():
+    src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
+    assert "sfx_grid_barrier(ws, 4u)" in src and "sfx_grid_exit(ws)" in src
+    assert "cooperative launch" in note
+
+
+def test_long_rows_prefer_row_templates_over_colbc():
+    """A row reduction broadcast back also parses as columns with I = 1; the
+    row templates are 7x faster on it, so they take precedence."""
+    for n in ("softmax_r4_c131072", "ln_r5_c70001"):
+        _, _, note = _note(os.path.join(EXTRA, n + ".json"))
+        assert note.startswith("row"), note
+
+
+def test_streaming_stores_in_templates():
+    src, _, _ = _note(os.path.join(T.PLANS, "C5.full.json"), k=4)  # probs_d
+    assert "st.global.cs.v4.f32" in src
+
+
+def test_host_stream_variant_differs_only_by_gates():
+    path = os.path.join(T.PLANS, "C1.full.json")
+    plain, _, _ = _note(path)
+    streamed, _, _ = _note(path, host_stream=1)
+    assert "sgate" not in plain and "sgate" in streamed and "sdone" in streamed
+
+
+def test_degenerate_reduce_is_a_reshape():
+    doc = {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [64, 1, 32]},
+        {"id": "r", "op": "reduce", "operands": ["x"], "shape": [64, 32], "reduce_dims": [1], "reducer": "max"},
+        {"id": "y", "op": "exp", "operands": ["r"], "shape": [64, 32]}], "outputs": ["y"]}
+    g = H.graph_from_json(doc)
+    prog = H.KernelProgram("y", ["r", "y"], ["y"], 1, 64, 0,
+                           [{"kind": "inline", "instr": "r"},
+                            {"kind": "materialize", "instr": "y", "schedule": [0, 1, "row"], "dest": "output",
+                             "root_index": 0}])
+    src, _, note = H.codegen(g, prog)
+    assert note.startswith("map"), note
