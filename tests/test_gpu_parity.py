@@ -393,3 +393,26 @@ def test_debug_coverage_check(ctx, name):
     ext = {e: inputs[e] for e in inputs}
     with pytest.raises(H.ExecError, match="incomplete coverage"):
         H.run_program(prog, g, ext, ctx=ctx, debug_checks=2)
+
+
+@pytest.mark.parametrize("name", ["bn_nhwc_16x16x8x128", "bn_4096x256"])
+def test_colbc_cuda_graph_replay(ctx, name):
+    """The cooperative grid-barrier kernel inside a captured CUDA graph (with a
+    map group on a concurrent branch for the NHWC plan), replayed 3 times on
+    one buffer set: the barrier counters reset themselves at kernel exit."""
+    import torch
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 17, -1.0, 1.0)
+    cg = H.CompiledGraph(ctx, g, rep)
+    try:
+        dev = torch.device("cuda", 0)
+        ins = [torch.from_numpy(np.ascontiguousarray(inputs[p])).to(dev) for p in cg.param_ids]
+        outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+        st = torch.cuda.Stream()
+        for _ in range(3):
+            cg.run([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], stream=st.cuda_stream, cuda_graph=True)
+        st.synchronize()
+        got = {o: t.cpu().numpy() for o, t in zip(g.outputs, outs)}
+    finally:
+        cg.close()
+    assert not _check(g, got, inputs, strict=True)
