@@ -1966,7 +1966,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   };
   // workspace: barrier counters (64 words), then per reduce partials[S][C] and totals[C] (8-byte slots)
   std::map<int, int64_t> part_word, tot_word;
-  int64_t words = 64;
+  int64_t words = 64;  // [0] arrivals, [1] exits, [2] launch sequence (cross-rank)
   for (int r : c.reduces) {
     part_word[r] = words;
     words += S * C * 2;
@@ -1975,6 +1975,22 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   }
   ks.workspace_bytes = words * 4;
   ks.cooperative = true;
+  // cross-rank (SyncBatchNorm): per level, each rank's column totals are pushed
+  // to every rank's peer arena (slots [2][PMAX][NR][C], 8 B) by the tile's first
+  // stripe CTA, flagged per tile with the step number, and folded in rank order
+  // by every thread.  Steps number (launch, level) pairs: launch_seq * L + lv.
+  const int PMAX = SFX_PEER_MAX_RANKS;
+  std::map<int, int> red_index;
+  for (int k = 0; k < NR; ++k) red_index[c.reduces[k]] = k;
+  const int64_t pflag_byte = (2LL * PMAX * NR * C) * 8;
+  if (c.peer) {
+    for (int r : c.reduces) {
+      const Node& rn = c.g.nodes[r];
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32)
+        throw Error(SFX_ERR_UNSUPPORTED, "cross-rank colbc supports sum reductions (max/min NaN-first rule: col template)");
+    }
+    ks.peer_bytes = (pflag_byte + tiles * PMAX * 4 + 255) / 256 * 256;
+  }
   body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
   body.line("const int cl = lane & " + std::to_string(CL - 1) + ", rl = lane / " + std::to_string(CL) + ";");
   body.line("const int rsub = warp * " + std::to_string(RL) + " + rl;");
@@ -1983,6 +1999,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
   body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
   body.line("const " + it + " co = cok ? c0 / " + fmt_i(I) + " : 0, ci = cok ? c0 % " + fmt_i(I) + " : 0;");
+  if (c.peer) body.line("const unsigned launch_seq = __ldcg(ws + 2);");
   auto inner_ix = [&](int lane) {
     em.lane = lane;
     return V == 1 ? em.uni("ci") : em.lane_plus("ci");
@@ -2111,6 +2128,35 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
       body.line("}");
     }
     body.line("sfx_grid_barrier(ws, " + std::to_string(2 * lv) + "u);");
+    if (c.peer) {
+      // exchange this level's totals across ranks (all reduces of the level)
+      body.line("if (pn > 1) {");
+      body.indent++;
+      body.line("const unsigned step = launch_seq * " + std::to_string(bp.max_level) + "u + " + std::to_string(lv) + "u;");
+      body.line("const long long par = step & 1u;");
+      body.line("if (blockIdx.y == 0) {");
+      body.line("  for (" + it + " cc = threadIdx.x; cc < " + fmt_i(TC) + "; cc += " + std::to_string(B) + ") {");
+      body.line("    const " + it + " col = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cc;");
+      body.line("    if (col >= " + fmt_i(C) + ") break;");
+      for (size_t k = 0; k < red.size(); ++k) {
+        const std::string T = acc_t(red[k]);
+        body.line("    { const " + T + " v = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
+                  fmt_i(tot_word[red[k]]) + ") + col));");
+        body.line("      for (int p = 0; p < pn; ++p) *(" + T + "*)((unsigned long long*)(peers[p] + poff) + ((par * " +
+                  std::to_string(PMAX) + " + prank) * " + std::to_string(NR) + " + " + std::to_string(red_index[red[k]]) +
+                  ") * " + fmt_i(C) + " + col) = v; }");
+      }
+      body.line("  }");
+      body.line("  __syncthreads();");
+      body.line("  if (threadIdx.x < pn) sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " +
+                fmt_i(pflag_byte) + ") + blockIdx.x * " + std::to_string(PMAX) + " + prank, step);");
+      body.line("}");
+      body.line("if (threadIdx.x < pn) sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(pflag_byte) +
+                ") + blockIdx.x * " + std::to_string(PMAX) + " + threadIdx.x, step);");
+      body.line("__syncthreads();");
+      body.indent--;
+      body.line("}");
+    }
     for (size_t k = 0; k < red.size(); ++k) {
       const Node& rn = c.g.nodes[red[k]];
       const std::string T = acc_t(red[k]);
@@ -2119,6 +2165,21 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
         tv[l] = em.fresh("tot");
         body.line(T + " " + tv[l] + " = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
                   fmt_i(tot_word[red[k]]) + ") + (cok ? c0 : 0) + " + std::to_string(l) + "));");
+      }
+      if (c.peer) {  // the ranks' totals, in rank order (identical on every rank)
+        body.line("if (pn > 1) {");
+        body.line("  const long long par = (launch_seq * " + std::to_string(bp.max_level) + "u + " + std::to_string(lv) +
+                  "u) & 1u;");
+        body.line("  const unsigned long long* xs = (const unsigned long long*)(peers[prank] + poff) + (par * " +
+                  std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(red_index[red[k]]) + ") * " +
+                  fmt_i(C) + " + (cok ? c0 : 0);");
+        for (int l = 0; l < V; ++l) {
+          body.line("  " + tv[l] + " = __ldcv((const " + T + "*)(xs + " + std::to_string(l) + "));");
+          body.line("  for (int q = 1; q < pn; ++q) " + tv[l] + " = " + fold_fn(red[k]) + "(" + tv[l] + ", __ldcv((const " +
+                    T + "*)(xs + (long long)q * " + std::to_string(NR) + " * " + fmt_i(C) + " + " + std::to_string(l) +
+                    ")));");
+        }
+        body.line("}");
       }
       if (T == "double")
         for (int l = 0; l < V; ++l) {
@@ -2187,7 +2248,11 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     body.indent--;
     body.line("}");
   }
-  body.line("sfx_grid_exit(ws);");
+  if (c.peer)  // the last CTA out also advances the launch sequence
+    body.line("if (threadIdx.x == 0 && atomicAdd(ws + 1, 1u) == gridDim.x * gridDim.y - 1u) { ws[0] = 0u; ws[1] = 0u; "
+              "ws[2] = launch_seq + 1u; }");
+  else
+    body.line("sfx_grid_exit(ws);");
   ks.code = assemble(sig, body);
   ks.block = B;
   ks.grid_x = tiles;
@@ -2413,12 +2478,21 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
       for (int64_t d : g.nodes[r].reduce_dims)
         if (d == 0) c.peer = true;
     if (c.peer) {
+      // column reductions: the col template; reductions broadcast back
+      // (SyncBatchNorm): colbc, whose per-level totals are combined across ranks
       ColPlan cp;
-      if ((strat != SFX_STRATEGY_AUTO && strat != SFX_STRATEGY_COL) || !analyze_col(c, &cp, &why))
+      ColBcPlan bp;
+      std::string why2;
+      if ((strat == SFX_STRATEGY_AUTO || strat == SFX_STRATEGY_COL) && analyze_col(c, &cp, &why)) {
+        strat = SFX_STRATEGY_COL;
+      } else if ((strat == SFX_STRATEGY_AUTO || strat == SFX_STRATEGY_COLBC) && analyze_colbc(c, &bp, &why2)) {
+        strat = SFX_STRATEGY_COLBC;
+      } else {
         throw Error(SFX_ERR_UNSUPPORTED, "group " + c.name +
-                                             " reduces over the sharded dim 0 but cannot use the column template"
-                                             " (cross-rank combine): " + (why.empty() ? "strategy forced" : why));
-      strat = SFX_STRATEGY_COL;
+                                             " reduces over the sharded dim 0 but cannot use the column templates"
+                                             " (cross-rank combine): " +
+                                             (why.empty() ? "strategy forced" : why + "; " + why2));
+      }
     }
   }
   if (strat == SFX_STRATEGY_AUTO) {

@@ -17,19 +17,28 @@ sys.path.insert(0, ROOT)
 
 from workloads import configs  # noqa: E402
 
-def bn_graph(shape, rdims, with_stats=False):
-    """Batch-norm statistics + normalise over `rdims` (contiguous), gamma/beta on the kept dims."""
+def bn_graph(shape, rdims, with_stats=False, count=None):
+    """Batch-norm statistics + normalise over `rdims` (contiguous), gamma/beta on
+    the kept dims.  `count`: the number of reduced elements the means divide by
+    — a rank's shard of a SyncBatchNorm graph divides by the GLOBAL count (explicit
+    sum + scale instead of the parser's mean lowering, ir.cpp:396-428)."""
     kept = [d for d in range(len(shape)) if d not in rdims]
     cshape = [shape[d] for d in kept]
+
+    def mean(name, src):
+        if count is None:
+            return [{"id": name, "op": "reduce", "operands": [src], "shape": cshape, "reduce_dims": rdims,
+                     "reducer": "mean"}]
+        return [{"id": name + ".sum", "op": "reduce", "operands": [src], "shape": cshape, "reduce_dims": rdims,
+                 "reducer": "sum"},
+                {"id": name, "op": "scale", "operands": [name + ".sum"], "shape": cshape, "scalar": 1.0 / count}]
     ins = [
         {"id": "x", "op": "parameter", "shape": shape},
         {"id": "g", "op": "parameter", "shape": cshape},
-        {"id": "b", "op": "parameter", "shape": cshape},
-        {"id": "mean", "op": "reduce", "operands": ["x"], "shape": cshape, "reduce_dims": rdims, "reducer": "mean"},
+        {"id": "b", "op": "parameter", "shape": cshape}] + mean("mean", "x") + [
         {"id": "mean_b", "op": "broadcast", "operands": ["mean"], "shape": shape, "broadcast_dim_map": kept},
         {"id": "d", "op": "sub", "operands": ["x", "mean_b"], "shape": shape},
-        {"id": "d2", "op": "mul", "operands": ["d", "d"], "shape": shape},
-        {"id": "var", "op": "reduce", "operands": ["d2"], "shape": cshape, "reduce_dims": rdims, "reducer": "mean"},
+        {"id": "d2", "op": "mul", "operands": ["d", "d"], "shape": shape}] + mean("var", "d2") + [
         {"id": "eps", "op": "constant", "shape": cshape, "value": 1e-5},
         {"id": "ve", "op": "add", "operands": ["var", "eps"], "shape": cshape},
         {"id": "rstd", "op": "rsqrt", "operands": ["ve"], "shape": cshape},
@@ -60,6 +69,8 @@ EXTRA = {
     "bn_4096x256": bn_graph([4096, 256], [0]),
     "bn_mid_8x512x64": bn_graph([8, 512, 64], [1]),
     "bn_nhwc_16x16x8x128": bn_graph([16, 16, 8, 128], [0, 1, 2], with_stats=True),
+    # one rank"s shard of a 2-rank SyncBatchNorm over 4096 rows (global count)
+    "bnsync_shard_2048x256": bn_graph([2048, 256], [0], count=4096),
     "bnmax_3000x37": {"instructions": [
         {"id": "x", "op": "parameter", "shape": [3000, 37]},
         {"id": "m", "op": "reduce", "operands": ["x"], "shape": [37], "reduce_dims": [0], "reducer": "max"},

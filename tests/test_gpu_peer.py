@@ -78,6 +78,25 @@ def _worker(rank, ws, port, case, q):
             st.synchronize()
             out.append({o: t.cpu().numpy() for o, t in zip(g.outputs, outs)})
             cg.close()
+        elif case == "bnsync":
+            g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", "bnsync_shard_2048x256.json"))
+            cg = H.CompiledGraph(ctx, g, rep, cross_rank=1)
+            assert [k.info["strategy"] for k in cg.kernels] == ["colbc"]
+            for it in range(3):
+                inputs = _bn_inputs(300 + it, rank)
+                out.append(cg.run_host(inputs))
+            import torch
+            dev = torch.device("cuda", 0)
+            inputs = _bn_inputs(400, rank)
+            ins = [torch.from_numpy(inputs[p]).to(dev) for p in cg.param_ids]
+            outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+            st = torch.cuda.Stream(device=dev)
+            for _ in range(3):
+                cg.run([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], stream=st.cuda_stream,
+                       cuda_graph=True)
+            st.synchronize()
+            out.append({o: t.cpu().numpy() for o, t in zip(g.outputs, outs)})
+            cg.close()
         elif case == "min_nan":
             g, prog, p = _min_program(rank)
             (got,) = H.run_program(prog, g, {"p": p}, ctx=ctx, cross_rank=1)
@@ -88,6 +107,13 @@ def _worker(rank, ws, port, case, q):
     finally:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _bn_inputs(seed, rank, rows=2048, cols=256):
+    """x: this rank's rows of the global batch; gamma / beta: the same on every rank."""
+    return {"x": _shard(seed, 0, rows, cols, rank),
+            "g": T.gen_tensor(seed, 1, cols, "f32", 0.5, 1.5),
+            "b": T.gen_tensor(seed, 2, cols, "f32", -1.0, 1.0)}
 
 
 def _min_rows(rank):
@@ -166,3 +192,24 @@ def test_cross_rank_min_nan_first_rule():
         got = outs[r][0]["c2"]
         assert np.array_equal(np.isnan(got), np.isnan(want)), r
         assert T.values_close(got, want), r
+
+
+def test_cross_rank_sync_batchnorm():
+    """SyncBatchNorm in one launch per rank: batch-norm statistics over the
+    GLOBAL batch (both ranks' rows), the colbc template combining each level's
+    column totals across ranks through peer memory between its grid barriers,
+    then normalising this rank's rows.  Against the fp64 restatement of the
+    unsharded graph; 3 host-path launches with fresh inputs + CUDA-graph replays."""
+    import sys
+    sys.path.insert(0, T.GOLDEN)
+    from make_extra_plans import bn_graph
+    outs = _spawn("bnsync")
+    full = H.graph_from_json(bn_graph([2048 * WS, 256], [0], count=2048 * WS))
+    for i, seed in enumerate([300, 301, 302, 400]):
+        per = [_bn_inputs(seed, r) for r in range(WS)]
+        inputs = {"x": np.concatenate([p["x"] for p in per]), "g": per[0]["g"], "b": per[0]["b"]}
+        ref = T.interpret(full, inputs, mode=1)["y"]
+        for r in range(WS):
+            y = outs[r][i]["y"]
+            want = ref[r * 2048:(r + 1) * 2048]
+            assert T.strict_close(y, want), (seed, r, T.mismatch_report(y, want))
