@@ -200,26 +200,34 @@ def test_innermost_moving_transpose_uses_smem_tiles():
     the map template stages it through a padded 32x33 shared-memory tile."""
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C4t.full.json"))
     src, cubin, note = H.codegen(g, rep.kernels[0].program)
-    assert "smem-tiled" in note and "[32][33]" in src
+    assert "smem-tiled" in note and "[64][65]" in src
     sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
     assert "STS" in sass and "LDS" in sass and "BAR.SYNC" in sass
 
 
 def test_cross_rank_rejects_non_column_batch_reduce():
-    """A reduction over the sharded dim 0 that the column template cannot take
-    fails loudly at compile time instead of silently reducing one shard."""
+    """A reduction over the sharded dim 0 that neither column template can take
+    (reduce dims {0, 2}: not contiguous) fails loudly at compile time instead of
+    silently reducing one shard.  (Column sums, and column statistics broadcast
+    back — SyncBatchNorm — are combined across ranks in-kernel.)"""
     doc = {"instructions": [
-        {"id": "p", "op": "parameter", "shape": [64, 128]},
-        {"id": "s", "op": "reduce", "operands": ["p"], "shape": [128], "reduce_dims": [0], "reducer": "sum"},
-        {"id": "sb", "op": "broadcast", "operands": ["s"], "shape": [64, 128], "broadcast_dim_map": [1]},
-        {"id": "y", "op": "sub", "operands": ["p", "sb"], "shape": [64, 128]},
+        {"id": "p", "op": "parameter", "shape": [8, 16, 4]},
+        {"id": "s", "op": "reduce", "operands": ["p"], "shape": [16], "reduce_dims": [0, 2], "reducer": "sum"},
+        {"id": "y", "op": "scale", "operands": ["s"], "shape": [16], "scalar": 2.0},
     ], "outputs": ["y"]}
     g = H.graph_from_json(doc)
-    prog = H.KernelProgram("y", ["s", "sb", "y"], ["y"], 1, 64, 512,
+    prog = H.KernelProgram("y", ["s", "y"], ["y"], 1, 64, 64,
                            [{"kind": "materialize", "instr": "s", "schedule": [0, 1, "row"], "dest": "shared",
-                             "offset": 0, "bytes": 512}, {"kind": "barrier"},
-                            {"kind": "inline", "instr": "sb"},
+                             "offset": 0, "bytes": 64}, {"kind": "barrier"},
                             {"kind": "materialize", "instr": "y", "schedule": [0, 1, "row"], "dest": "output",
                              "root_index": 0}])
     with pytest.raises(H.ExecError, match="sharded dim 0"):
         H.codegen(g, prog, cross_rank=1)
+    _, _, note = H.codegen(g, prog)  # single rank: the literal tier takes it
+    assert note.startswith("literal")
+
+
+def test_cross_rank_accepts_sync_batchnorm():
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", "bnsync_shard_2048x256.json"))
+    src, _, note = H.codegen(g, rep.kernels[0].program, cross_rank=1)
+    assert note.startswith("colbc") and "peers[p] + poff" in src and "launch_seq" in src
