@@ -212,6 +212,9 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   sfx::check_cu(d.cuModuleLoadData(&k->mod, cb.image.data()), "cuModuleLoadData");
   sfx::check_cu(d.cuModuleGetFunction(&k->fn, k->mod, k->src.entry.c_str()), "cuModuleGetFunction");
   d.cuFuncGetAttribute(&k->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k->fn);
+  if (k->src.cluster > 8)
+    sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1),
+                  "cuFuncSetAttribute(non-portable cluster)");
   if (k->src.smem > 48 * 1024)
     sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->src.smem),
                   "cuFuncSetAttribute(smem)");

@@ -1012,12 +1012,16 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   int CS = 1;
   if (V == 4 && !staged.empty() && o.row_pipeline != 1) {  // row_pipeline=1: plain multi-pass (A/B)
     const int64_t bytes = C * 4 * static_cast<int64_t>(staged.size());
+    // (pipe_stages doubles as the largest cluster size to consider: 16 is the
+    // non-portable maximum)
+    const int cs_max = o.pipe_stages == 16 ? 16 : 8;
+    const int64_t slice_max = o.pipe_stages == 16 ? 32 * 1024 : 64 * 1024;
     int cs = 2;
-    while (cs < 8 && bytes / cs > 64 * 1024) cs *= 2;
+    while (cs < cs_max && bytes / cs > slice_max) cs *= 2;
     // <= 64 KB of slices per CTA keeps 3 CTAs per SM, so one CTA's TMA load
     // overlaps another's passes; measured: 128 KB slices (1 CTA/SM) lose to
     // the plain multi-pass variant (softmax [256,262144]: 232 vs 185 us)
-    if (bytes / cs <= 64 * 1024 && C % (int64_t{cs} * V) == 0) CS = cs;
+    if (bytes / cs <= slice_max && C % (int64_t{cs} * V) == 0) CS = cs;
   }
   if (CS == 1) staged.clear();
   ks.entry = (CS > 1 ? "sfx_rowcl_" : "sfx_rowmp_") + c.name;
@@ -1226,6 +1230,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   ks.code = assemble(sig, body);
   ks.block = B;
   ks.grid_x = R * CS;
+  ks.cluster = CS;
   ks.vector_width = V;
   // residency cap through dynamic shared memory (plain variant, A/B knob)
   if (CS == 1 && o.pipe_ctas_per_sm > 0) ks.smem = 220 * 1024 / o.pipe_ctas_per_sm;
@@ -1941,7 +1946,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   const int RSUB = WARPS * RL;
   const int64_t TC = static_cast<int64_t>(CL) * V;
   const int64_t tiles = (C + TC - 1) / TC;
-  const int ctas_per_sm = 2;
+  const int ctas_per_sm = o.pipe_ctas_per_sm > 0 ? std::min(o.pipe_ctas_per_sm, 8) : 2;
   if (tiles > int64_t{kNumSMs} * ctas_per_sm)
     throw Error(SFX_ERR_UNSUPPORTED, "colbc: " + std::to_string(tiles) + " column tiles exceed one co-resident wave");
   int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / tiles);

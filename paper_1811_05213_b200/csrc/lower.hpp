@@ -41,6 +41,7 @@ struct KernelSource {
   int smem = 0;              // dynamic shared memory bytes
   int64_t workspace_bytes = 0;
   bool cooperative = false;  // grid-wide barriers: launched cooperatively (co-residency checked)
+  int cluster = 1;           // thread-block cluster size (__cluster_dims__); > 8 needs the non-portable opt-in
   // cross-rank column combine (opts.cross_rank): bytes of the symmetric peer
   // arena this kernel needs; the kernel then takes (peers, peer_off, rank,
   // nranks) after ws
