@@ -1046,11 +1046,50 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   const std::string& it = em.idx_t;
   body.line("const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;");
   const int64_t slice_bytes = SL * 4;
-  if (CS > 1) {
+  const int64_t stage_bytes = slice_bytes * static_cast<int64_t>(staged.size());
+  // persistent clusters (row_pipeline=3): NCL clusters loop over the rows, each
+  // CTA double-buffering its slices (the TMA copy of row i + 2*NCL is issued as
+  // soon as row i's stage is free, so loads run under the passes and stores)
+  const bool persist = CS > 1 && o.row_pipeline == 3;
+  const int64_t NCL = persist ? std::min<int64_t>(R, std::max<int64_t>(1, (kNumSMs * std::max<int64_t>(
+                                                                               1, (220 * 1024) / (2 * stage_bytes))) /
+                                                                                  CS))
+                              : 0;
+  auto issue = [&](const std::string& stage, const std::string& r, const std::string& bar) {
+    body.line("  sfx_mbar_expect_tx(" + bar + ", " + fmt_i(stage_bytes) + "u);");
+    for (size_t k = 0; k < staged.size(); ++k)
+      body.line("  sfx_bulk_g2s(sfx_smem + " + stage + " * " + fmt_i(stage_bytes) + " + " +
+                fmt_i(static_cast<int64_t>(k) * slice_bytes) + ", " + em.input_ptr.at(staged[k]) + " + (" + r +
+                ") * " + fmt_i(C) + " + (" + it + ")q * " + fmt_i(SL) + ", " + fmt_i(slice_bytes) + "u, " + bar + ");");
+  };
+  if (CS > 1 && persist) {
+    body.line("const unsigned q = sfx_cluster_rank();");
+    body.line("const " + it + " cid = (" + it + ")blockIdx.x / " + std::to_string(CS) + ";");
+    body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
+    body.line("unsigned long long* sbar = (unsigned long long*)(sfx_smem + " + fmt_i(2 * stage_bytes) + ");");
+    body.line("if (tid == 0) {");
+    body.line("  sfx_mbar_init(sbar, 1);");
+    body.line("  sfx_mbar_init(sbar + 1, 1);");
+    body.line("  sfx_fence_mbar_init();");
+    body.line("  if (cid < " + fmt_i(R) + ") {");
+    issue("0", "cid", "sbar");
+    body.line("  }");
+    body.line("  if (cid + " + fmt_i(NCL) + " < " + fmt_i(R) + ") {");
+    issue("1", "cid + " + fmt_i(NCL), "sbar + 1");
+    body.line("  }");
+    body.line("}");
+    body.line("__syncthreads();");
+    body.line("for (int itr = 0;; ++itr) {");
+    body.line("const " + it + " row = cid + (" + it + ")itr * " + fmt_i(NCL) + ";");
+    body.line("if (row >= " + fmt_i(R) + ") break;");
+    body.line("const int stg = itr & 1;");
+    body.line("sfx_mbar_wait_bounded(sbar + stg, (unsigned)((itr >> 1) & 1));");
+    ks.smem = static_cast<int>(2 * stage_bytes + 16);
+  } else if (CS > 1) {
     body.line("const unsigned q = sfx_cluster_rank();");
     body.line("const " + it + " row = (" + it + ")blockIdx.x / " + std::to_string(CS) + ";");
     body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
-    const int64_t bar_off = slice_bytes * static_cast<int64_t>(staged.size());
+    const int64_t bar_off = stage_bytes;
     body.line("unsigned long long* sbar = (unsigned long long*)(sfx_smem + " + fmt_i(bar_off) + ");");
     body.line("if (tid == 0) {");
     body.line("  sfx_mbar_init(sbar, 1);");
@@ -1074,8 +1113,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     std::string rb = em.ivar(Emitter::iadd(em.ivar(Emitter::imul("row", C)), em.ivar(Emitter::imul("q", SL))));
     for (size_t k = 0; k < staged.size(); ++k) {
       std::string p = em.fresh("sl");
-      body.line("const float* " + p + " = (const float*)(sfx_smem + " + fmt_i(static_cast<int64_t>(k) * slice_bytes) +
-                ");");
+      body.line("const float* " + p + " = (const float*)(sfx_smem + " + (persist ? "stg * " + fmt_i(stage_bytes) + " + " : "") +
+                fmt_i(static_cast<int64_t>(k) * slice_bytes) + ");");
       staged_map[staged[k]] = {p, rb};
     }
     em.staged = staged_map;
@@ -1226,10 +1265,18 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.line("}");
   }
   em.staged.clear();
+  if (persist) {
+    // this stage is free once every thread is past the final pass
+    body.line("__syncthreads();");
+    body.line("if (tid == 0 && row + " + fmt_i(2 * NCL) + " < " + fmt_i(R) + ") {");
+    issue("stg", "row + " + fmt_i(2 * NCL), "sbar + stg");
+    body.line("}");
+    body.line("}");  // row loop
+  }
   if (CS > 1) body.line("sfx_cluster_sync();  // no CTA leaves while a peer may still read its partials");
   ks.code = assemble(sig, body);
   ks.block = B;
-  ks.grid_x = R * CS;
+  ks.grid_x = (persist ? NCL : R) * CS;
   ks.cluster = CS;
   ks.vector_width = V;
   // residency cap through dynamic shared memory (plain variant, A/B knob)
@@ -1238,7 +1285,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " cluster of " + std::to_string(CS) +
               " CTAs x " + std::to_string(B) + " threads per row, " + std::to_string(staged.size()) +
               " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), DSMEM combine, levels=" +
-              std::to_string(rp.max_level);
+              std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "");
   else
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
               " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +

@@ -221,6 +221,18 @@ __device__ __forceinline__ int sfx_dsmem_ld(const int* p, unsigned rank) {
   return v;
 }
 
+// mbarrier phase wait that traps after 10 s instead of hanging the GPU
+__device__ __forceinline__ void sfx_mbar_wait_bounded(unsigned long long* bar, unsigned parity) {
+  const unsigned long long t0 = sfx_globaltimer();
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done) : "r"(sfx_smem_u32(bar)), "r"(parity) : "memory");
+    if (!done && sfx_globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
 // Reused 128-bit loads (broadcast vectors): default caching.
 __device__ __forceinline__ sfx_f4 sfx_ld4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
 __device__ __forceinline__ sfx_i4 sfx_ld4(const int* p) { return *reinterpret_cast<const sfx_i4*>(p); }

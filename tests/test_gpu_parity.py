@@ -32,8 +32,8 @@ def ctx():
     c.close()
 
 
-def _run(ctx, g, rep, inputs, strategy):
-    cg = H.CompiledGraph(ctx, g, rep, strategy)
+def _run(ctx, g, rep, inputs, strategy, **kw):
+    cg = H.CompiledGraph(ctx, g, rep, strategy, **kw)
     try:
         before = ctx.launch_count()
         outs = cg.run_host(inputs)
@@ -348,6 +348,9 @@ def test_long_and_odd_rows(ctx, name):
     else:
         assert strategies == [("col" if name.startswith(("mid", "full")) else "row")] and launched == 1
     assert not _check(g, outs, inputs, strict=True)
+    if name in ("softmax_r4_c131072", "ln_r6_c98304"):  # cluster rows: persistent double-buffered variant too
+        outs, launched, strategies = _run(ctx, g, rep, inputs, "auto", row_pipeline=3)
+        assert strategies == ["row"] and not _check(g, outs, inputs, strict=True)
     outs, launched, strategies = _run(ctx, g, rep, inputs, "literal")
     assert set(strategies) == {"literal"} and launched == len(rep.kernels)
     assert not _check(g, outs, inputs, literal=True)
