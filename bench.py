@@ -245,6 +245,7 @@ def run_ours(args):
             dist.init_process_group(args.dist_backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = dev if args.dist_backend == "nccl" else "cpu"  # where cross-rank reductions of scalars live
     ctx = H.Context(local)
     g, rep, bundle = H.load_bundle(plan_path(args.config))
     # the one batch-crossing exchange on this path is a column reduction over
@@ -333,9 +334,19 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     # keep the GPU under the same load until the sampler is producing samples,
     # so the timed region is bracketed by clock samples taken under load
+    # Ranks run the same number of load rounds: a step that exchanges data
+    # across ranks (the cross-rank column combine) must be issued equally often
+    # on every rank, so the continue decision is agreed each round (max).
     t_load = time.perf_counter()
     n_load = 0
-    while clk.count_after(t_load + 0.15) < 2 and time.perf_counter() - t_load < 5.0:
+    while True:
+        more = clk.count_after(t_load + 0.15) < 2 and time.perf_counter() - t_load < 5.0
+        if ws > 1:
+            flag = torch.tensor([1.0 if more else 0.0], device=red_dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            more = flag.item() > 0
+        if not more:
+            break
         for _ in range(16):
             step(n_load)
             n_load += 1
@@ -356,7 +367,14 @@ def run_ours(args):
     t_hi = time.perf_counter()
     launches = ctx.launch_count() - launches0
     t_post = time.perf_counter()
-    while clk.count_after(t_post) < 2 and time.perf_counter() - t_post < 3.0:
+    while True:  # same agreed-rounds rule as the load phase before the timed region
+        more = clk.count_after(t_post) < 2 and time.perf_counter() - t_post < 3.0
+        if ws > 1:
+            flag = torch.tensor([1.0 if more else 0.0], device=red_dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            more = flag.item() > 0
+        if not more:
+            break
         for _ in range(16):
             step(n_load)
             n_load += 1
@@ -368,7 +386,6 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    red_dev = dev if args.dist_backend == "nccl" else "cpu"
     ms_t = torch.tensor([ms], device=red_dev)
     if ws > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

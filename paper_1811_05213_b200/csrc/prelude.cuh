@@ -149,12 +149,13 @@ __device__ __forceinline__ void sfx_gate_wait(const unsigned* gate, unsigned nee
   }
 }
 // Wait until a peer has published sequence number `seq` (wrap-safe).  A rank
-// that never arrives (crashed process, mismatched graphs) traps after 20 s
-// instead of hanging the GPU.
+// that never arrives (crashed process, mismatched graphs) traps after 300 s
+// instead of hanging the GPU; ranks legitimately drift apart by seconds (a
+// first-use NVRTC compile on one rank, time-sliced ranks sharing a GPU).
 __device__ __forceinline__ void sfx_peer_wait(const unsigned* flag, unsigned seq) {
   const unsigned long long t0 = sfx_globaltimer();
   while ((int)(sfx_ld_acquire_sys(flag) - seq) < 0) {
-    if (sfx_globaltimer() - t0 > 20000000000ull) __trap();
+    if (sfx_globaltimer() - t0 > 300000000000ull) __trap();
     __nanosleep(64);
   }
 }
