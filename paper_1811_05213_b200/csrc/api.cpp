@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no cost unless a profiler attaches
+
 #include "dyn.hpp"
 #include "ir.hpp"
 #include "jit.hpp"
@@ -357,7 +359,11 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
   cfg.hStream = s;
   cfg.attrs = attr;
   cfg.numAttrs = n_attr;
-  sfx::check_cu(sfx::driver().cuLaunchKernelEx(&cfg, k->fn, args.data(), nullptr), "cuLaunchKernelEx");
+  // one NVTX range per group launch, named by its kernel (ncu --nvtx / nsys timelines)
+  nvtxRangePushA(k->src.entry.c_str());
+  CUresult lr = sfx::driver().cuLaunchKernelEx(&cfg, k->fn, args.data(), nullptr);
+  nvtxRangePop();
+  sfx::check_cu(lr, "cuLaunchKernelEx");
   k->ctx->launches.fetch_add(1);
 }
 
