@@ -2,6 +2,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <mutex>
+#include <fstream>
 #include <cstdlib>
 #include <functional>
 #include <map>
@@ -9,6 +12,8 @@
 #include <sstream>
 
 #include "emit.hpp"
+#include "jit.hpp"
+#include "dyn.hpp"
 
 namespace sfx {
 
@@ -2516,7 +2521,78 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   return "literal";
 }
 
+// ---- template parameter cache -------------------------------------------------
+//
+// Persisted, PerfLibrary-style text (reference tuning.cpp:41-125 stores measured
+// schedule costs the same way): one line per group signature
+//   signature|rows_per_cta|threads_per_row|items_per_thread|pipe_ctas_per_sm|tuned_us|default_us|source
+// where signature = <entry>-<fnv64 of the kernel the default options generate>.
+// tools/autotune.py measures candidate template parameters per group on the
+// B200 and writes the winners; lowering with default options looks the group up
+// and re-lowers with the recorded parameters.  SFX_TEMPLATE_PARAMS=<file>
+// overrides the location, SFX_TEMPLATE_PARAMS=0 disables the cache.
+namespace {
+struct TunedParams {
+  int rows_per_cta = 0, threads_per_row = 0, items_per_thread = 0, pipe_ctas_per_sm = 0;
+  std::string note;
+};
+const std::map<std::string, TunedParams>& template_params() {
+  static std::map<std::string, TunedParams> m;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = std::getenv("SFX_TEMPLATE_PARAMS");
+    if (e && e[0] == '0' && e[1] == 0) return;
+    std::string path = e ? e : library_dir() + "/template_params.txt";
+    std::ifstream in(path);
+    std::string line;
+    while (std::getline(in, line)) {
+      if (line.empty() || line[0] == '#') continue;
+      std::vector<std::string> f;
+      std::stringstream ss(line);
+      std::string x;
+      while (std::getline(ss, x, '|')) f.push_back(x);
+      if (f.size() < 7) continue;
+      TunedParams t;
+      t.rows_per_cta = std::atoi(f[1].c_str());
+      t.threads_per_row = std::atoi(f[2].c_str());
+      t.items_per_thread = std::atoi(f[3].c_str());
+      t.pipe_ctas_per_sm = std::atoi(f[4].c_str());
+      t.note = "tuned " + f[6] + " -> " + f[5] + " us";
+      m[f[0]] = t;
+    }
+  });
+  return m;
+}
+bool default_knobs(const sfx_compile_opts& o) {
+  return o.rows_per_cta == 0 && o.threads_per_row == 0 && o.items_per_thread == 0 && o.pipe_ctas_per_sm == 0 &&
+         o.row_pipeline == 0 && o.pipe_warps == 0 && o.pipe_stages == 0;
+}
+}  // namespace
+
+KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o);
+
 KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
+  KernelSource ks = lower_program_raw(g, pi, o);
+  char hex[32];
+  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(ks.code)));
+  const std::string sig = ks.entry + "-" + hex;
+  if (default_knobs(o)) {
+    auto it = template_params().find(sig);
+    if (it != template_params().end()) {
+      sfx_compile_opts t = o;
+      t.rows_per_cta = it->second.rows_per_cta;
+      t.threads_per_row = it->second.threads_per_row;
+      t.items_per_thread = it->second.items_per_thread;
+      t.pipe_ctas_per_sm = it->second.pipe_ctas_per_sm;
+      ks = lower_program_raw(g, pi, t);
+      ks.note += " [template_params: " + it->second.note + "]";
+    }
+  }
+  ks.note += " sig=" + sig;
+  return ks;
+}
+
+KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o) {
   if (pi < 0 || pi >= static_cast<int>(g.programs.size())) throw Error(SFX_ERR_INVALID, "program index out of range");
   const Program& p = g.programs[pi];
   if (p.barrier && dot_alone(g, p)) return lower_dot(g, p);  // no other lowering for LibraryCall

@@ -4,6 +4,7 @@ generated kernels that the GPU suite relies on."""
 
 import os
 import subprocess
+import sys
 
 import pytest
 
@@ -83,3 +84,20 @@ def test_degenerate_reduce_is_a_reshape():
                              "root_index": 0}])
     src, _, note = H.codegen(g, prog)
     assert note.startswith("map"), note
+
+
+def test_template_parameter_cache():
+    """The committed template parameter cache (tools/autotune.py output) is keyed
+    by the default kernel's signature: the full-size LayerNorm group picks up its
+    tuned threads-per-row, other shapes keep the defaults, and
+    SFX_TEMPLATE_PARAMS=0 turns the cache off."""
+    src, _, note = _note(os.path.join(T.PLANS, "C1.full.json"))
+    assert "[template_params:" in note and "threads/row=128" in note, note
+    _, _, small = _note(os.path.join(T.PLANS, "C1.small.json"))
+    assert "[template_params:" not in small
+    code = ("import sys; sys.path.insert(0, %r); import paper_1811_05213_b200 as P; "
+            "g, rep, _ = P.load_bundle(%r); print(P.codegen(g, rep.kernels[0].program)[2])"
+            % (T.ROOT, os.path.join(T.PLANS, "C1.full.json")))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         env=dict(os.environ, SFX_TEMPLATE_PARAMS="0")).stdout
+    assert "threads/row=32" in out and "[template_params:" not in out, out
