@@ -86,18 +86,21 @@ def test_degenerate_reduce_is_a_reshape():
     assert note.startswith("map"), note
 
 
-def test_template_parameter_cache():
-    """The committed template parameter cache (tools/autotune.py output) is keyed
-    by the default kernel's signature: the full-size LayerNorm group picks up its
-    tuned threads-per-row, other shapes keep the defaults, and
-    SFX_TEMPLATE_PARAMS=0 turns the cache off."""
-    src, _, note = _note(os.path.join(T.PLANS, "C1.full.json"))
-    assert "[template_params:" in note and "threads/row=128" in note, note
-    _, _, small = _note(os.path.join(T.PLANS, "C1.small.json"))
-    assert "[template_params:" not in small
+def test_template_parameter_cache(tmp_path):
+    """The template parameter cache (tools/autotune.py output, PerfLibrary-style
+    text) is keyed by the default kernel's signature: a listed group is re-lowered
+    with its recorded parameters, other shapes keep the defaults.  The committed
+    cache is empty after the round-1 sweep (no candidate beat the defaults in the
+    benchmark's mode), so the entry here is written for the test."""
+    _, _, note = _note(os.path.join(T.PLANS, "C1.full.json"))
+    sig = note.rsplit("sig=", 1)[1].strip()
+    cache = tmp_path / "template_params.txt"
+    cache.write_text("# test\n%s|0|128|0|0|12.77|13.30|C1/y\n" % sig)
     code = ("import sys; sys.path.insert(0, %r); import paper_1811_05213_b200 as P; "
+            "g, rep, _ = P.load_bundle(%r); print(P.codegen(g, rep.kernels[0].program)[2]); "
             "g, rep, _ = P.load_bundle(%r); print(P.codegen(g, rep.kernels[0].program)[2])"
-            % (T.ROOT, os.path.join(T.PLANS, "C1.full.json")))
+            % (T.ROOT, os.path.join(T.PLANS, "C1.full.json"), os.path.join(T.PLANS, "C1.small.json")))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                         env=dict(os.environ, SFX_TEMPLATE_PARAMS="0")).stdout
-    assert "threads/row=32" in out and "[template_params:" not in out, out
+                         env=dict(os.environ, SFX_TEMPLATE_PARAMS=str(cache))).stdout.splitlines()
+    assert "threads/row=128" in out[0] and "[template_params: tuned 13.30 -> 12.77 us]" in out[0], out
+    assert "[template_params:" not in out[1], out
