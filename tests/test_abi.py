@@ -231,3 +231,29 @@ def test_cross_rank_accepts_sync_batchnorm():
     g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", "bnsync_shard_2048x256.json"))
     src, _, note = H.codegen(g, rep.kernels[0].program, cross_rank=1)
     assert note.startswith("colbc") and "peers[p] + poff" in src and "launch_seq" in src
+
+
+def test_ctypes_mirror_matches_c_struct_layout(tmp_path):
+    """host.py's ctypes structures must match include/sfx.h field by field
+    (sizes and offsets as the C compiler lays them out)."""
+    import ctypes as C
+    structs = {
+        "sfx_instr": H.SfxInstr, "sfx_stmt": H.SfxStmt, "sfx_program": H.SfxProgram,
+        "sfx_graph_desc": H.SfxGraphDesc, "sfx_compile_opts": H.SfxCompileOpts, "sfx_kernel_info": H.SfxKernelInfo,
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sfx.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(T.ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                          check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[f"{cname} size"]) == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
