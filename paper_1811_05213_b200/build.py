@@ -17,7 +17,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsfx.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-SOURCES = ["ir.cpp", "emit.cpp", "lower.cpp", "dot.cpp", "prelude.cpp", "dyn.cpp", "jit.cpp", "api.cpp"]
+SOURCES = ["ir.cpp", "emit.cpp", "lower.cpp", "lower_analyze.cpp", "lower_map.cpp", "lower_row.cpp", "lower_col.cpp",
+           "lower_literal.cpp", "dot.cpp", "prelude.cpp", "dyn.cpp", "jit.cpp", "api.cpp"]
 
 
 def _gen_prelude():

@@ -1,0 +1,747 @@
+// Column-reduction templates: col (last-CTA combine, cross-rank) and colbc (grid barriers).
+#include "lower_impl.hpp"
+
+namespace sfx {
+namespace lw {
+
+// ---- COL ------------------------------------------------------------------------
+
+// Components of a node of `dims` at position (o, r, i) of an [O | R | I]
+// iteration space (o outer, r reduced, i inner), through a clean prefix split
+// of the dims when there is one, else through the linear index (o*R + r)*I + i.
+std::vector<Ix> orc_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t O, int64_t R, int64_t I,
+                          const Ix& o, const Ix& r, const Ix& i) {
+  int k0 = prefix_split(dims, O);
+  int k1 = k0 < 0 ? -1 : prefix_split(dims, O * R);
+  if (k0 >= 0 && k1 >= k0 && prod(dims, k1, dims.size()) == I && prod(dims, k0, k1) == R) {
+    std::vector<int64_t> d0(dims.begin(), dims.begin() + k0), d1(dims.begin() + k0, dims.begin() + k1),
+        d2(dims.begin() + k1, dims.end());
+    std::vector<Ix> a = em.from_linear(o, d0), b = em.from_linear(r, d1), c = em.from_linear(i, d2);
+    a.insert(a.end(), b.begin(), b.end());
+    a.insert(a.end(), c.begin(), c.end());
+    return a;
+  }
+  std::string ob = em.ivar(Emitter::imul(em.ivar(Emitter::iadd(Emitter::imul(o.e, R), r.e)), I));
+  Ix L;
+  if (i.kind == IX_PLUS) {
+    L = em.lane_plus(em.ivar(Emitter::iadd(ob, i.base)));
+  } else {
+    L = em.uni(em.ivar(Emitter::iadd(ob, i.e)));
+    L.kind = i.kind;
+  }
+  return em.from_linear(L, dims);
+}
+
+// Column template generalised to [outer | reduced | inner]: the reduce
+// operand's reduced dims are contiguous; "columns" are the O x I kept elements
+// (C3: O = 1).  A warp covers CL column vectors x RL rows (RL > 1 when there are
+// fewer than 32 column vectors, e.g. full reductions), 8 warps stride the rows
+// of a stripe, stripes combine in a single launch (last-CTA ticket).
+KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "col";
+  ks.entry = "sfx_col_" + c.name;
+  fill_common(c, ks);
+  const int64_t O = cp.O, R = cp.R, I = cp.I, C = cp.O * cp.I;
+  const int V = (I % 4 == 0) ? 4 : 1;
+  const int64_t cvec = (C + V - 1) / V;
+  int CL = 1;
+  while (CL < 32 && CL < cvec) CL *= 2;
+  const int RL = 32 / CL;
+  const int WARPS = 8, B = WARPS * 32;
+  const int RSUB = WARPS * RL;  // row sub-streams per CTA
+  const int64_t TC = static_cast<int64_t>(CL) * V;
+  const int64_t tiles = (C + TC - 1) / TC;
+  // row stripes: 2 CTAs per SM in exactly one wave, each thread keeping 16
+  // rows x (streamed inputs) 128-bit loads in flight under a 128-register cap
+  // (__launch_bounds__(256, 2)).  Measured on C3 (tools/gpu_ab_col.sh): 4 CTAs/SM
+  // x 4 rows 94.5 us, 4 x 8 rows 88.5 us, 2 x 16 rows 84.3 us (0.99 of the
+  // measured copy peak; a torch read-only sum of the same bytes takes 94.6 us).
+  // The col template reuses rows_per_cta as a stripe-count override,
+  // items_per_thread as rows per iteration and pipe_ctas_per_sm as the
+  // residency target.
+  const int ctas_per_sm = o.pipe_ctas_per_sm > 0 ? o.pipe_ctas_per_sm : 2;
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / tiles);
+  S = std::min<int64_t>(S, std::max<int64_t>(1, R / (8 * RSUB)));
+  S = std::min<int64_t>(S, 65535);
+  const int64_t RS = (R + S - 1) / S;
+  const int NR = static_cast<int>(c.reduces.size());
+
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  // workspace: tickets[tiles] (256-B padded), then partials[NR][S][C]
+  const int64_t ticket_words = (tiles + 63) / 64 * 64;
+  // float sums accumulate in double end to end (per-thread, CTA and stripe
+  // combines): a column of 65,536 fp32 terms with cancellation is otherwise
+  // off by ~eps*sum|x| (SURVEY §7 hard part 1); max/min/i32 are exact anyway.
+  auto acc_t = [&](int k) -> std::string {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
+  };
+  auto fold_fn = [&](int k) -> const char* {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum" : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax"
+                                                                                          : "sfx_fold_pmin";
+  };
+  std::vector<int64_t> part_word(NR);
+  int64_t words = ticket_words;
+  for (int k = 0; k < NR; ++k) {
+    part_word[k] = words;
+    words += S * C * (acc_t(k) == "double" ? 2 : 1);
+    words = (words + 63) / 64 * 64;
+  }
+  const int64_t seq_word = words;
+  if (c.peer) {
+    words += (tiles + 63) / 64 * 64;
+    ks.peer_bytes = ((2LL * SFX_PEER_MAX_RANKS * NR * C + 2LL * NR * C) * 8 + tiles * SFX_PEER_MAX_RANKS * 4 + 255) /
+                    256 * 256;
+  }
+  ks.workspace_bytes = words * 4;
+
+  body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const int cl = lane & " + std::to_string(CL - 1) + ", rl = lane / " + std::to_string(CL) + ";");
+  body.line("const int rsub = warp * " + std::to_string(RL) + " + rl;");
+  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cl * " + std::to_string(V) + ";");
+  body.line("const bool cok = c0 < " + fmt_i(C) + ";");
+  body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
+  // the column vector's outer / inner coordinates (a vector never crosses an
+  // outer index: I % V == 0)
+  body.line("const " + it + " co = c0 / " + fmt_i(I) + ", ci = c0 % " + fmt_i(I) + ";");
+  std::vector<std::vector<std::string>> acc(NR, std::vector<std::string>(V));
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    std::string init;
+    if (rn.reducer == SFX_REDUCE_SUM) init = rn.dtype == SFX_F32 ? "0.0" : "0";
+    else if (rn.dtype == SFX_F32) init = "sfx_bits_f(0x7fc00000)";  // NaN = identity of fmaxf/fminf
+    else init = rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+    for (int l = 0; l < V; ++l) {
+      acc[k][l] = em.fresh("acc");
+      body.line(acc_t(k) + " " + acc[k][l] + " = " + init + ";");
+    }
+  }
+  std::vector<int> full_roots, col_roots;
+  for (int r : c.p.roots) (c.dep.at(r) || c.g.nodes[r].numel() != R * C ? col_roots : full_roots).push_back(r);
+  auto inner_ix = [&](int lane) {
+    em.lane = lane;
+    return V == 1 ? em.uni("ci") : em.lane_plus("ci");
+  };
+
+  // one row of this thread's column vector: elementwise roots stored, reduce
+  // operands folded into the per-lane accumulators
+  auto emit_row = [&](const std::string& r) {
+    Ix rix = em.uni(r), oix = em.uni("co");
+    std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+    std::vector<std::vector<std::string>> faddr(full_roots.size(), std::vector<std::string>(V));
+    std::vector<bool> fvec(full_roots.size(), V == 4);
+    for (int lane = 0; lane < V; ++lane) {
+      Ix iix = inner_ix(lane);
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::vector<Ix> comps = orc_comps(em, c.g.nodes[full_roots[k]].dims, O, R, I, oix, rix, iix);
+        fv[k][lane] = em.value(full_roots[k], comps);
+        Ix L = em.linearize(comps, c.g.nodes[full_roots[k]].dims);
+        faddr[k][lane] = lane == 0 && L.kind == IX_PLUS ? L.base : L.e;
+        if (lane == 0 && L.kind != IX_PLUS) fvec[k] = false;
+      }
+      for (int k = 0; k < NR; ++k) {
+        const Node& rn = c.g.nodes[c.reduces[k]];
+        const Node& in = c.g.nodes[rn.operands[0]];
+        std::string v = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, oix, rix, iix));
+        body.line(acc[k][lane] + " = " + fold_fn(k) + "(" + acc[k][lane] + ", " + v + ");");
+      }
+    }
+    for (size_t k = 0; k < full_roots.size(); ++k) {
+      std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+      if (fvec[k])
+        body.line("sfx_st4(" + out + " + " + faddr[k][0] + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] +
+                  ", " + fv[k][3] + ");");
+      else
+        for (int l = 0; l < V; ++l) body.line(out + "[" + faddr[k][l] + "] = " + fv[k][l] + ";");
+    }
+  };
+  // UR rows per iteration, unguarded, so all their 128-bit loads are in flight
+  // together; then the remainder one row at a time
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 32) : 16;
+  body.line("if (cok) {");
+  body.indent++;
+  body.line(it + " r = r_begin + rsub;");
+  body.line("for (; r + " + std::to_string((UR - 1) * RSUB) + " < r_end; r += " + std::to_string(UR * RSUB) + ") {");
+  body.indent++;
+  em.push();
+  for (int u = 0; u < UR; ++u) {
+    std::string ru = "r" + std::to_string(u);
+    body.line("const " + it + " " + ru + " = r + " + std::to_string(u * RSUB) + ";");
+    emit_row(ru);
+  }
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.line("for (; r < r_end; r += " + std::to_string(RSUB) + ") {");
+  body.indent++;
+  em.push();
+  emit_row("r");
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.indent--;
+  body.line("}");
+
+  // CTA combine through shared memory (deterministic row-substream order)
+  for (int k = 0; k < NR; ++k) {
+    const std::string T = acc_t(k);
+    body.line("__shared__ " + T + " sp" + std::to_string(k) + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
+    for (int l = 0; l < V; ++l)
+      body.line("sp" + std::to_string(k) + "[rsub][cl * " + std::to_string(V) + " + " + std::to_string(l) +
+                "] = " + acc[k][l] + ";");
+  }
+  body.line("__syncthreads();");
+  body.line("unsigned* tickets = ws;");
+  body.line("const bool lead = warp == 0 && rl == 0 && cok;");
+  body.line("if (lead) {");
+  body.indent++;
+  for (int k = 0; k < NR; ++k) {
+    const std::string T = acc_t(k);
+    std::string part = "part" + std::to_string(k);
+    body.line(T + "* " + part + " = (" + T + "*)(ws + " + fmt_i(part_word[k]) + ");");
+    for (int l = 0; l < V; ++l) {
+      std::string sidx = "cl * " + std::to_string(V) + " + " + std::to_string(l);
+      std::string t = em.fresh("t");
+      body.line(T + " " + t + " = sp" + std::to_string(k) + "[0][" + sidx + "];");
+      body.line("for (int w = 1; w < " + std::to_string(RSUB) + "; ++w) " + t + " = " + fold_fn(k) + "(" + t +
+                ", sp" + std::to_string(k) + "[w][" + sidx + "]);");
+      body.line(part + "[(" + it + ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + "] = " + t + ";");
+    }
+  }
+  body.indent--;
+  body.line("}");
+  body.line("__threadfence();");
+  body.line("__syncthreads();");
+  body.line("__shared__ unsigned s_last;");
+  body.line("if (threadIdx.x == 0) s_last = (atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1u);");
+  body.line("__syncthreads();");
+  body.line("if (!s_last) return;");
+  body.line("__threadfence();");
+  // finisher: ordered combine over stripes (then, with cross_rank, over ranks
+  // in rank order through peer memory), then the column roots
+  const std::string Cs = fmt_i(C);
+  auto stripe_total = [&](int k) {
+    const std::string T = acc_t(k);
+    std::string part = "fp" + std::to_string(k);
+    body.line("const " + T + "* " + part + " = (const " + T + "*)(ws + " + fmt_i(part_word[k]) + ") + c0;");
+    std::vector<std::string> tv(V);
+    for (int l = 0; l < V; ++l) {
+      tv[l] = em.fresh("tot");
+      body.line(T + " " + tv[l] + " = __ldcg(" + part + " + " + std::to_string(l) + ");");
+    }
+    body.line("for (" + it + " s = 1; s < " + fmt_i(S) + "; ++s) {");
+    for (int l = 0; l < V; ++l)
+      body.line("  " + tv[l] + " = " + fold_fn(k) + "(" + tv[l] + ", __ldcg(" + part + " + s * " + Cs + " + " +
+                std::to_string(l) + "));");
+    body.line("}");
+    return tv;
+  };
+  // the sequential fold's first element (row 0 of the column; with
+  // cross_rank, row 0 of rank 0's shard)
+  auto first_elem = [&](int k, int l) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const Node& in = c.g.nodes[rn.operands[0]];
+    Ix iix = inner_ix(l);
+    return em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
+  };
+  auto needs_first = [&](int k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    return rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32;
+  };
+  std::map<int, std::vector<std::string>> total;
+  // peer arena layout (8-byte slots): data[2][PMAX][NR][C], first[2][NR][C],
+  // then flags[tiles][PMAX] (u32); local ws keeps one sequence word per tile
+  const int PMAX = SFX_PEER_MAX_RANKS;
+  const int64_t first_slot = 2LL * PMAX * NR * C;
+  const int64_t flag_byte = (first_slot + 2LL * NR * C) * 8;
+  // per reduce and lane: the column total in the accumulation type, declared
+  // at CTA scope so the cross-rank protocol can sit between its two halves
+  std::vector<std::vector<std::string>> ptot(NR, std::vector<std::string>(V));
+  if (c.peer) {
+    for (int k = 0; k < NR; ++k)
+      for (int l = 0; l < V; ++l) {
+        ptot[k][l] = em.fresh("ptot");
+        body.line(acc_t(k) + " " + ptot[k][l] + " = 0;");
+      }
+    body.line("__shared__ unsigned s_seq;");
+    body.line("if (threadIdx.x == 0) { const unsigned q = ws[" + fmt_i(seq_word) +
+              " + blockIdx.x] + 1u; ws[" + fmt_i(seq_word) + " + blockIdx.x] = q; s_seq = q; }");
+    body.line("__syncthreads();");
+    body.line("const unsigned seq = s_seq;");
+    body.line("const long long par = seq & 1u;");
+    body.line("if (lead) {");
+    body.indent++;
+    em.push();
+    for (int k = 0; k < NR; ++k) {
+      const std::string T = acc_t(k);
+      std::vector<std::string> tv = stripe_total(k);
+      for (int l = 0; l < V; ++l) body.line(ptot[k][l] + " = " + tv[l] + ";");
+      // a single rank has nothing to exchange: the protocol only runs for pn > 1
+      body.line("for (int p = 0; p < pn && pn > 1; ++p) {");
+      body.line("  unsigned long long* slot = (unsigned long long*)(peers[p] + poff) + ((par * " +
+                std::to_string(PMAX) + " + prank) * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs +
+                " + c0;");
+      for (int l = 0; l < V; ++l) body.line("  *(" + T + "*)(slot + " + std::to_string(l) + ") = " + tv[l] + ";");
+      if (needs_first(k)) {
+        body.line("  if (prank == 0) {");
+        body.line("    float* f = (float*)((unsigned long long*)(peers[p] + poff) + " + fmt_i(first_slot) +
+                  " + (par * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs + " + c0);");
+        for (int l = 0; l < V; ++l) body.line("    f[" + std::to_string(2 * l) + "] = " + first_elem(k, l) + ";");
+        body.line("  }");
+      }
+      body.line("}");
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    // the lead lanes' stores reach thread p through the CTA barrier; its
+    // release store at system scope is cumulative over them (no separate
+    // __threadfence_system: it cost 2 us on the critical path)
+    body.line("if (pn > 1) {");
+    body.line("  __syncthreads();");
+    body.line("  if (threadIdx.x < pn) {");
+    body.line("    sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " + fmt_i(flag_byte) +
+              ") + blockIdx.x * " + std::to_string(PMAX) + " + prank, seq);");
+    body.line("    sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(flag_byte) + ") + blockIdx.x * " +
+              std::to_string(PMAX) + " + threadIdx.x, seq);");
+    body.line("  }");
+    body.line("  __syncthreads();");
+    body.line("}");
+  }
+  body.line("if (lead) {");
+  body.indent++;
+  em.push();
+  for (int k = 0; k < NR; ++k) {
+    const Node& rn = c.g.nodes[c.reduces[k]];
+    const std::string T = acc_t(k);
+    std::vector<std::string> tv;
+    std::string first_peer;  // pn > 1: rank 0's published first element (per lane, below)
+    if (c.peer) {
+      // every rank folds the same slots in rank order: bit-identical results
+      body.line("if (pn > 1) {");
+      body.line("  const unsigned long long* xs = (const unsigned long long*)(peers[prank] + poff) + (par * " +
+                std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs + " + c0;");
+      for (int l = 0; l < V; ++l)
+        body.line("  " + ptot[k][l] + " = __ldcv((const " + T + "*)(xs + " + std::to_string(l) + "));");
+      body.line("  for (int q = 1; q < pn; ++q) {");
+      for (int l = 0; l < V; ++l)
+        body.line("    " + ptot[k][l] + " = " + fold_fn(k) + "(" + ptot[k][l] + ", __ldcv((const " + T +
+                  "*)(xs + (long long)q * " + std::to_string(NR) + " * " + Cs + " + " + std::to_string(l) + ")));");
+      body.line("  }");
+      body.line("}");
+      tv = ptot[k];
+    } else {
+      tv = stripe_total(k);
+    }
+    if (T == "double")
+      for (int l = 0; l < V; ++l) {
+        std::string fv32 = em.fresh("tot");
+        body.line("const float " + fv32 + " = (float)" + tv[l] + ";");
+        tv[l] = fv32;
+      }
+    if (needs_first(k)) {
+      // sequential std::max/min fold semantics: a NaN first element wins
+      for (int l = 0; l < V; ++l) {
+        std::string f0 = first_elem(k, l);
+        if (c.peer) {
+          std::string fp = em.fresh("f0");
+          body.line("const float " + fp + " = pn > 1 ? __ldcv((const float*)((const unsigned long long*)(peers[prank] + poff) + " +
+                    fmt_i(first_slot) + " + (par * " + std::to_string(NR) + " + " + std::to_string(k) + ") * " + Cs +
+                    " + c0 + " + std::to_string(l) + ")) : " + f0 + ";");
+          f0 = fp;
+        }
+        body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
+      }
+    }
+    (void)rn;
+    total[c.reduces[k]] = tv;
+  }
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    auto f = total.find(node);
+    if (f == total.end()) return "";
+    return f->second[em.lane];
+  };
+  for (int r : col_roots) {
+    std::vector<std::string> v(V);
+    for (int l = 0; l < V; ++l) {
+      em.lane = l;
+      Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+      v[l] = em.value(r, em.from_linear(col, c.g.nodes[r].dims));
+    }
+    std::string out = "out" + std::to_string(root_slot(c, r));
+    if (V == 4)
+      body.line("sfx_st4(" + out + " + c0, " + v[0] + ", " + v[1] + ", " + v[2] + ", " + v[3] + ");");
+    else
+      body.line(out + "[c0] = " + v[0] + ";");
+  }
+  em.pop();
+  body.indent--;
+  body.line("}");
+  body.line("if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;");
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = tiles;
+  ks.grid_y = S;
+  ks.vector_width = V;
+  ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
+            " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " lanes(col x row)=" +
+            std::to_string(CL) + "x" + std::to_string(RL);
+  return ks;
+}
+
+// Column reductions broadcast back (batch-norm): one launch, a co-resident
+// grid of column tiles x row stripes (2 CTAs/SM, one wave, cooperative
+// launch).  Per reduction level: every CTA folds its stripe (per-lane fp64
+// accumulators for f32 sums), combines its warps through shared memory and
+// writes a partial; a grid barrier; then every thread folds the S stripe
+// partials of its own columns in stripe order (identical totals in every CTA)
+// and keeps them in registers, where the broadcast-back reads them.  A final
+// pass writes the element roots.  Passes after the first re-read the stripe,
+// mostly from L2 (batch-norm [65536, 256]: 64 MB).
+KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "colbc";
+  ks.entry = "sfx_colbc_" + c.name;
+  fill_common(c, ks);
+  const int64_t O = bp.O, R = bp.R, I = bp.I, C = O * I;
+  const int V = (I % 4 == 0) ? 4 : 1;
+  const int64_t cvec = (C + V - 1) / V;
+  int CL = 1;
+  while (CL < 32 && CL < cvec) CL *= 2;
+  const int RL = 32 / CL;
+  const int WARPS = 8, B = WARPS * 32;
+  const int RSUB = WARPS * RL;
+  const int64_t TC = static_cast<int64_t>(CL) * V;
+  const int64_t tiles = (C + TC - 1) / TC;
+  const int ctas_per_sm = o.pipe_ctas_per_sm > 0 ? std::min(o.pipe_ctas_per_sm, 8) : 2;
+  if (tiles > int64_t{kNumSMs} * ctas_per_sm)
+    throw Error(SFX_ERR_UNSUPPORTED, "colbc: " + std::to_string(tiles) + " column tiles exceed one co-resident wave");
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / tiles);
+  S = std::min<int64_t>(S, std::max<int64_t>(1, R / RSUB));
+  S = std::max<int64_t>(1, std::min<int64_t>(S, kNumSMs * ctas_per_sm / tiles));
+  const int64_t RS = (R + S - 1) / S;
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
+  const int NR = static_cast<int>(c.reduces.size());
+  Emitter em(c.g, c.p, V, c.wide);
+  std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  auto acc_t = [&](int r) -> std::string {
+    const Node& rn = c.g.nodes[r];
+    return (rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? "double" : ctype(rn.dtype);
+  };
+  auto fold_fn = [&](int r) -> const char* {
+    const Node& rn = c.g.nodes[r];
+    return rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum" : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax"
+                                                                                         : "sfx_fold_pmin";
+  };
+  // workspace: barrier counters (64 words), then per reduce partials[S][C] and totals[C] (8-byte slots)
+  std::map<int, int64_t> part_word, tot_word;
+  int64_t words = 64;  // [0] arrivals, [1] exits, [2] launch sequence (cross-rank)
+  for (int r : c.reduces) {
+    part_word[r] = words;
+    words += S * C * 2;
+    tot_word[r] = words;
+    words += C * 2 + 64;
+  }
+  ks.workspace_bytes = words * 4;
+  ks.cooperative = true;
+  // cross-rank (SyncBatchNorm): per level, each rank's column totals are pushed
+  // to every rank's peer arena (slots [2][PMAX][NR][C], 8 B) by the tile's first
+  // stripe CTA, flagged per tile with the step number, and folded in rank order
+  // by every thread.  Steps number (launch, level) pairs: launch_seq * L + lv.
+  const int PMAX = SFX_PEER_MAX_RANKS;
+  std::map<int, int> red_index;
+  for (int k = 0; k < NR; ++k) red_index[c.reduces[k]] = k;
+  const int64_t pflag_byte = (2LL * PMAX * NR * C) * 8;
+  if (c.peer) {
+    for (int r : c.reduces) {
+      const Node& rn = c.g.nodes[r];
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32)
+        throw Error(SFX_ERR_UNSUPPORTED, "cross-rank colbc supports sum reductions (max/min NaN-first rule: col template)");
+    }
+    ks.peer_bytes = (pflag_byte + tiles * PMAX * 4 + 255) / 256 * 256;
+  }
+  body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const int cl = lane & " + std::to_string(CL - 1) + ", rl = lane / " + std::to_string(CL) + ";");
+  body.line("const int rsub = warp * " + std::to_string(RL) + " + rl;");
+  body.line("const " + it + " c0 = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cl * " + std::to_string(V) + ";");
+  body.line("const bool cok = c0 < " + fmt_i(C) + ";");
+  body.line("const " + it + " r_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  body.line("const " + it + " r_end = min((" + it + ")" + fmt_i(R) + ", r_begin + " + fmt_i(RS) + ");");
+  body.line("const " + it + " co = cok ? c0 / " + fmt_i(I) + " : 0, ci = cok ? c0 % " + fmt_i(I) + " : 0;");
+  if (c.peer) body.line("const unsigned launch_seq = __ldcg(ws + 2);");
+  auto inner_ix = [&](int lane) {
+    em.lane = lane;
+    return V == 1 ? em.uni("ci") : em.lane_plus("ci");
+  };
+  // totals of every finished level, per lane, in registers
+  std::map<int, std::vector<std::string>> total;
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    auto f = total.find(node);
+    if (f == total.end()) {
+      if (c.g.nodes[node].op == SFX_OP_REDUCE && !degenerate_reduce(c.g, c.g.nodes[node]))
+        throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
+      return "";
+    }
+    return f->second[em.lane];
+  };
+  // a pass over this CTA's stripe: UR rows per iteration (unguarded, loads in
+  // flight together), then the remainder
+  auto stripe_pass = [&](const std::function<void(const std::string&)>& row) {
+    body.line("if (cok) {");
+    body.indent++;
+    const std::string r = em.fresh("r");
+    body.line(it + " " + r + " = r_begin + rsub;");
+    body.line("for (; " + r + " + " + std::to_string((UR - 1) * RSUB) + " < r_end; " + r + " += " +
+              std::to_string(UR * RSUB) + ") {");
+    body.indent++;
+    em.push();
+    for (int u = 0; u < UR; ++u) {
+      std::string ru = em.fresh("ru");
+      body.line("const " + it + " " + ru + " = " + r + " + " + std::to_string(u * RSUB) + ";");
+      row(ru);
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.line("for (; " + r + " < r_end; " + r + " += " + std::to_string(RSUB) + ") {");
+    body.indent++;
+    em.push();
+    row(r);
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.indent--;
+    body.line("}");
+  };
+  for (int lv = 1; lv <= bp.max_level; ++lv) {
+    std::vector<int> red;
+    for (int r : c.reduces)
+      if (bp.level.at(r) == lv) red.push_back(r);
+    std::vector<std::vector<std::string>> acc(red.size(), std::vector<std::string>(V));
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      std::string init = rn.reducer == SFX_REDUCE_SUM ? (rn.dtype == SFX_F32 ? "0.0" : "0")
+                         : rn.dtype == SFX_F32        ? "sfx_bits_f(0x7fc00000)"
+                         : rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+      for (int l = 0; l < V; ++l) {
+        acc[k][l] = em.fresh("acc");
+        body.line(acc_t(red[k]) + " " + acc[k][l] + " = " + init + ";");
+      }
+    }
+    stripe_pass([&](const std::string& ru) {
+      Ix rix = em.uni(ru), oix = em.uni("co");
+      for (int l = 0; l < V; ++l) {
+        Ix iix = inner_ix(l);
+        for (size_t k = 0; k < red.size(); ++k) {
+          const Node& rn = c.g.nodes[red[k]];
+          const Node& in = c.g.nodes[rn.operands[0]];
+          std::string v = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, oix, rix, iix));
+          body.line(acc[k][l] + " = " + fold_fn(red[k]) + "(" + acc[k][l] + ", " + v + ");");
+        }
+      }
+    });
+    // CTA combine over row sub-streams (deterministic order), partials out
+    for (size_t k = 0; k < red.size(); ++k) {
+      const std::string T = acc_t(red[k]);
+      const std::string sp = em.fresh("sp");
+      body.line("__shared__ " + T + " " + sp + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
+      for (int l = 0; l < V; ++l)
+        body.line(sp + "[rsub][cl * " + std::to_string(V) + " + " + std::to_string(l) + "] = " + acc[k][l] + ";");
+      body.line("__syncthreads();");
+      body.line("if (warp == 0 && rl == 0 && cok) {");
+      for (int l = 0; l < V; ++l) {
+        std::string sidx = "cl * " + std::to_string(V) + " + " + std::to_string(l);
+        std::string t = em.fresh("t");
+        body.line("  " + T + " " + t + " = " + sp + "[0][" + sidx + "];");
+        body.line("  for (int w = 1; w < " + std::to_string(RSUB) + "; ++w) " + t + " = " + fold_fn(red[k]) + "(" + t +
+                  ", " + sp + "[w][" + sidx + "]);");
+        body.line("  *(" + T + "*)((unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) + ") + (" + it +
+                  ")blockIdx.y * " + fmt_i(C) + " + c0 + " + std::to_string(l) + ") = " + t + ";");
+      }
+      body.line("}");
+    }
+    body.line("sfx_grid_barrier(ws, " + std::to_string(2 * lv - 1) + "u);");
+    // the S stripe partials of each column are folded once, spread over the
+    // tile's S CTAs (CTA y takes columns y, y + S, ...; its 256 threads split
+    // the stripes and combine by a fixed shuffle / warp-order tree), into
+    // totals[C]; a second barrier; then every thread reads its columns'
+    // totals.  (Every CTA folding all S partials itself cost ~4x the data
+    // pass in L2 loads: batch-norm [65536,256] 208 us.)
+    for (size_t k = 0; k < red.size(); ++k) {
+      const std::string T = acc_t(red[k]);
+      const Node& rn = c.g.nodes[red[k]];
+      std::string ident = rn.reducer == SFX_REDUCE_SUM ? (T == "double" ? "0.0" : "0")
+                          : rn.dtype == SFX_F32        ? "sfx_bits_f(0x7fc00000)"
+                          : rn.reducer == SFX_REDUCE_MAX ? "(int)0x80000000u" : "0x7fffffff";
+      const std::string pt = "(const unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) + ")";
+      const std::string tt = "(unsigned long long*)(ws + " + fmt_i(tot_word[red[k]]) + ")";
+      const std::string fs = em.fresh("fs");
+      body.line("__shared__ " + T + " " + fs + "[" + std::to_string(WARPS) + "];");
+      body.line("for (" + it + " cc = blockIdx.y; cc < " + fmt_i(TC) + "; cc += " + fmt_i(S) + ") {");
+      body.line("  const " + it + " col = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cc;");
+      body.line("  if (col >= " + fmt_i(C) + ") break;");
+      body.line("  " + T + " a = " + ident + ";");
+      body.line("  for (" + it + " s = threadIdx.x; s < " + fmt_i(S) + "; s += " + std::to_string(B) + ") a = " +
+                fold_fn(red[k]) + "(a, __ldcg((const " + T + "*)(" + pt + " + s * " + fmt_i(C) + " + col)));");
+      body.line(std::string("  for (int m = 16; m >= 1; m /= 2) a = ") + fold_fn(red[k]) +
+                "(a, __shfl_xor_sync(0xffffffffu, a, m));");
+      body.line("  if (lane == 0) " + fs + "[warp] = a;");
+      body.line("  __syncthreads();");
+      body.line("  if (threadIdx.x == 0) {");
+      body.line("    " + T + " t = " + fs + "[0];");
+      body.line("    for (int w = 1; w < " + std::to_string(WARPS) + "; ++w) t = " + std::string(fold_fn(red[k])) + "(t, " +
+                fs + "[w]);");
+      body.line("    *(" + T + "*)(" + tt + " + col) = t;");
+      body.line("  }");
+      body.line("  __syncthreads();");
+      body.line("}");
+    }
+    body.line("sfx_grid_barrier(ws, " + std::to_string(2 * lv) + "u);");
+    if (c.peer) {
+      // exchange this level's totals across ranks (all reduces of the level)
+      body.line("if (pn > 1) {");
+      body.indent++;
+      body.line("const unsigned step = launch_seq * " + std::to_string(bp.max_level) + "u + " + std::to_string(lv) + "u;");
+      body.line("const long long par = step & 1u;");
+      body.line("if (blockIdx.y == 0) {");
+      body.line("  for (" + it + " cc = threadIdx.x; cc < " + fmt_i(TC) + "; cc += " + std::to_string(B) + ") {");
+      body.line("    const " + it + " col = (" + it + ")blockIdx.x * " + fmt_i(TC) + " + cc;");
+      body.line("    if (col >= " + fmt_i(C) + ") break;");
+      for (size_t k = 0; k < red.size(); ++k) {
+        const std::string T = acc_t(red[k]);
+        body.line("    { const " + T + " v = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
+                  fmt_i(tot_word[red[k]]) + ") + col));");
+        body.line("      for (int p = 0; p < pn; ++p) *(" + T + "*)((unsigned long long*)(peers[p] + poff) + ((par * " +
+                  std::to_string(PMAX) + " + prank) * " + std::to_string(NR) + " + " + std::to_string(red_index[red[k]]) +
+                  ") * " + fmt_i(C) + " + col) = v; }");
+      }
+      body.line("  }");
+      body.line("  __syncthreads();");
+      body.line("  if (threadIdx.x < pn) sfx_st_release_sys((unsigned*)(peers[threadIdx.x] + poff + " +
+                fmt_i(pflag_byte) + ") + blockIdx.x * " + std::to_string(PMAX) + " + prank, step);");
+      body.line("}");
+      body.line("if (threadIdx.x < pn) sfx_peer_wait((const unsigned*)(peers[prank] + poff + " + fmt_i(pflag_byte) +
+                ") + blockIdx.x * " + std::to_string(PMAX) + " + threadIdx.x, step);");
+      body.line("__syncthreads();");
+      body.indent--;
+      body.line("}");
+    }
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      const std::string T = acc_t(red[k]);
+      std::vector<std::string> tv(V);
+      for (int l = 0; l < V; ++l) {
+        tv[l] = em.fresh("tot");
+        body.line(T + " " + tv[l] + " = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
+                  fmt_i(tot_word[red[k]]) + ") + (cok ? c0 : 0) + " + std::to_string(l) + "));");
+      }
+      if (c.peer) {  // the ranks' totals, in rank order (identical on every rank)
+        body.line("if (pn > 1) {");
+        body.line("  const long long par = (launch_seq * " + std::to_string(bp.max_level) + "u + " + std::to_string(lv) +
+                  "u) & 1u;");
+        body.line("  const unsigned long long* xs = (const unsigned long long*)(peers[prank] + poff) + (par * " +
+                  std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(red_index[red[k]]) + ") * " +
+                  fmt_i(C) + " + (cok ? c0 : 0);");
+        for (int l = 0; l < V; ++l) {
+          body.line("  " + tv[l] + " = __ldcv((const " + T + "*)(xs + " + std::to_string(l) + "));");
+          body.line("  for (int q = 1; q < pn; ++q) " + tv[l] + " = " + fold_fn(red[k]) + "(" + tv[l] + ", __ldcv((const " +
+                    T + "*)(xs + (long long)q * " + std::to_string(NR) + " * " + fmt_i(C) + " + " + std::to_string(l) +
+                    ")));");
+        }
+        body.line("}");
+      }
+      if (T == "double")
+        for (int l = 0; l < V; ++l) {
+          std::string f = em.fresh("tot");
+          body.line("const float " + f + " = (float)" + tv[l] + ";");
+          tv[l] = f;
+        }
+      if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
+        const Node& in = c.g.nodes[rn.operands[0]];
+        for (int l = 0; l < V; ++l) {
+          em.push();
+          Ix iix = inner_ix(l);
+          std::string f0 = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni("0"), iix));
+          body.line(tv[l] + " = sfx_fold_first(" + f0 + ", " + tv[l] + ");");
+          em.pop();
+        }
+      }
+      total[red[k]] = tv;
+    }
+  }
+  // final pass: element roots; column roots from stripe 0
+  std::vector<int> full_roots, col_roots;
+  for (int r : c.p.roots) (c.g.nodes[r].numel() == O * R * I ? full_roots : col_roots).push_back(r);
+  if (!full_roots.empty())
+    stripe_pass([&](const std::string& ru) {
+      Ix rix = em.uni(ru), oix = em.uni("co");
+      std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+      std::vector<std::string> faddr(full_roots.size());
+      std::vector<bool> fvec(full_roots.size(), V == 4);
+      std::vector<std::vector<std::string>> fad(full_roots.size(), std::vector<std::string>(V));
+      for (int l = 0; l < V; ++l) {
+        Ix iix = inner_ix(l);
+        for (size_t k = 0; k < full_roots.size(); ++k) {
+          std::vector<Ix> comps = orc_comps(em, c.g.nodes[full_roots[k]].dims, O, R, I, oix, rix, iix);
+          fv[k][l] = em.value(full_roots[k], comps);
+          Ix L = em.linearize(comps, c.g.nodes[full_roots[k]].dims);
+          fad[k][l] = L.e;
+          if (l == 0) {
+            if (L.kind == IX_PLUS) faddr[k] = L.base;
+            else fvec[k] = false;
+          }
+        }
+      }
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+        if (fvec[k])
+          body.line("sfx_st4(" + out + " + " + faddr[k] + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] + ", " +
+                    fv[k][3] + ");");
+        else
+          for (int l = 0; l < V; ++l) body.line(out + "[" + fad[k][l] + "] = " + fv[k][l] + ";");
+      }
+    });
+  if (!col_roots.empty()) {
+    body.line("if (blockIdx.y == 0 && warp == 0 && rl == 0 && cok) {");
+    body.indent++;
+    em.push();
+    for (int r : col_roots) {
+      for (int l = 0; l < V; ++l) {
+        em.lane = l;
+        Ix col = V == 1 ? em.uni("c0") : em.lane_plus("c0");
+        std::string v = em.value(r, em.from_linear(col, c.g.nodes[r].dims));
+        body.line("out" + std::to_string(root_slot(c, r)) + "[c0 + " + std::to_string(l) + "] = " + v + ";");
+      }
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  if (c.peer)  // the last CTA out also advances the launch sequence
+    body.line("if (threadIdx.x == 0 && atomicAdd(ws + 1, 1u) == gridDim.x * gridDim.y - 1u) { ws[0] = 0u; ws[1] = 0u; "
+              "ws[2] = launch_seq + 1u; }");
+  else
+    body.line("sfx_grid_exit(ws);");
+  ks.code = assemble(sig, body);
+  ks.block = B;
+  ks.grid_x = tiles;
+  ks.grid_y = S;
+  ks.vector_width = V;
+  ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
+            " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " levels=" +
+            std::to_string(bp.max_level) + " (grid barriers, cooperative launch)";
+  return ks;
+}
+
+}  // namespace lw
+}  // namespace sfx
