@@ -322,14 +322,26 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
       body.line("for (int w = 1; w < " + std::to_string(W) + "; ++w) " + acc[k] + " = " + fold_of(rn) + "(" + acc[k] +
                 ", " + sm + "[w]);");
       if (CS > 1) {
-        // cluster combine: every CTA folds the CS partials in rank order
-        const std::string xp = em.fresh("xp");
+        // cluster combine: every CTA folds the CS partials in rank order.  One
+        // warp reads them (lane r from rank r, one DSMEM load each) and lane 0
+        // folds them in order; the CTA reads the result from local smem (all
+        // 512 threads reading every rank's slot over DSMEM cost 12% of the
+        // kernel's smem wavefronts in conflicts)
+        const std::string xp = em.fresh("xp"), xr = em.fresh("xr");
         body.line("__shared__ " + T + " " + xp + ";");
+        body.line("__shared__ " + T + " " + xr + ";");
         body.line("if (tid == 0) " + xp + " = " + acc[k] + ";");
         body.line("sfx_cluster_sync();");
-        body.line(acc[k] + " = sfx_dsmem_ld(&" + xp + ", 0u);");
-        body.line("for (unsigned r = 1; r < " + std::to_string(CS) + "u; ++r) " + acc[k] + " = " + fold_of(rn) + "(" +
-                  acc[k] + ", sfx_dsmem_ld(&" + xp + ", r));");
+        body.line("if (warp == 0) {");
+        body.line("  const " + T + " v = lane < " + std::to_string(CS) + " ? sfx_dsmem_ld(&" + xp + ", (unsigned)lane) : " +
+                  xp + ";");
+        body.line("  " + T + " a = __shfl_sync(0xffffffffu, v, 0);");
+        body.line("  for (int r = 1; r < " + std::to_string(CS) + "; ++r) a = " + fold_of(rn) +
+                  "(a, __shfl_sync(0xffffffffu, v, r));");
+        body.line("  if (lane == 0) " + xr + " = a;");
+        body.line("}");
+        body.line("__syncthreads();");
+        body.line(acc[k] + " = " + xr + ";");
       }
       std::string fin = acc[k];
       if (T == "double") {
