@@ -135,7 +135,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     const int64_t bytes = C * 4 * static_cast<int64_t>(staged.size());
     // (pipe_stages doubles as the largest cluster size to consider: 16 is the
     // non-portable maximum)
-    const int cs_max = o.pipe_stages == 16 ? 16 : 8;
+    // (pipe_stages = 16 / 8 forces the non-portable 16-CTA cluster on / off)
+    const int cs_max = o.pipe_stages == 8 ? 8 : 16;
     const int64_t slice_max = o.pipe_stages == 16 ? 32 * 1024 : 64 * 1024;
     int cs = 2;
     while (cs < cs_max && bytes / cs > slice_max) cs *= 2;

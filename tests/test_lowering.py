@@ -22,6 +22,7 @@ def _note(path, k=0, **kw):
 
 @pytest.mark.parametrize("name,entry,strategy", [
     ("softmax_r4_c131072", "sfx_rowcl_", "row"),      # cluster + DSMEM long rows
+    ("softmax_r2_c262144", "sfx_rowcl_", "row"),      # 16-CTA cluster (non-portable size)
     ("ln_r6_c98304", "sfx_rowcl_", "row"),
     ("ln_r5_c70001", "sfx_rowmp_", "row"),            # odd width: multi-pass
     ("softmax_r16_c16384", "sfx_row_", "row"),        # register-resident, multi-warp
