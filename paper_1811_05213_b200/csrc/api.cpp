@@ -972,9 +972,10 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
         uint64_t bytes = 0;
         for (int in : chunked) bytes += g.nodes[in].numel() * 4;
         for (int r : ret) bytes += g.nodes[r].numel() * 4;
-        // default: up to 32 chunks of >= 4 MB (measured: C1 67 MB best at 4-8 MB
-        // chunks, C2 537 MB at ~16 MB, C5's 3.2 GB probs_d flat from 16 to 100 MB)
-        const uint64_t cb = host_chunk_bytes() ? host_chunk_bytes() : std::max<uint64_t>(4 << 20, bytes / 32);
+        // default: up to 32 chunks of >= 8 MB (measured: C1 67 MB flat at 4-8 MB
+        // chunks, C4 / C4b 1.63 / 2.99 ms at 4 MB vs 1.58 / 2.87 at 8 MB, C2 537 MB
+        // best at ~16 MB, C5's 3.2 GB probs_d flat from 16 to 100 MB)
+        const uint64_t cb = host_chunk_bytes() ? host_chunk_bytes() : std::max<uint64_t>(8 << 20, bytes / 32);
         int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, static_cast<int64_t>(bytes / cb)));
         const int64_t unit = std::max<int64_t>(1, ks.stream_unit);
         rpc = ((R + want - 1) / want + unit - 1) / unit * unit;
