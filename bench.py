@@ -216,6 +216,25 @@ def run_reference_arm(args):
     return 0
 
 
+def agreed_rounds(more, round_fn, ws, red_dev):
+    """Run round_fn while more() holds on ANY rank: every rank runs the same
+    number of rounds, so a step that exchanges data across ranks (the
+    cross-rank column combine) is issued equally often everywhere."""
+    import torch
+    import torch.distributed as dist
+    n = 0
+    while True:
+        m = bool(more())
+        if ws > 1:
+            flag = torch.tensor([1.0 if m else 0.0], device=red_dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            m = flag.item() > 0
+        if not m:
+            return n
+        round_fn()
+        n += 1
+
+
 def config_obj(config, n, combine="peer"):
     if config not in ("C3", "C3b") or n == 1:
         par = f"batch-sharded independent graph instances x{n} (no collective)"
@@ -339,18 +358,14 @@ def run_ours(args):
     # on every rank, so the continue decision is agreed each round (max).
     t_load = time.perf_counter()
     n_load = 0
-    while True:
-        more = clk.count_after(t_load + 0.15) < 2 and time.perf_counter() - t_load < 5.0
-        if ws > 1:
-            flag = torch.tensor([1.0 if more else 0.0], device=red_dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-            more = flag.item() > 0
-        if not more:
-            break
+    def load_round():
+        nonlocal n_load
         for _ in range(16):
             step(n_load)
             n_load += 1
         torch.cuda.synchronize(dev)
+    agreed_rounds(lambda: clk.count_after(t_load + 0.15) < 2 and time.perf_counter() - t_load < 5.0,
+                  load_round, ws, red_dev)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -367,18 +382,8 @@ def run_ours(args):
     t_hi = time.perf_counter()
     launches = ctx.launch_count() - launches0
     t_post = time.perf_counter()
-    while True:  # same agreed-rounds rule as the load phase before the timed region
-        more = clk.count_after(t_post) < 2 and time.perf_counter() - t_post < 3.0
-        if ws > 1:
-            flag = torch.tensor([1.0 if more else 0.0], device=red_dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-            more = flag.item() > 0
-        if not more:
-            break
-        for _ in range(16):
-            step(n_load)
-            n_load += 1
-        torch.cuda.synchronize(dev)
+    agreed_rounds(lambda: clk.count_after(t_post) < 2 and time.perf_counter() - t_post < 3.0,
+                  load_round, ws, red_dev)
     clk.stop()
     # samples within 150 ms of the timed region, all under continuous load of the same step
     clocks = clk.summary(t_lo - 0.15, max(t_hi, t_post) + 0.15)

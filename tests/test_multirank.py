@@ -78,3 +78,33 @@ def test_bench_rank_environment_defaults(monkeypatch):
     monkeypatch.setenv("RANK", "3")
     monkeypatch.setenv("LOCAL_RANK", "3")
     assert bench.dist_env() == (8, 3, 3)
+
+
+def _rounds_worker(rank, ws, port, q):
+    import sys
+    sys.path.insert(0, T.ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import bench
+    local_want = 3 if rank == 0 else 7  # the ranks' own stopping points differ
+    done = []
+    n = bench.agreed_rounds(lambda: len(done) < local_want, lambda: done.append(1), ws, "cpu")
+    q.put((rank, n, len(done)))
+    dist.destroy_process_group()
+
+
+def test_bench_load_rounds_agree_across_ranks():
+    """bench.py's clock-sampling load phases stop on local timing; with a
+    cross-rank step the ranks must still run the same number of rounds."""
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rounds_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [7, 7] and [r[2] for r in res] == [7, 7]
