@@ -304,12 +304,17 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
     throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(k->src.outputs.size()) + " outputs");
   std::vector<CUdeviceptr> vals;
   vals.reserve(in.size() + out.size() + 1);
+  // every template assumes 16-byte aligned bases (128-bit ld/st, sfx_st4, TMA
+  // bulk copies); a misaligned base (e.g. a tensor view at an odd offset) would
+  // fault and poison the context, so it is refused here instead
   for (CUdeviceptr p : in) {
     if (!p) throw sfx::Error(SFX_ERR_EXEC, "null input pointer");
+    if (p & 15) throw sfx::Error(SFX_ERR_INVALID, "input pointer not 16-byte aligned (" + k->src.entry + ")");
     vals.push_back(p);
   }
   for (CUdeviceptr p : out) {
     if (!p) throw sfx::Error(SFX_ERR_EXEC, "null output pointer");
+    if (p & 15) throw sfx::Error(SFX_ERR_INVALID, "output pointer not 16-byte aligned (" + k->src.entry + ")");
     vals.push_back(p);
   }
   vals.push_back(k->ws);
@@ -529,13 +534,22 @@ void graph_enqueue(sfx_graph* G, const uint64_t* params, const uint64_t* outputs
   CUevent ev_fork = G->branch_events[K];
   sfx::check_cu(d.cuEventRecord(ev_fork, s), "cuEventRecord");
   std::vector<int> stream_of(K, -1);
-  int next = 0;
+  int next = 0, last_peer = -1;
   for (int p : G->order) {
     sfx_kernel* k = G->kernels[p];
     std::set<int> deps;
     for (int in : k->src.inputs) {
       auto it = producer.find(in);
       if (it != producer.end() && it->second != p) deps.insert(it->second);
+    }
+    // Kernels that exchange data with the other ranks (peer_bytes > 0) wait on
+    // peers' kernels, so every rank must run them in the same order, one at a
+    // time: each is chained after the previous one (condensation order, the
+    // same on every rank).  On parallel branches rank A could run X while
+    // rank B runs Y, each spinning on a peer kernel that cannot become resident.
+    if (k->src.peer_bytes > 0) {
+      if (last_peer >= 0) deps.insert(last_peer);
+      last_peer = p;
     }
     int si;
     if (deps.empty()) {

@@ -117,9 +117,36 @@ KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   return ks;
 }
 
+// Under cross_rank the graph is one rank's batch shard and dim 0 of every
+// tensor is the sharded batch.  A matmul whose contraction axis is dim 0 of an
+// operand (traced back through transposes), e.g. dW = X^T * dY, would return a
+// per-shard partial sum; no matmul kernel combines across ranks, so such a
+// group is refused rather than silently wrong.  (Conservative: a replicated
+// weight's dim 0 counts as batch too, like the reductions' rule.)
+bool contracts_over_batch(const Graph& g, const Program& p) {
+  for (int m : p.members) {
+    const Node& n = g.nodes[m];
+    if (!is_matmul(n) || n.operands.size() != 2) continue;
+    for (int side = 0; side < 2; ++side) {
+      int v = n.operands[side];
+      int64_t axis = g.nodes[v].rank() - (side == 0 ? 1 : 2);
+      while (g.nodes[v].op == SFX_OP_TRANSPOSE && axis >= 0 && axis < static_cast<int64_t>(g.nodes[v].perm.size())) {
+        axis = g.nodes[v].perm[axis];  // output axis a reads input axis perm[a] (exec.cpp:172-176)
+        v = g.nodes[v].operands[0];
+      }
+      if (axis == 0) return true;
+    }
+  }
+  return false;
+}
+
 KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o) {
   if (pi < 0 || pi >= static_cast<int>(g.programs.size())) throw Error(SFX_ERR_INVALID, "program index out of range");
   const Program& p = g.programs[pi];
+  if (o.cross_rank && contracts_over_batch(g, p))
+    throw Error(SFX_ERR_UNSUPPORTED, "group " + g.nodes[p.fusion_root].id +
+                                         ": a matmul contracts over the sharded dim 0 (cross_rank); only the column "
+                                         "templates combine across ranks");
   if (p.barrier && dot_alone(g, p)) return lower_dot(g, p);  // no other lowering for LibraryCall
   Ctx c = make_ctx(g, p);
   std::string why;

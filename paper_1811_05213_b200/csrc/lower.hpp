@@ -77,6 +77,7 @@ KernelSource lower_dot(const Graph& g, const Program& p);
 // A program whose only member is a matmul: an unfused barrier, or a fuse_dot
 // group with nothing stitched to the BatchMatMul.  Runs the dot kernel.
 bool dot_alone(const Graph& g, const Program& p);
+bool is_matmul(const Node& n);
 
 // Synthetic one-member program for an instruction the planner left unfused
 // (Program::barrier set; includes a literal-tier plan).

@@ -328,8 +328,14 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
         // folds them in order; the CTA reads the result from local smem (all
         // 512 threads reading every rank's slot over DSMEM cost 12% of the
         // kernel's smem wavefronts in conflicts)
-        const std::string xp = em.fresh("xp"), xr = em.fresh("xr");
-        body.line("__shared__ " + T + " " + xp + ";");
+        // Persistent clusters reuse the slot row after row: it is double-buffered
+        // by row parity, because with a single cluster barrier per reduction a
+        // fast CTA may publish row i+1's partial before a peer's warp 0 has read
+        // row i's (two rows ahead needs the peer past row i+1's barrier, i.e.
+        // done reading row i)
+        const std::string xa = em.fresh("xp"), xr = em.fresh("xr");
+        const std::string xp = persist ? xa + "[itr & 1]" : xa;
+        body.line("__shared__ " + T + " " + xa + (persist ? "[2]" : "") + ";");
         body.line("__shared__ " + T + " " + xr + ";");
         body.line("if (tid == 0) " + xp + " = " + acc[k] + ";");
         body.line("sfx_cluster_sync();");

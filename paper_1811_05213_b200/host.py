@@ -434,7 +434,7 @@ def codegen(graph: TensorGraph, program: KernelProgram, strategy="auto", **kw):
     return src.value.decode(), path.value.decode(), strat.value.decode()
 
 
-def codegen_barrier(graph: TensorGraph, report: "CompileReport", k: int):
+def codegen_barrier(graph: TensorGraph, report: "CompileReport", k: int, **kw):
     """Like codegen() for the k-th unfused matmul barrier of a compiled module
     (instruction order), which runs as its own kernel."""
     programs = [kk.program for kk in report.kernels]
@@ -442,7 +442,7 @@ def codegen_barrier(graph: TensorGraph, report: "CompileReport", k: int):
     src = C.create_string_buffer(1 << 22)
     path = C.create_string_buffer(4096)
     strat = C.create_string_buffer(1024)
-    opts = compile_opts()
+    opts = compile_opts(**kw)
     _check(lib().sfx_program_codegen(gd.ref(), len(programs) + k, C.byref(opts), src, len(src), path, len(path),
                                      strat, len(strat)))
     return src.value.decode(), path.value.decode(), strat.value.decode()

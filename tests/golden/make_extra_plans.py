@@ -66,6 +66,22 @@ EXTRA = {
     "softmax_r2_c262144": configs.c2_softmax(B=1, H=1, S=2, L=262144),  # 16-CTA (non-portable) cluster
     "ln_r6_c98304": configs.c1_layernorm(R=6, C=98304),
     "ln_r5_c70001": configs.c1_layernorm(R=5, C=70001),
+    # more rows than persistent clusters (row_pipeline=3 loops rows per cluster)
+    "softmax_r40_c131072": configs.c2_softmax(B=1, H=1, S=40, L=131072),
+    
+    # a single-reduction group (RMSNorm: one reduce level + element roots)
+    "rms_r80_c98304": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [80, 98304]},
+        {"id": "g", "op": "parameter", "shape": [98304]},
+        {"id": "x2", "op": "mul", "operands": ["x", "x"], "shape": [80, 98304]},
+        {"id": "ms", "op": "reduce", "operands": ["x2"], "shape": [80], "reduce_dims": [1], "reducer": "mean"},
+        {"id": "eps", "op": "constant", "shape": [80], "value": 1e-6},
+        {"id": "mse", "op": "add", "operands": ["ms", "eps"], "shape": [80]},
+        {"id": "r", "op": "rsqrt", "operands": ["mse"], "shape": [80]},
+        {"id": "rb", "op": "broadcast", "operands": ["r"], "shape": [80, 98304], "broadcast_dim_map": [0]},
+        {"id": "gb", "op": "broadcast", "operands": ["g"], "shape": [80, 98304], "broadcast_dim_map": [1]},
+        {"id": "n", "op": "mul", "operands": ["x", "rb"], "shape": [80, 98304]},
+        {"id": "y", "op": "mul", "operands": ["n", "gb"], "shape": [80, 98304]}], "outputs": ["y"]},
     # column statistics broadcast back (batch-norm): the colbc template
     "bn_4096x256": bn_graph([4096, 256], [0]),
     "bn_mid_8x512x64": bn_graph([8, 512, 64], [1]),
@@ -101,11 +117,35 @@ EXTRA = {
 }
 
 
+def two_cross_rank_groups(rows=2048, cols=256, count=4096):
+    """One rank's shard with TWO independent batch-crossing groups: SyncBatchNorm
+    over x (colbc) and a bias-grad column sum over (dy, z) (col).  Both wait on
+    the peer ranks inside the kernel, so the executor must run them in the same
+    order on every rank (never on parallel branches)."""
+    bn = bn_graph([rows, cols], [0], count=count)
+    ins = bn["instructions"] + [
+        {"id": "dy", "op": "parameter", "shape": [rows, cols]},
+        {"id": "z", "op": "parameter", "shape": [rows, cols]},
+        {"id": "zero", "op": "constant", "shape": [rows, cols], "value": 0.0},
+        {"id": "mask", "op": "compare", "operands": ["z", "zero"], "shape": [rows, cols]},
+        {"id": "dx", "op": "mul", "operands": ["dy", "mask"], "shape": [rows, cols]},
+        {"id": "db", "op": "reduce", "operands": ["dx"], "shape": [cols], "reduce_dims": [0], "reducer": "sum"}]
+    return {"instructions": ins, "outputs": ["y", "db"]}
+
+
+# batch-sharded graphs run with cross_rank (tests/test_gpu_peer.py)
+XRANK = {"two_xrank_shard_2048x256": two_cross_rank_groups()}
+
+
 def main():
-    out_dir = os.path.join(HERE, "plans_extra")
-    os.makedirs(out_dir, exist_ok=True)
     tool = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
-    for name, doc in EXTRA.items():
+    for sub, table in (("plans_extra", EXTRA), ("plans_xrank", XRANK)):
+        export(tool, os.path.join(HERE, sub), table)
+
+
+def export(tool, out_dir, table):
+    os.makedirs(out_dir, exist_ok=True)
+    for name, doc in table.items():
         with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
             f.write(configs.dumps(doc))
             path = f.name

@@ -97,6 +97,24 @@ def _worker(rank, ws, port, case, q):
             st.synchronize()
             out.append({o: t.cpu().numpy() for o, t in zip(g.outputs, outs)})
             cg.close()
+        elif case == "two_groups":
+            g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_xrank", "two_xrank_shard_2048x256.json"))
+            cg = H.CompiledGraph(ctx, g, rep, cross_rank=1)
+            assert sorted(k.info["strategy"] for k in cg.kernels) == ["col", "colbc"]
+            import torch
+            dev = torch.device("cuda", 0)
+            for it in range(2):
+                inputs = _two_inputs(500 + it, rank)
+                out.append(cg.run_host(inputs))
+                ins = [torch.from_numpy(inputs[p]).to(dev) for p in cg.param_ids]
+                outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+                st = torch.cuda.Stream(device=dev)
+                for _ in range(3):  # device path: the captured graph, replayed
+                    cg.run([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], stream=st.cuda_stream,
+                           cuda_graph=True)
+                st.synchronize()
+                out.append({o: t.cpu().numpy() for o, t in zip(g.outputs, outs)})
+            cg.close()
         elif case == "min_nan":
             g, prog, p = _min_program(rank)
             (got,) = H.run_program(prog, g, {"p": p}, ctx=ctx, cross_rank=1)
@@ -114,6 +132,13 @@ def _bn_inputs(seed, rank, rows=2048, cols=256):
     return {"x": _shard(seed, 0, rows, cols, rank),
             "g": T.gen_tensor(seed, 1, cols, "f32", 0.5, 1.5),
             "b": T.gen_tensor(seed, 2, cols, "f32", -1.0, 1.0)}
+
+
+def _two_inputs(seed, rank, rows=2048, cols=256):
+    d = _bn_inputs(seed, rank, rows, cols)
+    d["dy"] = _shard(seed, 3, rows, cols, rank)
+    d["z"] = _shard(seed, 4, rows, cols, rank)
+    return d
 
 
 def _min_rows(rank):
@@ -213,3 +238,25 @@ def test_cross_rank_sync_batchnorm():
             y = outs[r][i]["y"]
             want = ref[r * 2048:(r + 1) * 2048]
             assert T.strict_close(y, want), (seed, r, T.mismatch_report(y, want))
+
+
+def test_two_cross_rank_groups_run_in_rank_order():
+    """Two independent batch-crossing groups in one graph (SyncBatchNorm colbc +
+    bias-grad col): both spin on peer ranks inside the kernel, so the executor
+    chains them in condensation order on every rank instead of putting them on
+    parallel branches (which could pair rank A's X with rank B's Y and hang).
+    Host path and CUDA-graph replays, against the fp64 restatement of the
+    unsharded graph."""
+    import sys
+    sys.path.insert(0, T.GOLDEN)
+    from make_extra_plans import two_cross_rank_groups
+    outs = _spawn("two_groups")
+    full = H.graph_from_json(two_cross_rank_groups(rows=2048 * WS, count=2048 * WS))
+    for i, seed in enumerate([500, 500, 501, 501]):
+        per = [_two_inputs(seed, r) for r in range(WS)]
+        inputs = {k: (np.concatenate([p[k] for p in per]) if k in ("x", "dy", "z") else per[0][k]) for k in per[0]}
+        ref = T.interpret(full, inputs, mode=1)
+        for r in range(WS):
+            y, db = outs[r][i]["y"], outs[r][i]["db"]
+            assert T.strict_close(y, ref["y"][r * 2048:(r + 1) * 2048]), (seed, r)
+            assert T.strict_close(db, ref["db"]), (seed, r, T.mismatch_report(db, ref["db"]))

@@ -105,3 +105,31 @@ def test_template_parameter_cache(tmp_path):
                          env=dict(os.environ, SFX_TEMPLATE_PARAMS=str(cache))).stdout.splitlines()
     assert "threads/row=128" in out[0] and "[template_params: tuned 13.30 -> 12.77 us]" in out[0], out
     assert "[template_params:" not in out[1], out
+
+
+def test_cross_rank_refuses_matmul_over_the_batch():
+    """Under cross_rank (one rank's batch shard, dim 0 = batch) a matmul that
+    contracts over dim 0 — dW = X^T * dY, traced through the transpose — would
+    be a per-shard partial sum: refused with SFX_ERR_UNSUPPORTED.  A batched
+    matmul contracting inside each batch element compiles."""
+    doc = {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [64, 32]},
+        {"id": "dy", "op": "parameter", "shape": [64, 16]},
+        {"id": "xt", "op": "transpose", "operands": ["x"], "shape": [32, 64], "permutation": [1, 0]},
+        {"id": "dw", "op": "library_call", "operands": ["xt", "dy"], "shape": [32, 16], "callee": "matmul"}],
+        "outputs": ["dw"]}
+    g = H.graph_from_json(doc)
+    rep = H.CompileReport.from_bundle({"graph": doc, "kernels": [], "unfused": ["xt", "dw"], "fused_kernels": 2,
+                                      "baseline_kernels": 2, "fusion_ratio": 1.0})
+    # barrier programs: [xt, dw]; dw is the second
+    assert H.codegen_barrier(g, rep, 1)[2].startswith("dot")
+    with pytest.raises(H.ExecError, match="contracts over the sharded dim 0"):
+        H.codegen_barrier(g, rep, 1, cross_rank=1)
+    bdoc = {"instructions": [
+        {"id": "q", "op": "parameter", "shape": [4, 8, 16]},
+        {"id": "k", "op": "parameter", "shape": [4, 16, 8]},
+        {"id": "s", "op": "batch_matmul", "operands": ["q", "k"], "shape": [4, 8, 8]}], "outputs": ["s"]}
+    bg = H.graph_from_json(bdoc)
+    brep = H.CompileReport.from_bundle({"graph": bdoc, "kernels": [], "unfused": ["s"], "fused_kernels": 1,
+                                       "baseline_kernels": 1, "fusion_ratio": 1.0})
+    assert H.codegen_barrier(bg, brep, 0, cross_rank=1)[2].startswith("dot")

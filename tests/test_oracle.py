@@ -149,3 +149,21 @@ def test_fast_generator_equals_numpy_stream():
     f = T.gen_inputs_fast(g, 3, -1.0, 1.0)
     for k in a:
         assert np.array_equal(a[k], f[k])
+
+
+def test_batch_slices_equal_b1_graph_on_offset_stream():
+    """The C5 full-size GPU check compares batch b of the b64 output with the
+    b1 graph run on batch b's slice of the input stream.  Pinned here on a
+    small batch count: the oracle on the B=3 graph, sliced per batch, equals
+    the oracle on the b1 graph with batch_slice_inputs — bit for bit."""
+    from workloads import configs
+    full = H.parse_graph(configs.c5_bert(B=3, S=32))
+    small = H.parse_graph(configs.c5_bert(B=1, S=32))
+    fin = T.gen_inputs_fast(full, 42, -1.0, 1.0)
+    want = T.interpret(full, fin, 0)
+    for b in range(3):
+        sin = T.batch_slice_inputs(full, small, 42, b)
+        got = T.interpret(small, sin, 0)
+        for o in small.outputs:
+            n = small.at(o).numel()
+            assert np.array_equal(got[o].reshape(-1), want[o].reshape(-1)[b * n:(b + 1) * n]), (b, o)
