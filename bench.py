@@ -1,19 +1,28 @@
 """Benchmark: fused-graph effective HBM GB/s (% of peak) and kernel launches per graph.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+                    [--shard strong|weak]
 
 One step = one execution of the whole compiled graph (every fusion group of
-the reference plan = one stitched sm_100a launch) over one graph instance
-with inputs resident in HBM.  Default workload: C5, the BERT-base
-encoder-layer non-MatMul graph at batch 64, seq 512 (5 groups, 5.03 GB of
-compulsory traffic), the BASELINE.json config that is batch-sharded across
-GPUs.  Under torchrun each rank runs its own instance on its own GPU (weak
-scaling, replicas of independent graph instances; no collective on this
-path).  `value` = compulsory bytes of all ranks / max-over-ranks device time.
+the reference plan = one stitched sm_100a launch) over one instance of the
+named config with inputs resident in HBM.  Default workload: C5, the
+BERT-base encoder-layer non-MatMul graph at batch 64, seq 512 (5 groups, 5.03
+GB of compulsory traffic).
+
+Multi-GPU, one process per GPU: `--shard strong` (default)
+batch-shards ONE global instance — rank r of n runs the reference's plan of
+its shard graph (workloads/plans/<C>.shard<n>.json, b64/n for C5; membership
+equal to the global plan's, tests/test_shards.py) on its rows; the only
+exchange is C3's batch-crossing column sum, combined across ranks inside the
+column kernel over peer memory.  `--shard weak` runs a full replica per rank.
+`value` = compulsory bytes of all ranks / max-over-ranks device time.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run.
 
 `--impl reference` times the reference's own CPU executor (run_compiled,
 built from the reference sources into oracle/_ref by oracle/Makefile; else
-the C oracle port) on a bounded sample of the same workload on all host cores.
+the C oracle port) on a bounded sample of the same workload whose reference
+plan has the global plan's group membership (asserted), on all host cores
+and on one core.
 """
 
 from __future__ import annotations
@@ -121,24 +130,69 @@ def dist_env():
     return ws, rank, local
 
 
-def plan_path(config):
-    return os.path.join(ROOT, "workloads", "plans", f"{config}.full.json")
+def plan_path(config, n=1, shard="strong"):
+    """The plan a rank runs: the global plan, or (strong sharding over n > 1
+    ranks) the reference's plan of one rank's shard graph."""
+    if n == 1 or shard == "weak":
+        return os.path.join(ROOT, "workloads", "plans", f"{config}.full.json")
+    p = os.path.join(ROOT, "workloads", "plans", f"{config}.shard{n}.json")
+    if not os.path.exists(p):
+        raise SystemExit(f"bench.py: no {n}-way shard plan for {config} ({p}); shard counts: 2, 4, 8")
+    return p
+
+
+def membership(bundle):
+    """Group membership of a plan bundle (what plan parity compares)."""
+    return [(k["fusion_root"], sorted(k["members"]), list(k["roots"])) for k in bundle["kernels"]]
 
 
 # --------------------------------------------------------------------------- reference arm
 
+REF_FOOTPRINT = 64 << 20  # PipelineOptions::footprint_limit default (options.hpp)
+_sample_cache = {}
+
+
 def reference_sample(config):
     """A bounded sample of the same workload for the reference's CPU executor:
-    the same rows (same lengths and op mix), fewer of them."""
+    the same rows (same lengths and op mix), fewer of them, planned by the
+    reference with its footprint cap scaled to the sample (returns doc,
+    description, footprint_limit).  The cap matters for C5 only: the reference
+    merges the two LayerNorm groups when a whole group fits under it
+    (fusion.cpp:69-85), so an unscaled sample would run a 4-group plan; the b8
+    shard (4096 tokens) is the largest batch shard planned like b64 under the
+    default 64 MiB, and the 64-token sample gets 64 MiB x 64/4096 = 1 MiB.
+    reference_sample_plan() asserts the membership equals the global plan's."""
     from workloads import configs
+    if config == "C5" and os.environ.get("SFX_REF_SAMPLE") == "b8":
+        # the exact b8 shard (rank r's graph at 8 GPUs), default options: ~4 min
+        # of single-core work per instance (SURVEY §8(d)), for a one-off record
+        return configs.c5_bert(B=8, S=512), "C5 b8 shard (1/8 of b64 s512, default options)", REF_FOOTPRINT
     if config == "C5":
-        # query block of 64 tokens: attention rows of 512, LN rows of 768, GELU rows of 3072,
-        # in the same byte proportions as b64 s512 (1/512 of it)
-        return configs.c5_bert(B=1, S=512, Sq=64), "C5 query block: batch 1, 64 query rows x 512 keys (1/512 of b64 s512)"
+        fl = REF_FOOTPRINT * 64 // 4096
+        return (configs.c5_bert(B=1, S=512, Sq=64), "C5 query block: batch 1, 64 query rows x 512 keys "
+                "(1/512 of b64 s512; footprint_limit 1 MiB = the b8 shard's 64 MiB scaled by 64/4096 tokens)", fl)
     sizes = {"C1": dict(R=64, C=1024), "C2": dict(B=1, H=1, S=128, L=512), "C3": dict(N=512, C=1024),
              "C3b": dict(N=512, C=1024), "C4": dict(B=1, S=128, H=16, D=64), "C4b": dict(B=1, S=128, H=16, D=64),
              "C4t": dict(B=1, S=128, H=16, D=64)}
-    return configs.build(config, **sizes[config]), f"{config} at {sizes[config]}"
+    return configs.build(config, **sizes[config]), f"{config} at {sizes[config]}", REF_FOOTPRINT
+
+
+def reference_sample_plan(config, path):
+    """The reference's plan of the sample (ref_tool plan, same footprint cap the
+    timing uses), checked against the global plan: same groups, same members."""
+    if config in _sample_cache:
+        return _sample_cache[config]
+    doc, sample, fl = reference_sample(config)
+    r = subprocess.run([REF_TOOL, "plan", path, "--footprint-limit", str(fl)], capture_output=True, text=True,
+                       check=True)
+    got = membership(json.loads(r.stdout))
+    with open(plan_path(config)) as f:
+        want = membership(json.load(f))
+    if got != want:
+        raise RuntimeError(f"reference plan of the {config} sample differs from the global plan: "
+                           f"{[g[0] for g in got]} vs {[w[0] for w in want]}")
+    _sample_cache[config] = len(got)
+    return len(got)
 
 
 def graph_bytes(doc):
@@ -152,16 +206,22 @@ def graph_bytes(doc):
 
 
 def time_reference_cpu(config, threads, iters=1):
-    doc, sample = reference_sample(config)
+    """One sample: `threads` independent run_compiled instances on as many host
+    threads (the reference executor is single-threaded and reentrant)."""
+    doc, sample, fl = reference_sample(config)
     nbytes = graph_bytes(doc)
+    groups = None
     with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
         json.dump(doc, f)
         path = f.name
     try:
         if os.path.exists(REF_TOOL):
-            r = subprocess.run([REF_TOOL, "bench", path, "42", str(threads), str(iters)], capture_output=True,
-                               text=True, check=True)
+            groups = reference_sample_plan(config, path)
+            r = subprocess.run([REF_TOOL, "bench", path, "42", str(threads), str(iters), "--footprint-limit", str(fl)],
+                               capture_output=True, text=True, check=True)
             info = json.loads(r.stdout)
+            if len(info["groups"]) != groups:
+                raise RuntimeError(f"reference ran {len(info['groups'])} groups, planned {groups}")
             secs = info["seconds"]
             kind = "reference"
             execu = "reference run_compiled (oracle/_ref, built from the reference sources)"
@@ -181,9 +241,21 @@ def time_reference_cpu(config, threads, iters=1):
     finally:
         os.unlink(path)
     gbs = threads * iters * nbytes / secs / 1e9
-    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": f"{sample}; {execu}; {threads} independent instances x {iters} iteration(s); "
-                      f"{nbytes} compulsory bytes per instance; {secs:.2f} s wall"}, secs
+    cb = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind, "plan_groups": groups,
+          "sample": f"{sample}; {execu}; {threads} independent instance(s) x {iters} iteration(s); "
+                    f"{nbytes} compulsory bytes per instance; {secs:.2f} s wall"}
+    return cb, secs
+
+
+def cpu_baseline_both(config):
+    """All host cores (throughput) and one core (the reference's own,
+    single-threaded executor), on the same sample."""
+    threads = os.cpu_count() or 1
+    cb, secs = time_reference_cpu(config, threads)
+    one, secs1 = time_reference_cpu(config, 1) if threads > 1 else (cb, secs)
+    cb["value_1core"] = one["value"]
+    cb["sample_1core"] = one["sample"]
+    return cb, secs
 
 
 def run_reference_arm(args):
@@ -192,25 +264,37 @@ def run_reference_arm(args):
         return 0
     threads = os.cpu_count() or 1
     # W untimed samples, then K timed samples (each: one bounded sample of the
-    # workload as independent instances on every host thread)
-    for _ in range(args.warmup):
-        time_reference_cpu(args.config, threads)
+    # workload as independent instances on every host thread).  The whole run
+    # is bounded to a few minutes: warm-ups stop after ~30 s, and the timed
+    # samples are cut to what fits in ~150 s (reported as steps_timed).
+    t0 = time.perf_counter()
+    w_done = 0
+    t_step = None
+    while w_done < args.warmup and (w_done == 0 or time.perf_counter() - t0 < 30.0):
+        _, t_step = time_reference_cpu(args.config, threads)
+        w_done += 1
+    k_run = max(1, min(args.steps, int(150.0 // max(t_step, 1e-3))))
     times, values, cb = [], [], None
-    for _ in range(args.steps):
+    for _ in range(k_run):
         cb, secs = time_reference_cpu(args.config, threads)
         times.append(secs)
         values.append(cb["value"])
     ms = 1000.0 * sum(times) / len(times)
     # throughput over the timed samples: total bytes / total time
     value = sum(v * t for v, t in zip(values, times)) / sum(times)
-    cb = dict(cb, value=value)
+    one, _ = time_reference_cpu(args.config, 1) if threads > 1 else (cb, None)
+    cb = dict(cb, value=value, value_1core=one["value"], sample_1core=one["sample"])
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": config_obj(args.config, args.gpus),
+        "steps": args.steps, "warmup": args.warmup, "steps_timed": k_run, "warmup_run": w_done,
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": scaling_of(args), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_obj(args.config, args.gpus, args.combine, args.shard),
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": (f"CPU reference: each step is one bounded sample on {threads} host threads; "
+                 f"{k_run} of the {args.steps} requested steps timed, {w_done} warm-up(s), to keep the run "
+                 "within a few minutes"),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -235,15 +319,33 @@ def agreed_rounds(more, round_fn, ws, red_dev):
         n += 1
 
 
-def config_obj(config, n, combine="peer"):
-    if config not in ("C3", "C3b") or n == 1:
-        par = f"batch-sharded independent graph instances x{n} (no collective)"
-    elif combine == "peer":
-        par = f"batch-sharded x{n}; column sums combined across ranks inside the column kernel (peer memory)"
+def scaling_of(args):
+    return "strong" if args.shard == "strong" else "weak"
+
+
+def config_obj(config, n, combine="peer", shard="strong"):
+    """The workload (identical on both arms); run details go in `run`."""
+    from workloads import configs
+    strong = shard == "strong" and n > 1
+    if strong:
+        per = configs.shard_sizes(config, n)
+        d = configs.SHARD_DIM[config]
+        par = f"one global instance batch-sharded over {n} GPUs along {d} ({d}={per[d]} per rank)"
     else:
-        par = f"batch-sharded x{n} + NCCL all-reduce of the column sums"
-    return {"workload": f"{config}: {WORKLOAD_NAMES[config]}", "plan": f"workloads/plans/{config}.full.json "
-            "(reference compile_graph, default PipelineOptions)", "instances_per_gpu": 1, "parallelism": par}
+        par = f"independent graph instances x{n} (one full instance per GPU)" if n > 1 else "1 GPU"
+    if config in ("C3", "C3b") and n > 1:
+        par += ("; column sums combined across ranks inside the column kernel (peer memory)" if combine == "peer"
+                else "; NCCL all-reduce of the column sums")
+    else:
+        par += "; no collective"
+    c = {"workload": f"{config}: {WORKLOAD_NAMES[config]}",
+         "plan": os.path.relpath(plan_path(config, n, shard), ROOT) + " (reference compile_graph, default "
+                 "PipelineOptions)",
+         "parallelism": par}
+    if strong:
+        c["shard"] = {"dim": configs.SHARD_DIM[config], "ranks": n, "per_rank": configs.shard_sizes(config, n),
+                      "global": configs.FULL[config]}
+    return c
 
 
 # --------------------------------------------------------------------------- our arm
@@ -266,7 +368,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     red_dev = dev if args.dist_backend == "nccl" else "cpu"  # where cross-rank reductions of scalars live
     ctx = H.Context(local)
-    g, rep, bundle = H.load_bundle(plan_path(args.config))
+    g, rep, bundle = H.load_bundle(plan_path(args.config, ws, args.shard))
     # the one batch-crossing exchange on this path is a column reduction over
     # the batch (C3's db).  Default: the column kernel combines the ranks'
     # partials itself through peer memory (cross_rank); --combine nccl runs
@@ -283,7 +385,8 @@ def run_ours(args):
     # inputs resident in HBM; enough rotating sets that the sets exceed L2 (126 MB)
     per_set = sum(g.at(p).numel() * 4 for p in cg.param_ids) + sum(g.at(o).numel() * 4 for o in g.outputs)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    nsets = max(1, min(8, math.ceil(3 * l2 / per_set)))
+    # (small per-rank shards at 8 GPUs need many sets: C1 at 8 ranks is 8.4 MB)
+    nsets = max(1, min(64, math.ceil(3 * l2 / per_set)))
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     sets = []
@@ -506,17 +609,18 @@ def run_ours(args):
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            cpu, _ = time_reference_cpu(args.config, os.cpu_count() or 1)
+            cpu, _ = cpu_baseline_both(args.config)
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": scaling_of(args),
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.rand U(-1,1) inputs resident in HBM)",
-        "config": dict(config_obj(args.config, ws, args.combine), **{
-            "l2_policy": f"{nsets} rotating input/output set(s) of {per_set / 1e6:.1f} MB (> L2 {l2 / 1e6:.0f} MB)",
-            "groups": n_kernels, "launches_per_graph": n_kernels,
-            "instances_in_flight": inflight}),
+        "config": config_obj(args.config, ws, args.combine, args.shard),
+        "run": {"l2_policy": f"{nsets} rotating input/output set(s) of {per_set / 1e6:.1f} MB per rank "
+                             f"({nsets * per_set / 1e6:.0f} MB > L2 {l2 / 1e6:.0f} MB)",
+                "groups": n_kernels, "launches_per_graph": n_kernels, "instances_in_flight": inflight,
+                "bytes_per_rank_per_step": algo_bytes, "ranks": ws},
         "pct_of_peak": 100.0 * value / ws / peak,
         "peak_gbs": peak, "peak_kind": peak_kind,
         "kernel_launches_per_graph": n_kernels,
@@ -538,6 +642,19 @@ def run_ours(args):
     return 0
 
 
+def self_launch(args):
+    """`--gpus N` without torchrun: re-run this script as N ranks under
+    torch.distributed.run (127.0.0.1 rendezvous) and relay rank 0's line."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -552,8 +669,17 @@ def main():
                     help="cross-rank column sums: fused into the column kernel over peer memory, or NCCL after it")
     ap.add_argument("--inflight", type=int, default=0,
                     help="independent graph instances in flight per GPU (0 = auto)")
+    ap.add_argument("--shard", default="strong", choices=["strong", "weak"],
+                    help="strong: one global instance batch-sharded over the ranks (SURVEY §8(e)); "
+                         "weak: a full instance per rank")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -237,6 +237,16 @@ sfx_status sfx_graph_kernel_count(sfx_graph* g, int32_t* n_kernels, int32_t* n_p
  * pipeline.cpp:124-127); those are the kernels program_index >= n_programs of
  * sfx_graph_kernel.  use_cuda_graph=1 replays
  * a captured CUDA graph for this exact pointer set (captured on first use). */
+/* Concurrency: kernels that own a workspace (column / colbc cross-CTA
+ * combine) get one workspace per stream, so launches of one kernel or graph on
+ * different streams may run concurrently (each with its own buffers).  Every
+ * CUDA graph captured by sfx_graph_run owns its workspaces (replays of one
+ * capture are serialised by CUDA).  Exceptions: cross_rank kernels use one
+ * workspace and one peer region and must run in the same order on every rank,
+ * never concurrently with themselves; a launch captured by the CALLER's own
+ * stream capture uses the kernel's default workspace, so such captured
+ * replays must not overlap other launches of that kernel.  Calls on one
+ * sfx_graph from several host threads are serialised internally. */
 sfx_status sfx_graph_run(sfx_graph* g, const uint64_t* params, int32_t n_params,
                          const uint64_t* outputs, int32_t n_outputs, void* stream,
                          int32_t use_cuda_graph);

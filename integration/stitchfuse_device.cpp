@@ -3,8 +3,10 @@
 // descriptors of include/sfx.h and drives libsfx.so.
 #include "stitchfuse_device.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -130,7 +132,91 @@ struct Desc {
     desc.n_programs = static_cast<int32_t>(programs.size());
     desc.programs = programs.data();
   }
+
+  // Plan signature: every byte the lowering reads (the descriptors with their
+  // pointers replaced by the pointed-to contents) plus the options.  Equal
+  // signatures compile to the same kernels, so the compiled object is reused.
+  std::string signature(const sfx_compile_opts& o) const {
+    std::string k;
+    auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+    put(&o, sizeof o);
+    for (size_t i = 0; i < instrs.size(); ++i) {
+      sfx_instr c = instrs[i];  // memset-initialised: padding is zero
+      c.id = nullptr;
+      c.literal = nullptr;
+      put(&c, sizeof c);
+      k.append(instrs[i].id).push_back('\0');
+      put(literals[i].data(), literals[i].size() * sizeof(double));
+    }
+    put(outputs.data(), outputs.size() * sizeof(int32_t));
+    for (size_t p = 0; p < programs.size(); ++p) {
+      sfx_program sp = programs[p];
+      sp.members = sp.roots = nullptr;
+      sp.stmts = nullptr;
+      put(&sp, sizeof sp);
+      put(members[p].data(), members[p].size() * sizeof(int32_t));
+      put(roots[p].data(), roots[p].size() * sizeof(int32_t));
+      put(stmts[p].data(), stmts[p].size() * sizeof(sfx_stmt));
+    }
+    return k;
+  }
 };
+
+// Compiled kernels / modules by plan signature, least recently used evicted
+// beyond SFX_BINDING_CACHE entries (default 8; a cached module keeps its device
+// intermediates and host-path staging buffers; 0 = compile every call).
+// Entries are shared_ptrs: an evicted object lives until its last user returns.
+template <typename T>
+class Cache {
+ public:
+  explicit Cache(sfx_status (*destroy)(T*)) : destroy_(destroy) {
+    const char* e = std::getenv("SFX_BINDING_CACHE");
+    cap_ = e ? std::max(0, std::atoi(e)) : 8;
+  }
+  std::shared_ptr<T> get(const std::string& key, const std::function<T*()>& make) {
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = map_.find(key);
+    if (it != map_.end()) {
+      it->second.second = ++tick_;
+      return it->second.first;
+    }
+    auto destroy = destroy_;
+    std::shared_ptr<T> obj(make(), [destroy](T* p) { destroy(p); });
+    ++compiles_;
+    if (cap_ == 0) return obj;
+    if (map_.size() >= static_cast<size_t>(cap_)) {
+      auto lru = map_.begin();
+      for (auto j = map_.begin(); j != map_.end(); ++j)
+        if (j->second.second < lru->second.second) lru = j;
+      map_.erase(lru);
+    }
+    map_.emplace(key, std::make_pair(obj, ++tick_));
+    return obj;
+  }
+  long long compiles() {
+    std::lock_guard<std::mutex> lock(mu_);
+    return compiles_;
+  }
+
+ private:
+  sfx_status (*destroy_)(T*);
+  int cap_ = 8;
+  unsigned long long tick_ = 0;
+  long long compiles_ = 0;
+  std::map<std::string, std::pair<std::shared_ptr<T>, unsigned long long>> map_;
+  std::mutex mu_;
+};
+
+// Never destroyed (process exit reclaims device memory; destroying modules
+// after the CUDA context is gone would fail).
+Cache<sfx_kernel>& kernel_cache() {
+  static auto* c = new Cache<sfx_kernel>(&sfx_kernel_destroy);
+  return *c;
+}
+Cache<sfx_graph>& graph_cache() {
+  static auto* c = new Cache<sfx_graph>(&sfx_graph_destroy);
+  return *c;
+}
 
 const void* host_data(const TensorValue& v) {
   return v.shape.etype == ElementType::F32 ? static_cast<const void*>(v.f32.data())
@@ -145,15 +231,20 @@ sfx_compile_opts g_opts{};
 }  // namespace
 
 long long launches() { return sfx_launch_count(context()); }
+long long compiles() { return kernel_cache().compiles() + graph_cache().compiles(); }
 void set_strategy(int sfx_strategy) { g_opts.strategy = sfx_strategy; }
+void set_debug_checks(int level) { g_opts.debug_checks = level; }
 
 std::vector<TensorValue> run_program(const KernelProgram& program, const TensorGraph& graph,
                                      const std::map<InstrId, TensorValue>& externals) {
   sfx_ctx* ctx = context();
   Desc d(graph, {&program});
-  sfx_kernel* k = nullptr;
-  check(sfx_program_compile(ctx, &d.desc, 0, &g_opts, &k));
-  std::unique_ptr<sfx_kernel, decltype(&sfx_kernel_destroy)> guard(k, &sfx_kernel_destroy);
+  std::shared_ptr<sfx_kernel> kp = kernel_cache().get(d.signature(g_opts), [&] {
+    sfx_kernel* nk = nullptr;
+    check(sfx_program_compile(ctx, &d.desc, 0, &g_opts, &nk));
+    return nk;
+  });
+  sfx_kernel* k = kp.get();
   sfx_kernel_info info;
   check(sfx_kernel_get_info(k, &info));
   std::vector<int32_t> slots(info.n_inputs);
@@ -200,9 +291,12 @@ std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const T
   std::vector<const KernelProgram*> progs;
   for (const CompiledKernel& k : report.kernels) progs.push_back(&k.program);
   Desc d(graph, progs);
-  sfx_graph* g = nullptr;
-  check(sfx_graph_compile(ctx, &d.desc, &g_opts, &g));
-  std::unique_ptr<sfx_graph, decltype(&sfx_graph_destroy)> guard(g, &sfx_graph_destroy);
+  std::shared_ptr<sfx_graph> gp = graph_cache().get(d.signature(g_opts), [&] {
+    sfx_graph* ng = nullptr;
+    check(sfx_graph_compile(ctx, &d.desc, &g_opts, &ng));
+    return ng;
+  });
+  sfx_graph* g = gp.get();
   int32_t n = 0;
   std::vector<int32_t> params(graph.instructions().size());
   check(sfx_graph_param_instrs(g, params.data(), static_cast<int32_t>(params.size()), &n));

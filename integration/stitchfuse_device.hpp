@@ -35,7 +35,17 @@ std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const T
 // Number of kernels the device executor launched so far (plan-parity check).
 long long launches();
 
+// Number of plans compiled so far.  Compiled kernels / modules are cached by
+// plan signature (graph + program + options), so repeated run_program /
+// run_compiled calls on the same plan reuse them: no re-lowering, no NVRTC,
+// no module load, no device allocation.
+long long compiles();
+
 // Lowering tier for subsequent calls (SFX_STRATEGY_AUTO by default).
 void set_strategy(int sfx_strategy);
+
+// sfx_compile_opts.debug_checks for subsequent calls: 1 = the coverage check of
+// the reference executor (exec.cpp:393-410) around every launch.
+void set_debug_checks(int level);
 
 }  // namespace stitchfuse_device

@@ -13,6 +13,11 @@
 //        device-eligible fixtures runs and equals interpret
 //   device_parity shrink [--literal]
 //        test_exec.cpp:139-155: lowered smem limits (shrunk plans) keep outputs
+//   device_parity crit9 | crit7
+//        acceptance criteria 9 (50 fuse_dot executor runs, coverage-checked)
+//        and 7 (shrunk fuse_dot fixture), test_acceptance.cpp:276-391
+//   device_parity cache
+//        the binding's compiled-plan cache: one compile per plan signature
 // Prints one JSON line; exit 0 iff every eligible case passed.
 #include <cstdlib>
 #include <cstring>
@@ -293,6 +298,123 @@ int cmd_shrink(uint64_t seed, int count) {
   return finish("shrink", t, skipped);
 }
 
+// Acceptance criterion 9 (test_acceptance.cpp:375-391): 50 random fuse_dot
+// plans (rng 90001) executed with full coverage — here with the device
+// coverage check around every launch (debug_checks=1) — and, beyond the
+// reference's criterion, compared with its interpret.
+int cmd_crit9() {
+  Tally t;
+  int skipped = 0;
+  CostModelParams params;
+  std::mt19937_64 rng2(90001);
+  stitchfuse_device::set_debug_checks(1);
+  for (int i = 0; i < 50; ++i) {
+    TensorGraph g = testsupport::random_graph(rng2);
+    PipelineOptions options;
+    options.fuse_dot = true;
+    PerfLibrary lib;
+    CompileReport rep;
+    try {
+      rep = compile_graph(g, options, lib, params);
+    } catch (const std::exception& e) {
+      ++t.cases;
+      t.fail("graph " + std::to_string(i) + ": compile_graph: " + e.what());
+      continue;
+    }
+    auto inputs = testsupport::random_inputs(g, rng2);  // same rng order as the reference test
+    if (!eligible(g)) {
+      ++skipped;
+      continue;
+    }
+    run_case("graph " + std::to_string(i), g, rep, inputs, t);
+  }
+  stitchfuse_device::set_debug_checks(0);
+  return finish("criterion 9 (fuse_dot, coverage-checked)", t, skipped);
+}
+
+// Acceptance criterion 7's executor leg (test_acceptance.cpp:291-312): the
+// fuse_dot fixture planned under smem_limit 1024 (shrunk [Exponential.1,
+// Divide.1]) keeps Dot.1 values_close to interpret.
+int cmd_crit7() {
+  Tally t;
+  TensorGraph g = parse_graph(fixture_graphs().at("softmax_batchdot"));  // test_acceptance.cpp:29
+  PipelineOptions options;
+  options.fuse_dot = true;
+  options.smem_limit = 1024;
+  PerfLibrary lib;
+  CostModelParams params;
+  CompileReport rep = compile_graph(g, options, lib, params);
+  std::mt19937_64 rng2(70001);
+  auto inputs = testsupport::random_inputs(g, rng2);
+  ++t.cases;
+  try {
+    auto ref = interpret(g, inputs);
+    auto dev = stitchfuse_device::run_compiled(rep, g, inputs);
+    if (rep.kernels[0].smem.shrunk != std::vector<InstrId>{"Exponential.1", "Divide.1"}) t.fail("shrink order");
+    else if (!testsupport::values_close(dev.at("Dot.1"), ref.at("Dot.1"), 1e-5)) t.fail("Dot.1");
+    else ++t.passed;
+  } catch (const std::exception& e) {
+    t.fail(e.what());
+  }
+  return finish("criterion 7 (shrunk fuse_dot fixture)", t, 0);
+}
+
+// The binding caches compiled plans by signature: repeated run_compiled /
+// run_program calls on one plan compile once, launch every time, and return
+// the same values; a different plan compiles again.
+int cmd_cache() {
+  Tally t;
+  std::mt19937_64 rng(113);
+  testsupport::RandomGraphConfig cfg;
+  cfg.allow_library_calls = false;
+  TensorGraph g = testsupport::random_graph(rng, cfg);
+  TensorGraph g2 = testsupport::random_graph(rng, cfg);
+  PipelineOptions o;
+  PerfLibrary lib;
+  CostModelParams params;
+  CompileReport rep = compile_graph(g, o, lib, params);
+  CompileReport rep2 = compile_graph(g2, o, lib, params);
+  auto inputs = testsupport::random_inputs(g, rng);
+  auto inputs2 = testsupport::random_inputs(g2, rng);
+  auto ref = interpret(g, inputs);
+  auto check_round = [&](const std::string& what, long long want_compiles) {
+    ++t.cases;
+    long long c0 = stitchfuse_device::compiles(), l0 = stitchfuse_device::launches();
+    auto dev = stitchfuse_device::run_compiled(rep, g, inputs);
+    long long dc = stitchfuse_device::compiles() - c0, dl = stitchfuse_device::launches() - l0;
+    std::string why;
+    if (dc != want_compiles) t.fail(what + ": " + std::to_string(dc) + " compiles");
+    else if (dl != expected_launches(rep)) t.fail(what + ": " + std::to_string(dl) + " launches");
+    else if (!compare(g, ref, dev, inputs, &why)) t.fail(what + ": " + why);
+    else ++t.passed;
+  };
+  check_round("first run_compiled", 1);
+  check_round("second run_compiled", 0);
+  ++t.cases;
+  long long c0 = stitchfuse_device::compiles();
+  stitchfuse_device::run_compiled(rep2, g2, inputs2);
+  if (stitchfuse_device::compiles() - c0 == 1) ++t.passed;
+  else t.fail("a different plan must compile");
+  check_round("back to the first plan", 0);
+  // run_program: one group, twice
+  const KernelProgram& prog = rep.kernels.at(0).program;
+  std::map<InstrId, TensorValue> ext;
+  for (const InstrId& id : prog.comp.members)
+    for (const InstrId& op : g.at(id).operands)
+      if (!prog.comp.members.count(op)) ext[op] = ref.at(op);
+  for (int r = 0; r < 2; ++r) {
+    ++t.cases;
+    long long k0 = stitchfuse_device::compiles();
+    auto outs = stitchfuse_device::run_program(prog, g, ext);
+    bool ok = stitchfuse_device::compiles() - k0 == (r == 0 ? 1 : 0);
+    for (size_t k = 0; k < prog.comp.roots.size(); ++k)
+      ok = ok && testsupport::values_close(outs[k], ref.at(prog.comp.roots[k]), 1e-5);
+    if (ok) ++t.passed;
+    else t.fail("run_program round " + std::to_string(r));
+  }
+  return finish("binding cache", t, 0);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -308,6 +430,9 @@ int main(int argc, char** argv) {
     std::string cmd = pos.at(0);
     if (cmd == "random") return cmd_random(std::stoull(pos.at(1)), std::stoi(pos.at(2)), alt);
     if (cmd == "schedules") return cmd_schedules();
+    if (cmd == "crit9") return cmd_crit9();
+    if (cmd == "crit7") return cmd_crit7();
+    if (cmd == "cache") return cmd_cache();
     if (cmd == "shrink") return cmd_shrink(pos.size() > 1 ? std::stoull(pos[1]) : 7, pos.size() > 2 ? std::stoi(pos[2]) : 30);
     throw std::runtime_error("unknown command " + cmd);
   } catch (const std::exception& e) {

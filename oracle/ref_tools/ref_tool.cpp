@@ -7,12 +7,13 @@
 // oracle restatement and the device executor against them.  Nothing in the
 // product (paper_1811_05213_b200/) links or calls this.
 //
-//   ref_tool plan   <graph.json> [--fuse-dot] [--smem-limit N]      -> plan bundle JSON (stdout)
+//   ref_tool plan   <graph.json> [--fuse-dot] [--smem-limit N] [--footprint-limit N]
+//                                                                   -> plan bundle JSON (stdout)
 //   ref_tool random <seed> <count> <outdir> [--no-libcalls] [--fuse-dot-alternate]
 //                                                                   -> one bundle per graph
 //   ref_tool run    <bundle-or-graph.json> <seed> <lo> <hi> <out-prefix> [--compiled] [--no-interpret]
 //                                                                   -> <prefix>.interpret.bin / .compiled.bin
-//   ref_tool bench  <graph.json> <seed> <threads> <iters> [--interpret]
+//   ref_tool bench  <graph.json> <seed> <threads> <iters> [--interpret] [--footprint-limit N]
 //                                                                   -> JSON timing line
 #include <atomic>
 #include <chrono>
@@ -180,6 +181,7 @@ int cmd_plan(int argc, char** argv) {
   for (int i = 3; i < argc; ++i) {
     if (!std::strcmp(argv[i], "--fuse-dot")) o.fuse_dot = true;
     else if (!std::strcmp(argv[i], "--smem-limit") && i + 1 < argc) o.smem_limit = std::stoll(argv[++i]);
+    else if (!std::strcmp(argv[i], "--footprint-limit") && i + 1 < argc) o.footprint_limit = std::stoll(argv[++i]);
   }
   TensorGraph g = parse_graph(slurp(argv[2]));
   CompileReport r = compile(g, o);
@@ -260,14 +262,19 @@ int cmd_run(int argc, char** argv) {
 // single-threaded and reentrant); each thread compiles its own
 // plan and runs run_compiled (or interpret) `iters` times.
 int cmd_bench(int argc, char** argv) {
-  if (argc < 6) throw std::runtime_error("usage: bench <graph> <seed> <threads> <iters> [--interpret]");
+  if (argc < 6)
+    throw std::runtime_error("usage: bench <graph> <seed> <threads> <iters> [--interpret] [--footprint-limit N]");
   TensorGraph g = load_any(argv[2]);
   uint64_t seed = std::stoull(argv[3]);
   int threads = std::stoi(argv[4]);
   int iters = std::stoi(argv[5]);
-  bool use_interp = argc > 6 && !std::strcmp(argv[6], "--interpret");
-  auto inputs = gen_inputs(g, seed, -1.0f, 1.0f);
+  bool use_interp = false;
   PipelineOptions o;
+  for (int i = 6; i < argc; ++i) {
+    if (!std::strcmp(argv[i], "--interpret")) use_interp = true;
+    else if (!std::strcmp(argv[i], "--footprint-limit") && i + 1 < argc) o.footprint_limit = std::stoll(argv[++i]);
+  }
+  auto inputs = gen_inputs(g, seed, -1.0f, 1.0f);
   CompileReport r = compile(g, o);
   std::atomic<uint64_t> sink{0};
   auto t0 = std::chrono::steady_clock::now();
@@ -281,9 +288,11 @@ int cmd_bench(int argc, char** argv) {
     });
   for (auto& th : pool) th.join();
   double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  json groups = json::array();
+  for (const auto& k : r.kernels) groups.push_back(k.comp.fusion_root);
   json line = {{"seconds", s}, {"threads", threads}, {"iters", iters},
                {"executor", use_interp ? "interpret" : "run_compiled"},
-               {"fused_kernels", r.fused_kernels}};
+               {"fused_kernels", r.fused_kernels}, {"groups", groups}, {"footprint_limit", o.footprint_limit}};
   std::cout << line.dump() << "\n";
   return sink.load() > 0 ? 0 : 1;
 }

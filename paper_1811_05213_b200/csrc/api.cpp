@@ -127,7 +127,14 @@ struct sfx_kernel {
   sfx::KernelSource src;
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
+  // Workspace (cross-CTA tickets / partials; the kernels reset their tickets
+  // on exit).  Launches on one stream are ordered, so each stream gets its own
+  // workspace and launches on different streams never share one; `ws` is the
+  // kernel's default (cross-rank kernels, whose launches are ordered on every
+  // rank anyway, and launches captured outside sfx_graph_run).
   CUdeviceptr ws = 0;
+  std::mutex ws_mu;
+  std::map<CUstream, CUdeviceptr> stream_ws;
   uint64_t peer_off = 0;  // this kernel's region of the symmetric peer arena
   int regs = 0;
   int debug = 0;                    // sfx_compile_opts.debug_checks
@@ -175,6 +182,11 @@ uint64_t host_chunk_bytes() {
 
 struct sfx_graph {
   sfx_ctx* ctx = nullptr;
+  std::mutex run_mu;                 // one host thread enqueues at a time
+  // CUDA-graph replays: every captured pointer set owns its kernels'
+  // workspaces (replays of one exec are serialised by CUDA; different execs may
+  // run concurrently on different streams)
+  std::map<std::vector<uint64_t>, std::vector<CUdeviceptr>> captured_ws;
   sfx::Graph graph;
   std::vector<sfx_kernel*> kernels;  // per program: planned groups, then matmul barriers
   // host path: row / map kernels recompiled with the host-streaming gate code
@@ -296,6 +308,31 @@ void launch(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector
                                          ")");
 }
 
+// Workspaces prepared for a capture in progress on this thread (sfx_graph_run),
+// by kernel; null outside one.
+thread_local const std::map<const sfx_kernel*, CUdeviceptr>* t_capture_ws = nullptr;
+
+CUdeviceptr workspace_for(sfx_kernel* k, CUstream s) {
+  if (k->src.workspace_bytes <= 0) return 0;
+  if (t_capture_ws) {
+    auto it = t_capture_ws->find(k);
+    if (it != t_capture_ws->end()) return it->second;
+  }
+  if (k->src.peer_bytes > 0) return k->ws;  // cross-rank: one ordered sequence per rank
+  const sfx::Driver& d = sfx::driver();
+  CUstreamCaptureStatus cap = CU_STREAM_CAPTURE_STATUS_NONE;
+  sfx::check_cu(d.cuStreamIsCapturing(s, &cap), "cuStreamIsCapturing");
+  if (cap != CU_STREAM_CAPTURE_STATUS_NONE) return k->ws;  // captured by the caller: no allocation allowed
+  std::lock_guard<std::mutex> lock(k->ws_mu);
+  auto it = k->stream_ws.find(s);
+  if (it != k->stream_ws.end()) return it->second;
+  CUdeviceptr w = k->ctx->alloc(static_cast<uint64_t>(k->src.workspace_bytes));
+  // zeroed in stream order, ahead of this stream's first launch
+  sfx::check_cu(d.cuMemsetD32Async(w, 0, (k->src.workspace_bytes + 3) / 4, s), "cuMemsetD32Async");
+  k->stream_ws.emplace(s, w);
+  return w;
+}
+
 void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
                 const StreamArgs& sa, bool drop_last_cta) {
   if (in.size() != k->src.inputs.size())
@@ -317,7 +354,7 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
     if (p & 15) throw sfx::Error(SFX_ERR_INVALID, "output pointer not 16-byte aligned (" + k->src.entry + ")");
     vals.push_back(p);
   }
-  vals.push_back(k->ws);
+  vals.push_back(workspace_for(k, s));
   std::vector<void*> args(vals.size());
   for (size_t i = 0; i < vals.size(); ++i) args[i] = &vals[i];
   CUdeviceptr peers = k->ctx->peer_table;
@@ -378,6 +415,7 @@ void destroy_kernel(sfx_kernel* k) {
     k->ctx->bind();
     if (k->mod) sfx::driver().cuModuleUnload(k->mod);
     if (k->ws) k->ctx->release(k->ws);
+    for (auto& [st, w] : k->stream_ws) k->ctx->release(w);
   } catch (...) {
   }
   delete k;
@@ -846,6 +884,7 @@ sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params,
       throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(G->params.size()) + " params");
     if (n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
       throw sfx::Error(SFX_ERR_INVALID, "expected " + std::to_string(G->graph.outputs.size()) + " outputs");
+    std::lock_guard<std::mutex> lock(G->run_mu);
     G->ctx->bind();
     CUstream s = static_cast<CUstream>(stream);
     const sfx::Driver& d = sfx::driver();
@@ -859,13 +898,29 @@ sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params,
     auto it = G->captured.find(key);
     if (it == G->captured.end()) {
       int64_t before = G->ctx->launches.load();
+      // this capture's own workspaces, allocated and zeroed before capturing
+      std::map<const sfx_kernel*, CUdeviceptr> cws;
+      std::vector<CUdeviceptr>& owned_ws = G->captured_ws[key];
+      for (sfx_kernel* k : G->kernels)
+        if (k->src.workspace_bytes > 0 && k->src.peer_bytes == 0) {
+          CUdeviceptr w = G->ctx->alloc(static_cast<uint64_t>(k->src.workspace_bytes));
+          owned_ws.push_back(w);
+          sfx::check_cu(d.cuMemsetD32Async(w, 0, (k->src.workspace_bytes + 3) / 4, s), "cuMemsetD32Async");
+          cws[k] = w;
+        }
+      sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
       sfx::check_cu(d.cuStreamBeginCapture(s, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "cuStreamBeginCapture");
       CUgraph graph = nullptr;
+      t_capture_ws = &cws;
       try {
         graph_enqueue(G, params, outputs, s);
+        t_capture_ws = nullptr;
       } catch (...) {
+        t_capture_ws = nullptr;
         d.cuStreamEndCapture(s, &graph);
         if (graph) d.cuGraphDestroy(graph);
+        for (CUdeviceptr w : owned_ws) G->ctx->release(w);
+        G->captured_ws.erase(key);
         throw;
       }
       sfx::check_cu(d.cuStreamEndCapture(s, &graph), "cuStreamEndCapture");
@@ -886,6 +941,7 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
     if (n_params != static_cast<int32_t>(G->params.size()) ||
         n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
       throw sfx::Error(SFX_ERR_INVALID, "param/output count mismatch");
+    std::lock_guard<std::mutex> lock(G->run_mu);
     G->ctx->bind();
     const sfx::Driver& d = sfx::driver();
     CUstream s = static_cast<CUstream>(stream);
@@ -1094,6 +1150,8 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
     } catch (...) {
     }
     if (G->stream_flags) G->ctx->release(G->stream_flags);
+    for (auto& [key, ws] : G->captured_ws)
+      for (CUdeviceptr w : ws) G->ctx->release(w);
     for (sfx_kernel* k : G->kernels) destroy_kernel(k);
     for (sfx_kernel* k : G->host_kernels) destroy_kernel(k);
     for (auto& [n, p] : G->owned) G->ctx->release(p);

@@ -380,6 +380,9 @@ DEVICE_PARITY = os.path.join(T.ROOT, "oracle", "_ref", "device_parity")
     ["random", "113", "40", "--fuse-dot-alternate", "--literal"],
     ["schedules"], ["schedules", "--literal"],                  # test_exec.cpp:108-137
     ["shrink"],                                                  # test_exec.cpp:139-155
+    ["crit9"],                  # acceptance criterion 9: 50 fuse_dot runs, coverage-checked
+    ["crit7"],                  # acceptance criterion 7: shrunk fuse_dot fixture
+    ["cache"],                  # the binding compiles each plan once (signature cache)
 ])
 def test_reference_suites_through_device_binding(args):
     """The reference's own test loops (its random graphs, its inputs, its
@@ -433,3 +436,45 @@ def test_colbc_cuda_graph_replay(ctx, name):
     finally:
         cg.close()
     assert not _check(g, got, inputs, strict=True)
+
+
+@pytest.mark.parametrize("cuda_graph", [False, True])
+def test_concurrent_launches_on_four_streams(ctx, cuda_graph):
+    """One compiled C3 graph (the column kernel owns a cross-CTA workspace:
+    tickets + partials) launched on 4 streams at once with 4 buffer sets: each
+    stream (and each captured CUDA graph) has its own workspace, so every
+    concurrent result is bit-identical to a serial launch on the same inputs,
+    which matches the fp64 oracle."""
+    import torch
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, "C3.full.json"))
+    cg = H.CompiledGraph(ctx, g, rep)
+    try:
+        dev = torch.device("cuda", 0)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(77)
+        sets = []
+        for _ in range(4):
+            ins = [torch.rand(g.at(p).shape, generator=gen, device=dev) * 2 - 1 for p in cg.param_ids]
+            outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+            sets.append((ins, outs))
+        ptrs = lambda st: ([t.data_ptr() for t in st[0]], [t.data_ptr() for t in st[1]])  # noqa: E731
+        serial = []
+        s0 = torch.cuda.Stream()
+        for st in sets:
+            cg.run(*ptrs(st), stream=s0.cuda_stream)
+            s0.synchronize()
+            serial.append(st[1][0].clone())
+        want = T.interpret(g, {p: t.cpu().numpy() for p, t in zip(cg.param_ids, sets[0][0])}, 1)["db"]
+        assert T.strict_close(serial[0].cpu().numpy(), want)
+        streams = [torch.cuda.Stream() for _ in range(4)]
+        for _ in range(5):
+            for st in sets:
+                st[1][0].fill_(float("nan"))
+            torch.cuda.synchronize()
+            for s, st in zip(streams, sets):
+                cg.run(*ptrs(st), stream=s.cuda_stream, cuda_graph=cuda_graph)
+            torch.cuda.synchronize()
+            for st, ref in zip(sets, serial):
+                assert torch.equal(st[1][0], ref)
+    finally:
+        cg.close()

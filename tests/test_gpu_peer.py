@@ -3,10 +3,10 @@
 The batch-sharded path's one exchange is a column reduction over the batch
 (C3's db).  With cross_rank=1 the column kernel itself pushes each column
 tile's partial to every rank's peer arena and folds the ranks in rank order
-inside the same launch (no NCCL call).  The box has one GPU, so the two ranks
-here are two processes sharing cuda:0 through CUDA IPC — the same
-cuIpcOpenMemHandle path that maps a peer GPU's arena over NVLink on a
-multi-GPU node.  Handles are exchanged over gloo (127.0.0.1).
+inside the same launch (no NCCL call).  Each rank runs on its own GPU when the
+box has enough of them (rank % device_count); on a 1-GPU box the ranks are
+processes sharing cuda:0 through CUDA IPC — the same cuIpcOpenMemHandle path
+that maps a peer GPU's arena over NVLink on a multi-GPU node.  Handles are exchanged over gloo (127.0.0.1).
 
 Checks: every rank's db equals the fp64 restatement of the UNSHARDED graph
 (rows of all ranks) within the north_star bounds and is bit-identical across
@@ -52,7 +52,12 @@ def _worker(rank, ws, port, case, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     try:
-        ctx = H.Context(0)
+        import torch
+        # distinct GPUs when the box has them (NVLink peer mapping), else both
+        # ranks share cuda:0 through the same IPC path
+        dev_i = rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_i)
+        ctx = H.Context(dev_i)
         ctx.peer_init(rank, ws, H.torch_all_gather, nbytes=1 << 22)
         out = []
         if case in ("C3", "C3b"):
@@ -68,7 +73,7 @@ def _worker(rank, ws, port, case, q):
             assert ctx.launch_count() - before == 4 * cg.launches_per_run
             # device-resident runs with CUDA-graph replay on one buffer set
             import torch
-            dev = torch.device("cuda", 0)
+            dev = torch.device("cuda", dev_i)
             ins = [torch.from_numpy(_shard(200, i, n, c, rank)).to(dev) for i in range(2)]
             outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
             st = torch.cuda.Stream(device=dev)
@@ -86,7 +91,7 @@ def _worker(rank, ws, port, case, q):
                 inputs = _bn_inputs(300 + it, rank)
                 out.append(cg.run_host(inputs))
             import torch
-            dev = torch.device("cuda", 0)
+            dev = torch.device("cuda", dev_i)
             inputs = _bn_inputs(400, rank)
             ins = [torch.from_numpy(inputs[p]).to(dev) for p in cg.param_ids]
             outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
@@ -102,7 +107,7 @@ def _worker(rank, ws, port, case, q):
             cg = H.CompiledGraph(ctx, g, rep, cross_rank=1)
             assert sorted(k.info["strategy"] for k in cg.kernels) == ["col", "colbc"]
             import torch
-            dev = torch.device("cuda", 0)
+            dev = torch.device("cuda", dev_i)
             for it in range(2):
                 inputs = _two_inputs(500 + it, rank)
                 out.append(cg.run_host(inputs))

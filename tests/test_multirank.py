@@ -108,3 +108,37 @@ def test_bench_load_rounds_agree_across_ranks():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert [r[1] for r in res] == [7, 7] and [r[2] for r in res] == [7, 7]
+
+
+def test_bench_plan_per_rank():
+    """Strong sharding: rank r of n runs the reference's shard plan; weak
+    scaling and n = 1 run the global plan; shard counts without a plan fail."""
+    import bench
+    assert bench.plan_path("C5", 1).endswith("C5.full.json")
+    assert bench.plan_path("C5", 8).endswith("C5.shard8.json")
+    assert bench.plan_path("C5", 8, "weak").endswith("C5.full.json")
+    with pytest.raises(SystemExit):
+        bench.plan_path("C5", 3)
+    c = bench.config_obj("C5", 8)
+    assert c["shard"] == {"dim": "B", "ranks": 8, "per_rank": {"B": 8, "S": 512}, "global": {"B": 64, "S": 512}}
+    assert "column kernel" in bench.config_obj("C3", 4)["parallelism"]
+
+
+def test_bench_gpus_mismatch_and_self_launch():
+    """--gpus N must agree with WORLD_SIZE; without torchrun, --gpus N
+    re-launches bench.py as N ranks (here the CPU reference arm: rank 0 prints
+    the line with n_gpus = N, the other ranks exit 0)."""
+    import json
+    import subprocess
+    import sys
+    bench = os.path.join(T.ROOT, "bench.py")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, bench, "--gpus", "2", "--impl", "reference", "--config", "C1"],
+                       env=dict(env, WORLD_SIZE="1"), capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
+    r = subprocess.run([sys.executable, bench, "--gpus", "2", "--impl", "reference", "--config", "C1",
+                        "--steps", "1", "--warmup", "3"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert lines[0]["config"]["shard"]["per_rank"] == {"R": 4096, "C": 1024}

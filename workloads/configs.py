@@ -310,3 +310,20 @@ def build(name: str, **sizes) -> dict:
 
 def dumps(doc: dict) -> str:
     return json.dumps(doc, indent=1) + "\n"
+
+
+# Batch sharding: the dimension each config is split along
+# across ranks, and the per-rank sizes of an n-way shard.  Rank r owns
+# indices [r*N/n, (r+1)*N/n) of that dimension; every other size is unchanged.
+SHARD_DIM = {"C1": "R", "C2": "B", "C3": "N", "C3b": "N", "C4": "B", "C4b": "B", "C4t": "B", "C5": "B", "C5L": "B"}
+SHARD_COUNTS = (2, 4, 8)
+
+
+def shard_sizes(name: str, n: int) -> dict:
+    sizes = dict(FULL[name])
+    d = SHARD_DIM[name]
+    if sizes[d] % n:
+        raise ValueError(f"{name}: {d}={sizes[d]} does not split {n} ways")
+    sizes[d] //= n
+    return sizes
+

@@ -48,6 +48,25 @@ def main():
                 f.write("\n")
             print(f"{path}: fused={bundle['fused_kernels']} baseline={bundle['baseline_kernels']}"
                   f" groups={[k['fusion_root'] for k in bundle['kernels']]}")
+    # one rank's shard of each named config at 2/4/8 GPUs, planned by the
+    # reference on the shard graph (the 64 MiB footprint cap makes membership
+    # size-dependent, fusion.cpp:69-85: tests/test_shards.py checks it equals
+    # the global plan's)
+    for name in configs.SHARD_DIM:
+        if name == "C5L":
+            continue
+        for n in configs.SHARD_COUNTS:
+            sizes = configs.shard_sizes(name, n)
+            bundle = plan_bundle(configs.build(name, **sizes))
+            for k in bundle["kernels"]:
+                k.pop("dump", None)
+            bundle["workload"] = {"name": name, "size": f"shard{n}", "sizes": sizes, "shards": n,
+                                  "shard_dim": configs.SHARD_DIM[name], "global_sizes": configs.FULL[name]}
+            path = os.path.join(outdir, f"{name}.shard{n}.json")
+            with open(path, "w") as f:
+                json.dump(bundle, f, separators=(",", ":"))
+                f.write("\n")
+            print(f"{path}: fused={bundle['fused_kernels']} groups={[k['fusion_root'] for k in bundle['kernels']]}")
 
 
 if __name__ == "__main__":
