@@ -428,6 +428,7 @@ def run_ours(args):
         sets.append(([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], ins, outs))
     nsets = len(sets)
     streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(inflight - 1)]
+    torch.cuda.synchronize(dev)  # inputs were written on torch's stream; ours do not wait for it
 
     def step(i):
         s = streams[i % inflight]

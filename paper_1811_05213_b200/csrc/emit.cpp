@@ -211,7 +211,13 @@ std::string Emitter::load(int node, const std::vector<Ix>& comps) {
     const Tile& t = tt->second;
     std::string B = t.mb ? imod(comps[t.jb].e, t.mb) : comps[t.jb].e;
     std::string A = t.ma ? imod(idiv(comps[t.ja].e, t.sa), t.ma) : comps[t.ja].e;
-    std::string addr = t.arr + "[" + B + " - " + t.b0 + "][" + A + " - " + t.a0 + "]";
+    std::string addr;
+    if (t.swz) {
+      const std::string ra = ivar("(int)(" + A + " - " + t.a0 + ")"), rb = ivar("(int)(" + B + " - " + t.b0 + ")");
+      addr = t.arr + "[" + ra + " * 64 + ((((" + rb + ") >> 2) ^ ((" + ra + " >> 2) & 7)) << 2) + ((" + rb + ") & 3)]";
+    } else {
+      addr = t.arr + "[" + B + " - " + t.b0 + "][" + A + " - " + t.a0 + "]";
+    }
     std::string key = "tld:" + addr;
     std::string v = find(key);
     if (v.empty()) {

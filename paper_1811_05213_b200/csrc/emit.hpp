@@ -64,10 +64,15 @@ class Emitter {
   // externals staged as a transposed shared-memory tile: element at input comps
   // c lives at arr[B - b0][A - a0], B = c[jb] (or c[jb] % mb when that dim
   // merges several root axes), A = c[ja] (or c[ja] / sa % ma)
+  // swz: the vectorised tile instead — a flat [64 a][64 b] array, rows along
+  // the root's innermost axis a, 16-byte chunks of b XOR-swizzled by (a/4)&7:
+  // element (a, b) at arr[a*64 + (((b>>2) ^ ((a>>2)&7))<<2) + (b&3)], written
+  // with 128-bit stores and read conflict-free by 8 a-rows x 4 b per warp
   struct Tile {
     std::string arr, b0, a0;
     int jb = 0, ja = 0;
     int64_t mb = 0, sa = 1, ma = 0;
+    bool swz = false;
   };
   std::map<int, Tile> tiled;
   // Strategy hook for member nodes: return a variable name to use instead of

@@ -94,6 +94,7 @@ struct TilePlan {
 bool analyze_tiled(const Ctx& c, TilePlan* tp);
 KernelSource lower_map(const Ctx& c, const sfx_compile_opts& o);
 KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp, const sfx_compile_opts& o);
+KernelSource lower_map_tiled_v4(const Ctx& c, const TilePlan& tp, const sfx_compile_opts& o);
 
 // ---- row templates (lower_row.cpp) ----
 int row_tpr(int64_t C, int V, int streams = 1);

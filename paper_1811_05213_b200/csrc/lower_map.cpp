@@ -269,6 +269,142 @@ bool analyze_tiled(const Ctx& c, TilePlan* tp) {
   return !tp->inputs.empty();
 }
 
+// The vectorised tiled transpose: 64 x 64 tiles over root axes (a = root
+// innermost, b = the tiled inputs' innermost), 256 threads.
+//   load:    each thread LDG.128s 4 consecutive b of one a-row (16 threads per
+//            row, 4 passes) and STS.128s them into the row's XOR-swizzled
+//            16-byte chunk (conflict-free: 8 threads of a phase hit 8 chunks);
+//   compute: a warp covers 8 a-vectors (32 consecutive a) x 4 b; each thread
+//            reads its 4 a-values (4 LDS.32, the swizzle puts the warp's 8 rows
+//            x 4 b on 32 distinct banks), evaluates the roots for 4 lanes and
+//            STG.128s them — 4 full 128-byte lines per warp store.
+KernelSource lower_map_tiled_v4(const Ctx& c, const TilePlan& tp, const sfx_compile_opts& o) {
+  (void)o;
+  KernelSource ks;
+  ks.strategy = "map";
+  ks.entry = "sfx_mapt_" + c.name;
+  fill_common(c, ks);
+  const std::vector<int64_t>& dims = c.g.nodes[c.p.roots[0]].dims;
+  const int n = static_cast<int>(dims.size());
+  const int a = tp.a, b = tp.b;
+  const int64_t na = dims[a], nb = dims[b];
+  const int TT = 64;
+  const int64_t nta = (na + TT - 1) / TT, ntb = (nb + TT - 1) / TT;
+  std::vector<int64_t> rest_dims;
+  std::vector<int> rest_axes;
+  for (int i = 0; i < n; ++i)
+    if (i != a && i != b) rest_dims.push_back(dims[i]), rest_axes.push_back(i);
+  const int64_t nrest = prod(rest_dims, 0, rest_dims.size());
+  Emitter em(c.g, c.p, 4, c.wide);
+  std::string sig = signature(c, em, ks.entry, 256);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("const int tid = threadIdx.x;");
+  body.line(it + " tix = blockIdx.x;");
+  body.line("const " + it + " a0 = (tix % " + fmt_i(nta) + ") * " + std::to_string(TT) + "; tix /= " + fmt_i(nta) + ";");
+  body.line("const " + it + " b0 = (tix % " + fmt_i(ntb) + ") * " + std::to_string(TT) + "; tix /= " + fmt_i(ntb) + ";");
+  body.line("const " + it + " rest = tix;");
+  std::vector<Ix> rest = em.from_linear(em.uni("rest"), rest_dims);
+  int ti = 0;
+  for (auto& [e, tile] : tp.inputs) {
+    const Node& en = c.g.nodes[e];
+    Emitter::Tile t = tile;
+    t.arr = "tile" + std::to_string(ti++);
+    t.b0 = "b0";
+    t.a0 = "a0";
+    t.swz = true;
+    body.line(std::string("__shared__ __align__(16) ") + ctype(en.dtype) + " " + t.arr + "[" + std::to_string(TT * TT) +
+              "];");
+    em.tiled[e] = t;
+  }
+  // load phase: thread -> (a-row tid/16 + 16*pass, b-vector tid%16)
+  body.line("const int sx_lra = tid >> 4, sx_lb4 = (tid & 15) << 2;");
+  for (int pass = 0; pass < TT / 16; ++pass) {
+    body.line("{");
+    body.indent++;
+    em.push();
+    const std::string ra = em.fresh("ra"), av = em.fresh("la"), bv = em.fresh("lb");
+    body.line("const int " + ra + " = sx_lra + " + std::to_string(16 * pass) + ";");
+    body.line("const " + it + " " + av + " = a0 + " + ra + ";");
+    body.line("const " + it + " " + bv + " = b0 + sx_lb4;");
+    body.line("if (" + av + " < " + fmt_i(na) + " && " + bv + " < " + fmt_i(nb) + ") {");
+    body.indent++;
+    std::vector<Ix> rc(n);
+    rc[a] = em.uni(av);
+    rc[b] = em.uni(bv);
+    for (size_t k = 0; k < rest_axes.size(); ++k) rc[rest_axes[k]] = rest[k];
+    for (auto& [e, tile] : tp.inputs) {
+      const Node& en = c.g.nodes[e];
+      const Labels& lab = tp.labels.at(e);
+      std::vector<Ix> ic(en.rank());
+      for (int d = 0; d < en.rank(); ++d) {
+        std::string v = "0";
+        for (auto& [axis, ext] : lab[d]) v = Emitter::iadd(Emitter::imul(v, ext), rc[axis].e);
+        ic[d] = em.uni(em.ivar(v));
+      }
+      Ix L = em.linearize(ic, en.dims);
+      const std::string q = em.fresh("q");
+      const char* vt = en.dtype == SFX_F32 ? "sfx_f4" : "sfx_i4";
+      body.line(std::string("const ") + vt + " " + q + " = sfx_ld4s(" + em.input_ptr.at(e) + " + " + L.e + ");");
+      body.line("*reinterpret_cast<" + std::string(vt) + "*>(&" + em.tiled[e].arr + "[" + ra + " * 64 + (((sx_lb4 >> 2) ^ ((" +
+                ra + " >> 2) & 7)) << 2)]) = " + q + ";");
+    }
+    body.indent--;
+    body.line("}");
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  body.line("__syncthreads();");
+  // compute phase: warp w covers a-half (w & 1), b-group (w >> 1); lane l:
+  // a-vector l & 7, b offset l >> 3
+  body.line("const int sx_cw = tid >> 5, sx_cl = tid & 31;");
+  body.line("const int sx_ca4 = ((sx_cw & 1) << 5) + ((sx_cl & 7) << 2), sx_cbo = ((sx_cw >> 1) << 2) + (sx_cl >> 3);");
+  for (int pass = 0; pass < TT / 16; ++pass) {
+    body.line("{");
+    body.indent++;
+    em.push();
+    const std::string av = em.fresh("ca"), bv = em.fresh("cb");
+    body.line("const " + it + " " + av + " = a0 + sx_ca4;");
+    body.line("const " + it + " " + bv + " = b0 + sx_cbo + " + std::to_string(16 * pass) + ";");
+    body.line("if (" + av + " < " + fmt_i(na) + " && " + bv + " < " + fmt_i(nb) + ") {");
+    body.indent++;
+    std::vector<std::vector<std::string>> vals(c.p.roots.size(), std::vector<std::string>(4));
+    std::string base;
+    for (int lane = 0; lane < 4; ++lane) {
+      em.lane = lane;
+      std::vector<Ix> rc(n);
+      rc[a] = em.lane_plus(av);
+      rc[b] = em.uni(bv);
+      for (size_t k = 0; k < rest_axes.size(); ++k) rc[rest_axes[k]] = rest[k];
+      for (size_t r = 0; r < c.p.roots.size(); ++r) vals[r][lane] = em.value(c.p.roots[r], rc);
+      if (lane == 0) {
+        Ix L = em.linearize(rc, dims);
+        if (L.kind != IX_PLUS) throw Error(SFX_ERR_INVALID, "internal: tiled root store is not lane-contiguous");
+        base = L.base;
+      }
+    }
+    em.lane = 0;
+    for (size_t r = 0; r < c.p.roots.size(); ++r)
+      body.line("sfx_st4(out" + std::to_string(root_slot(c, c.p.roots[r])) + " + " + base + ", " + vals[r][0] + ", " +
+                vals[r][1] + ", " + vals[r][2] + ", " + vals[r][3] + ");");
+    body.indent--;
+    body.line("}");
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  ks.code = assemble(sig, body);
+  ks.block = 256;
+  ks.grid_x = nta * ntb * nrest;
+  ks.vector_width = 4;
+  ks.note = "kLoop with " + std::to_string(tp.inputs.size()) + " smem-tiled transposed input(s), tile 64x64 over root "
+            "axes (" + std::to_string(a) + "," + std::to_string(b) + "), 128-bit global loads/stores, XOR-swizzled "
+            "16-byte chunks";
+  return ks;
+}
+
 KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "map";
@@ -282,6 +418,15 @@ KernelSource lower_map_tiled(const Ctx& c, const TilePlan& tp, const sfx_compile
   // flight (32: 4, latency-bound at 4.5 TB/s on C4t); items_per_thread=1
   // selects 32 for A/B
   const int TT = o.items_per_thread == 1 ? 32 : 64;
+  // 128-bit path: both tile axes split into 4-vectors, every tiled input's
+  // b-run contiguous and 16-byte aligned (its innermost index is b, or b mod a
+  // multiple of 4)
+  bool vec = TT == 64 && na % 4 == 0 && nb % 4 == 0 && o.row_pipeline != 1;  // row_pipeline=1: scalar tile (A/B)
+  for (auto& [e, tile] : tp.inputs) {
+    (void)e;
+    if (tile.mb != 0 && tile.mb % 4 != 0) vec = false;
+  }
+  if (vec) return lower_map_tiled_v4(c, tp, o);
   const int64_t nta = (na + TT - 1) / TT, ntb = (nb + TT - 1) / TT;
   std::vector<int64_t> rest_dims;
   std::vector<int> rest_axes;

@@ -82,6 +82,19 @@ EXTRA = {
         {"id": "gb", "op": "broadcast", "operands": ["g"], "shape": [80, 98304], "broadcast_dim_map": [1]},
         {"id": "n", "op": "mul", "operands": ["x", "rb"], "shape": [80, 98304]},
         {"id": "y", "op": "mul", "operands": ["n", "gb"], "shape": [80, 98304]}], "outputs": ["y"]},
+    # innermost-moving transposes with ragged 64x64 tiles: the 128-bit swizzled
+    # tile (both axes multiples of 4) and the scalar tile (odd extents)
+    "tr_8x300x140": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [8, 300, 140]},
+        {"id": "b", "op": "parameter", "shape": [140]},
+        {"id": "bb", "op": "broadcast", "operands": ["b"], "shape": [8, 300, 140], "broadcast_dim_map": [2]},
+        {"id": "xb", "op": "add", "operands": ["x", "bb"], "shape": [8, 300, 140]},
+        {"id": "xt", "op": "transpose", "operands": ["xb"], "shape": [8, 140, 300], "permutation": [0, 2, 1]},
+        {"id": "y", "op": "scale", "operands": ["xt"], "shape": [8, 140, 300], "scalar": 0.125}], "outputs": ["y"]},
+    "tr_8x301x141": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [8, 301, 141]},
+        {"id": "xt", "op": "transpose", "operands": ["x"], "shape": [8, 141, 301], "permutation": [0, 2, 1]},
+        {"id": "y", "op": "exp", "operands": ["xt"], "shape": [8, 141, 301]}], "outputs": ["y"]},
     # column statistics broadcast back (batch-norm): the colbc template
     "bn_4096x256": bn_graph([4096, 256], [0]),
     "bn_mid_8x512x64": bn_graph([8, 512, 64], [1]),

@@ -1,0 +1,102 @@
+"""stitchfuse-device: the reference CLI's `run` command (reference
+proj/tools/stitchfuse.cpp:52-88, 122-171, 231-261) with the device executor,
+built by oracle/Makefile against the reference library (its own CLI needs
+CLI11, absent here).  The graph is planned by the reference's compile_graph.
+
+CPU: flag handling and exit codes (0 ok, 1 user error, 2 internal error /
+mismatch) through `--host` (the reference executor in the same binary).
+GPU: for the reference's fixtures and the configs (small sizes), the device
+run prints the same lines as the reference executor — output ids, shapes,
+checksums to the CLI's 6 significant digits — passes --compare-reference, and
+exits 0; --fuse-dot and --smem-limit reach the planner."""
+
+import json
+import os
+import subprocess
+
+import pytest
+
+import sfx_testlib as T
+from workloads import configs
+
+CLI = os.path.join(T.ROOT, "oracle", "_ref", "stitchfuse-device")
+FIX = os.path.join(T.GOLDEN, "fixtures")
+pytestmark = pytest.mark.skipif(not os.path.exists(CLI), reason="stitchfuse-device not built (needs /root/reference)")
+
+
+def _write(tmp_path, name, doc):
+    p = tmp_path / name
+    p.write_text(doc if isinstance(doc, str) else json.dumps(doc))
+    return str(p)
+
+
+def _inputs_for(graph_path, tmp_path, seed0=100):
+    g = json.load(open(graph_path))
+    spec = {}
+    for i, ins in enumerate(x for x in g["instructions"] if x["op"] == "parameter"):
+        s = {"shape": ins["shape"], "random_seed": seed0 + i}
+        if ins.get("dtype") == "i32":
+            s["dtype"] = "i32"
+        spec[ins["id"]] = s
+    return _write(tmp_path, "inputs.json", spec)
+
+
+def _run(*args):
+    return subprocess.run([CLI] + list(args), capture_output=True, text=True, timeout=600)
+
+
+def test_exit_codes_and_user_errors(tmp_path):
+    graph = os.path.join(FIX, "elementwise_chain.json")
+    inp = _inputs_for(graph, tmp_path)
+    r = _run("run", graph, "--inputs", inp, "--compare-reference", "--host")
+    assert r.returncode == 0 and r.stdout.strip().endswith("reference check: PASS"), r.stderr
+    assert _run("run", graph).returncode == 1                                   # --inputs required
+    assert _run("run", str(tmp_path / "missing.json"), "--inputs", inp).returncode == 1
+    assert _run("frobnicate", graph, "--inputs", inp).returncode == 1
+    assert _run("run", graph, "--inputs", inp, "--smem-limit", "abc").returncode == 1
+    bad = _write(tmp_path, "bad.json", {"nope": {"shape": [2]}})
+    r = _run("run", graph, "--inputs", bad, "--host")
+    assert r.returncode == 1 and "unknown input id nope" in r.stderr
+    short = _write(tmp_path, "short.json", {"Param.0": {"shape": [4, 8, 16], "data": [1.0, 2.0]}})
+    assert _run("run", graph, "--inputs", short, "--host").returncode == 1      # data size mismatch
+    empty = _write(tmp_path, "empty.json", {})
+    r = _run("run", graph, "--inputs", empty, "--host")
+    assert r.returncode == 2 and "internal error" in r.stderr                  # missing parameter value
+
+
+def _cases():
+    out = [(os.path.join(FIX, f), []) for f in sorted(os.listdir(FIX)) if f != "libcall_mix.json"]
+    out.append((os.path.join(FIX, "softmax_batchdot.json"), ["--fuse-dot"]))
+    out.append((os.path.join(FIX, "softmax_batchdot.json"), ["--fuse-dot", "--smem-limit", "1024"]))
+    out.append((os.path.join(FIX, "libcall_mix.json"), []))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph,flags", _cases(), ids=lambda v: os.path.basename(v) if isinstance(v, str) else "+".join(v))
+def test_device_run_matches_reference_cli_fixtures(tmp_path, graph, flags):
+    inp = _inputs_for(graph, tmp_path)
+    dev = _run(*flags, "run", graph, "--inputs", inp, "--compare-reference")
+    ref = _run(*flags, "run", graph, "--inputs", inp, "--compare-reference", "--host")
+    assert ref.returncode == 0, ref.stderr
+    assert dev.returncode == ref.returncode, dev.stderr
+    assert dev.stdout == ref.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t", "C5"])
+def test_device_run_matches_reference_cli_configs(tmp_path, name):
+    graph = _write(tmp_path, "g.json", configs.dumps(configs.build(name, **configs.SMALL[name])))
+    inp = _inputs_for(graph, tmp_path)
+    dev = _run("run", graph, "--inputs", inp, "--compare-reference", "--seed", "3")
+    ref = _run("run", graph, "--inputs", inp, "--compare-reference", "--seed", "3", "--host")
+    assert ref.returncode == 0 and dev.returncode == 0, (dev.stderr, ref.stderr)
+    dl, rl = dev.stdout.splitlines(), ref.stdout.splitlines()
+    assert len(dl) == len(rl) and dl[-1] == rl[-1] == "reference check: PASS"
+    for d, r in zip(dl[:-1], rl[:-1]):
+        di, dshape, dsum = d.split()
+        ri, rshape, rsum = r.split()
+        assert (di, dshape) == (ri, rshape)
+        a, b = float(dsum.split("=")[1]), float(rsum.split("=")[1])
+        # checksums print with 6 significant digits; reductions may differ in the last one
+        assert a == b or abs(a - b) <= 2e-5 * max(1.0, abs(b)), (d, r)

@@ -133,3 +133,16 @@ def test_cross_rank_refuses_matmul_over_the_batch():
     brep = H.CompileReport.from_bundle({"graph": bdoc, "kernels": [], "unfused": ["s"], "fused_kernels": 1,
                                        "baseline_kernels": 1, "fusion_ratio": 1.0})
     assert H.codegen_barrier(bg, brep, 0, cross_rank=1)[2].startswith("dot")
+
+
+def test_tiled_transpose_is_vectorised():
+    """C4t's innermost-moving transpose: 128-bit global loads (LDG.128) into an
+    XOR-swizzled tile (STS.128), 128-bit streaming stores (STG.128); the only
+    scalar global loads left are the broadcast bias's.  Odd extents keep the
+    scalar [64][65] tile."""
+    src, cubin, note = _note(os.path.join(T.PLANS, "C4t.full.json"))
+    assert "XOR-swizzled" in note and src.count("= sfx_ld4s(in") == 4
+    sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+    assert sass.count("LDG.E.NA.128") == 4 and sass.count("STS.128") == 4 and sass.count("STG.E.EF.128") == 4
+    _, _, note = _note(os.path.join(EXTRA, "tr_8x301x141.json"))
+    assert "smem-tiled" in note and "XOR" not in note
