@@ -197,10 +197,13 @@ def test_parse_graph_lowers_mean_like_the_reference():
 
 def test_innermost_moving_transpose_uses_smem_tiles():
     """C4t (key transpose [B,S,H,D]->[B,H,D,S]) moves the innermost dimension:
-    the map template stages it through a padded 32x33 shared-memory tile."""
+    the map template stages it through a 64x64 shared-memory tile (XOR-swizzled
+    128-bit rows here; the padded [64][65] scalar tile for odd extents)."""
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C4t.full.json"))
     src, cubin, note = H.codegen(g, rep.kernels[0].program)
-    assert "smem-tiled" in note and "[64][65]" in src
+    assert "smem-tiled" in note and "tile0[4096]" in src
+    _, _, note1 = H.codegen(g, rep.kernels[0].program, row_pipeline=1)  # scalar tile (A/B knob)
+    assert "XOR" not in note1
     sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
     assert "STS" in sass and "LDS" in sass and "BAR.SYNC" in sass
 
