@@ -214,6 +214,28 @@ sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_inde
                                char* cubin_path_out, uint64_t path_cap, char* strategy_out,
                                uint64_t strategy_cap);
 sfx_status sfx_kernel_get_info(sfx_kernel* k, sfx_kernel_info* info);
+
+/* ---- measured perf library (the paper's library-miss path: build, run and
+ * time a kernel, record it; reference tuning.cpp:192-201 fills misses with an
+ * analytical estimate instead) ---- */
+/* Device timer: compiles program `program_index` with `opts`, launches it
+ * `reps` times back to back on synthetic inputs and returns the average
+ * per-launch time in microseconds; *checksum (may be NULL) = fp64 sum of
+ * output 0, for checking that candidate lowerings agree. */
+sfx_status sfx_program_time(sfx_ctx* ctx, const sfx_graph_desc* graph, int32_t program_index,
+                            const sfx_compile_opts* opts, int32_t reps, double* us_out, double* checksum);
+/* Template parameter cache (the B200 side of the perf library): groups are
+ * filed under the signature of the kernel their default options generate;
+ * lowering with default options uses a group's recorded parameters. */
+sfx_status sfx_program_signature(const sfx_graph_desc* graph, int32_t program_index, const sfx_compile_opts* opts,
+                                 char* out, uint64_t cap);
+int32_t sfx_template_param_has(const char* signature);
+sfx_status sfx_template_param_put(const char* signature, int32_t rows_per_cta, int32_t threads_per_row,
+                                  int32_t items_per_thread, int32_t pipe_ctas_per_sm, double tuned_us,
+                                  double default_us, const char* source);
+/* The whole cache in its file format (SFX_TEMPLATE_PARAMS / template_params.txt);
+ * *needed = bytes including the terminator. */
+sfx_status sfx_template_params_text(char* out, uint64_t cap, uint64_t* needed);
 /* Instruction indices of the input slots (ascending external id, splats excluded). */
 sfx_status sfx_kernel_input_instrs(sfx_kernel* k, int32_t* out, int32_t cap);
 /* One launch.  inputs: device pointers per input slot; outputs: per root (comp.roots order). */

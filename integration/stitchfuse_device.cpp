@@ -13,6 +13,13 @@
 #include <variant>
 
 #include "sfx.h"
+#include "stitchfuse/fixtures.hpp"
+#include "stitchfuse/kernelgen.hpp"
+#include "stitchfuse/schedule.hpp"
+#include "stitchfuse/smem.hpp"
+#include "stitchfuse/span.hpp"
+#include "stitchfuse/tuning.hpp"
+#include "json.hpp"
 
 namespace stitchfuse_device {
 
@@ -314,6 +321,157 @@ std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const T
   for (const InstrId& o : graph.outputs()) pout.push_back(host_data(values[o]));
   check(sfx_graph_run_host(g, pin.data(), n, pout.data(), static_cast<int32_t>(pout.size()), nullptr));
   return values;
+}
+
+// ---- measured perf library ---------------------------------------------------
+
+namespace {
+
+// A graph holding one instruction of `g` with its operands as parameters.
+TensorGraph single_instruction_graph(const TensorGraph& g, const Instruction& ins) {
+  nlohmann::json doc = nlohmann::json::parse(serialize_graph(g));
+  nlohmann::json one;
+  for (const auto& j : doc["instructions"])
+    if (j["id"] == ins.id) one = j;
+  nlohmann::json out = {{"instructions", nlohmann::json::array()}, {"outputs", {ins.id}}};
+  std::vector<std::string> ops;
+  for (size_t k = 0; k < ins.operands.size(); ++k) {
+    const Shape& sh = g.at(ins.operands[k]).shape;
+    const std::string pid = "in" + std::to_string(k);
+    nlohmann::json p = {{"id", pid}, {"op", "parameter"}, {"shape", sh.dims}};
+    if (sh.etype == ElementType::I32) p["dtype"] = "i32";
+    out["instructions"].push_back(p);
+    ops.push_back(pid);
+  }
+  one["operands"] = ops;
+  out["instructions"].push_back(one);
+  return parse_graph(out.dump());
+}
+
+}  // namespace
+
+MeasureStats measure_misses(const TensorGraph& graph, const PipelineOptions& options, PerfLibrary& lib,
+                            const CostModelParams& params, int reps, int max_keys) {
+  MeasureStats st;
+  PerfLibrary probe = lib;
+  compile_graph(graph, options, probe, params);  // misses become synthetic entries
+  sfx_ctx* ctx = context();
+  sfx_compile_opts lit{};
+  lit.strategy = SFX_STRATEGY_LITERAL;
+  for (const auto& [key, entry] : probe.entries()) {
+    const PerfEntry* have = lib.find(key);
+    if (!entry.synthetic || (have && !have->synthetic)) continue;
+    ++st.keys_missed;
+    if (max_keys >= 0 && st.keys_measured >= max_keys) continue;
+    const Instruction* ins = nullptr;
+    for (const Instruction& i : graph.instructions())
+      if (opcode_name(i) == key.opcode && i.shape.dims == key.shape) {
+        ins = &i;
+        break;
+      }
+    if (!ins) continue;
+    try {
+      TensorGraph g1 = single_instruction_graph(graph, *ins);
+      PipelineOptions o1 = options;
+      o1.fuse_dot = true;  // a lone BatchMatMul key is measured as its own group
+      FusionPlan fp = fuse_module(g1, o1);
+      const FusedComputation* comp = nullptr;
+      for (const FusedComputation& c : fp.computations)
+        if (c.members.count(ins->id)) comp = &c;
+      if (!comp) continue;
+      Schedule sched;
+      sched.split_dim = key.split_dim;
+      sched.sword = key.sword;
+      sched.type = key.sched_type;
+      ResolveResult r = resolve_schedule(*comp, g1, {{ins->id, sched}}, o1);
+      if (!r.ok()) continue;
+      SchedulePlan plan = *r.plan;
+      plan.block_threads = key.block_threads;
+      SpanMap sm = compute_span(g1);
+      SmemResult smem = plan_shared_memory(*comp, g1, sm, plan, o1);
+      if (!std::holds_alternative<SharedMemPlan>(smem)) continue;
+      KernelProgram prog = emit_program(*comp, g1, sm, plan, std::get<SharedMemPlan>(smem), o1);
+      Desc d(g1, {&prog});
+      double us = 0;
+      check(sfx_program_time(ctx, &d.desc, 0, &lit, reps, &us, nullptr));
+      PerfEntry e;
+      e.cost_us = us;
+      e.synthetic = false;
+      lib.insert(key, e);
+      ++st.keys_measured;
+    } catch (const std::exception& e) {
+      st.notes.push_back(key.opcode + ": " + e.what());
+    }
+  }
+  return st;
+}
+
+MeasureStats tune_templates(const CompileReport& report, const TensorGraph& graph, int reps) {
+  MeasureStats st;
+  sfx_ctx* ctx = context();
+  std::vector<const KernelProgram*> progs;
+  for (const CompiledKernel& k : report.kernels) progs.push_back(&k.program);
+  Desc d(graph, progs);
+  for (size_t i = 0; i < progs.size(); ++i) {
+    const int32_t pi = static_cast<int32_t>(i);
+    sfx_compile_opts dflt{};
+    char sig[512];
+    check(sfx_program_signature(&d.desc, pi, &dflt, sig, sizeof sig));
+    if (sfx_template_param_has(sig)) continue;  // hit
+    std::string strategy(256, '\0');
+    check(sfx_program_codegen(&d.desc, pi, &dflt, nullptr, 0, nullptr, 0, strategy.data(), strategy.size()));
+    strategy = strategy.substr(0, strategy.find(' '));
+    std::vector<sfx_compile_opts> cands;
+    auto cand = [&](int rows, int tpr, int items, int ctas) {
+      sfx_compile_opts o{};
+      o.rows_per_cta = rows;
+      o.threads_per_row = tpr;
+      o.items_per_thread = items;
+      o.pipe_ctas_per_sm = ctas;
+      cands.push_back(o);
+    };
+    if (strategy == "map") {
+      for (int u : {1, 2, 4, 8}) cand(0, 0, u, 0);
+    } else if (strategy == "row") {
+      for (int t : {32, 64, 128, 256}) cand(0, t, 0, 0);
+      for (int r : {1, 2}) cand(r, 0, 0, 0);
+    } else if (strategy == "col") {
+      cand(0, 0, 24, 1), cand(0, 0, 32, 1), cand(0, 0, 8, 2), cand(0, 0, 12, 3);
+    } else {
+      continue;  // literal / colbc / dot: no template knobs
+    }
+    double t0 = 0, c0 = 0;
+    check(sfx_program_time(ctx, &d.desc, pi, &dflt, reps, &t0, &c0));
+    ++st.groups_tuned;
+    double best = t0;
+    const sfx_compile_opts* win = nullptr;
+    for (const sfx_compile_opts& o : cands) {
+      double t = 0, c = 0;
+      if (sfx_program_time(ctx, &d.desc, pi, &o, reps, &t, &c) != SFX_OK) continue;  // knob not applicable
+      if (!(std::abs(c - c0) <= 1e-4 * std::max(1.0, std::abs(c0)))) continue;   // must compute the same
+      if (t < 0.98 * t0 && t < best) best = t, win = &o;
+    }
+    const std::string root = progs[i]->comp.fusion_root;
+    if (win) {
+      check(sfx_template_param_put(sig, win->rows_per_cta, win->threads_per_row, win->items_per_thread,
+                                   win->pipe_ctas_per_sm, best, t0, ("measured on miss: " + root).c_str()));
+      ++st.groups_changed;
+      st.notes.push_back(root + ": " + sig + " " + std::to_string(t0) + " -> " + std::to_string(best) + " us");
+    } else {
+      check(sfx_template_param_put(sig, 0, 0, 0, 0, t0, t0, ("measured on miss, defaults kept: " + root).c_str()));
+      st.notes.push_back(root + ": " + sig + " defaults kept (" + std::to_string(t0) + " us)");
+    }
+  }
+  return st;
+}
+
+std::string template_params_text() {
+  uint64_t need = 0;
+  check(sfx_template_params_text(nullptr, 0, &need));
+  std::string t(need, '\0');
+  check(sfx_template_params_text(t.data(), t.size(), &need));
+  t.resize(need ? need - 1 : 0);
+  return t;
 }
 
 }  // namespace stitchfuse_device

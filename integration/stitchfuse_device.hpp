@@ -8,6 +8,7 @@
 #pragma once
 
 #include <map>
+#include <string>
 #include <vector>
 
 #include "stitchfuse/exec.hpp"
@@ -47,5 +48,39 @@ void set_strategy(int sfx_strategy);
 // sfx_compile_opts.debug_checks for subsequent calls: 1 = the coverage check of
 // the reference executor (exec.cpp:393-410) around every launch.
 void set_debug_checks(int level);
+
+// ---- measured perf library: the paper's library-miss path on the B200 ----
+// (on a miss, build, run and time the kernel, record it.
+// The reference's lookup_or_estimate, tuning.cpp:192-201, records an
+// analytical estimate marked synthetic instead.)
+struct MeasureStats {
+  int keys_missed = 0;    // perf keys the planner looked up without a measured entry
+  int keys_measured = 0;  // of those, timed on the device and recorded (synthetic = false)
+  int groups_tuned = 0;   // planned groups whose template parameters were measured on miss
+  int groups_changed = 0; // ... where a candidate beat the default parameters (>= 2%)
+  std::vector<std::string> notes;
+};
+
+// Plans `graph` with `lib`; every key the planner missed (lookup_or_estimate
+// inserted a synthetic estimate for it) is measured: the instruction alone,
+// run under exactly that key's schedule and block size by the literal tier
+// (the reference's chunk_box blocks, so the cost is schedule-sensitive), and
+// recorded in `lib` in the reference's own format.  Re-planning with `lib`
+// then hits on every key.  `max_keys` < 0: no limit.
+MeasureStats measure_misses(const TensorGraph& graph, const stitchfuse::PipelineOptions& options,
+                            stitchfuse::PerfLibrary& lib, const stitchfuse::CostModelParams& params, int reps = 10,
+                            int max_keys = -1);
+
+// Template parameters of the report's planned groups, measured on miss in the
+// B200 template parameter cache: a group not in the cache (keyed by its
+// default kernel's signature) is timed with its default parameters and every
+// candidate of its template; the winner (>= 2% faster with the same output
+// checksum, else the defaults) is recorded, so later lowerings of that group
+// use it.  Returns what was tuned.
+MeasureStats tune_templates(const CompileReport& report, const TensorGraph& graph, int reps = 20);
+
+// The template parameter cache in its file format (write it where
+// SFX_TEMPLATE_PARAMS points to persist it).
+std::string template_params_text();
 
 }  // namespace stitchfuse_device

@@ -16,9 +16,12 @@
 //   device_parity crit9 | crit7
 //        acceptance criteria 9 (50 fuse_dot executor runs, coverage-checked)
 //        and 7 (shrunk fuse_dot fixture), test_acceptance.cpp:276-391
+//   device_parity perflib <graph.json> <lib_out> <template_params_out> [max_keys]
+//        the measured perf library: misses measured on the device, re-plan hits
 //   device_parity cache
 //        the binding's compiled-plan cache: one compile per plan signature
 // Prints one JSON line; exit 0 iff every eligible case passed.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -415,6 +418,51 @@ int cmd_cache() {
   return finish("binding cache", t, 0);
 }
 
+std::vector<std::pair<InstrId, std::set<InstrId>>> membership(const CompileReport& r) {
+  std::vector<std::pair<InstrId, std::set<InstrId>>> m;
+  for (const CompiledKernel& k : r.kernels) m.push_back({k.comp.fusion_root, k.comp.members});
+  return m;
+}
+
+// The measured perf library (integration/): plan a graph, measure every key
+// the planner missed on the device (literal tier under that key's schedule),
+// re-plan with the measured library (no misses left), then tune the planned
+// groups' template parameters on miss.  Default-library plans are the parity
+// contract: their membership is printed next to the measured one.
+int cmd_perflib(const std::string& graph_path, const std::string& lib_out, const std::string& tp_out, int max_keys) {
+  std::ifstream in(graph_path);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  TensorGraph g = parse_graph(ss.str());
+  PipelineOptions o;
+  CostModelParams params;
+  PerfLibrary empty;
+  CompileReport base = compile_graph(g, o, empty, params);
+  PerfLibrary lib;
+  auto t0 = std::chrono::steady_clock::now();
+  stitchfuse_device::MeasureStats ms = stitchfuse_device::measure_misses(g, o, lib, params, 10, max_keys);
+  double measure_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  size_t measured = 0;
+  for (const auto& [k, e] : lib.entries()) measured += !e.synthetic;
+  lib.hits_ = lib.misses_ = 0;
+  PerfLibrary replan = lib;
+  CompileReport with = compile_graph(g, o, replan, params);
+  stitchfuse_device::MeasureStats tt = stitchfuse_device::tune_templates(base, g, 20);
+  stitchfuse_device::MeasureStats again = stitchfuse_device::tune_templates(base, g, 20);
+  lib.store(lib_out);
+  std::ofstream(tp_out) << stitchfuse_device::template_params_text();
+  json line = {{"mode", "perflib"}, {"graph", graph_path}, {"keys_missed", ms.keys_missed},
+               {"keys_measured", ms.keys_measured}, {"measured_entries", measured}, {"measure_seconds", measure_s},
+               {"replan_misses", replan.misses()}, {"replan_hits", replan.hits()},
+               {"membership_default_equals_measured", membership(base) == membership(with)},
+               {"groups_default", base.kernels.size()}, {"groups_measured", with.kernels.size()},
+               {"groups_tuned", tt.groups_tuned}, {"groups_changed", tt.groups_changed},
+               {"retune_groups_tuned", again.groups_tuned}, {"notes", tt.notes}, {"measure_notes", ms.notes}};
+  std::cout << line.dump() << std::endl;
+  const bool ok = ms.keys_measured > 0 && replan.misses() == 0 && tt.groups_tuned > 0 && again.groups_tuned == 0;
+  return ok ? 0 : 1;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -433,6 +481,8 @@ int main(int argc, char** argv) {
     if (cmd == "crit9") return cmd_crit9();
     if (cmd == "crit7") return cmd_crit7();
     if (cmd == "cache") return cmd_cache();
+    if (cmd == "perflib")
+      return cmd_perflib(pos.at(1), pos.at(2), pos.at(3), pos.size() > 4 ? std::stoi(pos[4]) : -1);
     if (cmd == "shrink") return cmd_shrink(pos.size() > 1 ? std::stoull(pos[1]) : 7, pos.size() > 2 ? std::stoi(pos[2]) : 30);
     throw std::runtime_error("unknown command " + cmd);
   } catch (const std::exception& e) {

@@ -742,6 +742,126 @@ sfx_status sfx_program_codegen(const sfx_graph_desc* graph, int32_t program_inde
   });
 }
 
+sfx_status sfx_program_signature(const sfx_graph_desc* graph, int32_t program_index, const sfx_compile_opts* opts,
+                                 char* out, uint64_t cap) {
+  return guard([&] {
+    sfx::Graph g = sfx::graph_from_desc(graph);
+    if (program_index >= static_cast<int32_t>(g.programs.size())) add_barrier_programs(g);
+    sfx_compile_opts o{};
+    if (opts) o = *opts;
+    const std::string sig = sfx::kernel_signature(g, program_index, o);
+    if (!out || cap <= sig.size()) throw sfx::Error(SFX_ERR_INVALID, "signature buffer too small");
+    std::memcpy(out, sig.c_str(), sig.size() + 1);
+  });
+}
+
+int32_t sfx_template_param_has(const char* signature) {
+  return signature && sfx::template_param_find(signature) ? 1 : 0;
+}
+
+sfx_status sfx_template_param_put(const char* signature, int32_t rows_per_cta, int32_t threads_per_row,
+                                  int32_t items_per_thread, int32_t pipe_ctas_per_sm, double tuned_us,
+                                  double default_us, const char* source) {
+  return guard([&] {
+    if (!signature || !*signature) throw sfx::Error(SFX_ERR_INVALID, "empty signature");
+    std::string src = source ? source : "";
+    for (char& ch : src)
+      if (ch == '|' || ch == '\n') ch = ' ';
+    sfx::template_param_put(signature, rows_per_cta, threads_per_row, items_per_thread, pipe_ctas_per_sm, tuned_us,
+                            default_us, src);
+  });
+}
+
+sfx_status sfx_template_params_text(char* out, uint64_t cap, uint64_t* needed) {
+  return guard([&] {
+    const std::string t = sfx::template_params_text();
+    if (needed) *needed = t.size() + 1;
+    if (out && cap > t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+  });
+}
+
+// Device timer for the perf-library miss path: one group compiled with `opts`,
+// launched back to back on synthetic inputs (every element 0.5 / 1; rotating
+// buffer sets when a set is smaller than 3x L2), CUDA events around `reps`
+// launches.  *checksum = fp64 sum of output 0 of the first set (candidate
+// kernels of one group must agree on it).
+sfx_status sfx_program_time(sfx_ctx* ctx, const sfx_graph_desc* graph, int32_t program_index,
+                            const sfx_compile_opts* opts, int32_t reps, double* us_out, double* checksum) {
+  return guard([&] {
+    if (!ctx || !us_out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    sfx::Graph g = sfx::graph_from_desc(graph);
+    if (program_index >= static_cast<int32_t>(g.programs.size())) add_barrier_programs(g);
+    std::unique_ptr<sfx_kernel, void (*)(sfx_kernel*)> k(build_kernel(ctx, g, program_index, opts), destroy_kernel);
+    const sfx::Driver& d = sfx::driver();
+    ctx->bind();
+    int l2 = 0;
+    d.cuDeviceGetAttribute(&l2, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, ctx->dev);
+    uint64_t per_set = 0;
+    for (int n : k->src.inputs) per_set += g.nodes[n].numel() * 4;
+    for (int n : k->src.outputs) per_set += g.nodes[n].numel() * 4;
+    const int nsets = static_cast<int>(std::min<uint64_t>(8, std::max<uint64_t>(1, (3ull * l2 + per_set - 1) /
+                                                                                      std::max<uint64_t>(per_set, 1))));
+    std::vector<std::vector<CUdeviceptr>> ins(nsets), outs(nsets);
+    CUstream s = nullptr;
+    CUevent e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&] {
+      for (auto& v : ins)
+        for (CUdeviceptr p : v) ctx->release(p);
+      for (auto& v : outs)
+        for (CUdeviceptr p : v) ctx->release(p);
+      if (e0) d.cuEventDestroy(e0);
+      if (e1) d.cuEventDestroy(e1);
+      if (s) d.cuStreamDestroy(s);
+    };
+    try {
+      sfx::check_cu(d.cuStreamCreate(&s, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+      for (int i = 0; i < nsets; ++i) {
+        for (int n : k->src.inputs) {
+          CUdeviceptr p = ctx->alloc(g.nodes[n].numel() * 4);
+          ins[i].push_back(p);
+          const uint32_t bits = g.nodes[n].dtype == SFX_F32 ? 0x3f000000u : 1u;
+          sfx::check_cu(d.cuMemsetD32Async(p, bits, g.nodes[n].numel(), s), "cuMemsetD32Async");
+        }
+        for (int n : k->src.outputs) outs[i].push_back(ctx->alloc(g.nodes[n].numel() * 4));
+      }
+      for (int i = 0; i < 3; ++i) launch(k.get(), ins[i % nsets], outs[i % nsets], s);
+      sfx::check_cu(d.cuEventCreate(&e0, CU_EVENT_DEFAULT), "cuEventCreate");
+      sfx::check_cu(d.cuEventCreate(&e1, CU_EVENT_DEFAULT), "cuEventCreate");
+      const int r = std::max(1, reps);
+      sfx::check_cu(d.cuEventRecord(e0, s), "cuEventRecord");
+      for (int i = 0; i < r; ++i) launch(k.get(), ins[i % nsets], outs[i % nsets], s);
+      sfx::check_cu(d.cuEventRecord(e1, s), "cuEventRecord");
+      sfx::check_cu(d.cuEventSynchronize(e1), "cuEventSynchronize");
+      float ms = 0;
+      sfx::check_cu(d.cuEventElapsedTime(&ms, e0, e1), "cuEventElapsedTime");
+      *us_out = 1000.0 * ms / r;
+      if (checksum) {
+        const int o = k->src.outputs.empty() ? -1 : k->src.outputs[0];
+        double sum = 0;
+        if (o >= 0) {
+          const int64_t n = std::min<int64_t>(g.nodes[o].numel(), int64_t{16} << 20);
+          std::vector<uint32_t> host(n);
+          sfx::check_cu(d.cuMemcpyDtoH(host.data(), outs[(r - 1) % nsets][0], n * 4), "cuMemcpyDtoH");
+          for (uint32_t bits : host) {
+            if (g.nodes[o].dtype == SFX_F32) {
+              float f;
+              std::memcpy(&f, &bits, 4);
+              sum += f;
+            } else {
+              sum += static_cast<int32_t>(bits);
+            }
+          }
+        }
+        *checksum = sum;
+      }
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 sfx_status sfx_kernel_get_info(sfx_kernel* k, sfx_kernel_info* info) {
   return guard([&] {
     if (!k || !info) throw sfx::Error(SFX_ERR_INVALID, "null argument");

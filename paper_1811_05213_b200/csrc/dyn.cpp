@@ -56,6 +56,8 @@ const Driver& driver() {
     SFX_BIND(cuEventCreate)
     SFX_BIND(cuEventDestroy)
     SFX_BIND(cuEventRecord)
+    SFX_BIND(cuEventSynchronize)
+    SFX_BIND(cuEventElapsedTime)
     SFX_BIND(cuModuleLoadData)
     SFX_BIND(cuModuleUnload)
     SFX_BIND(cuModuleGetFunction)

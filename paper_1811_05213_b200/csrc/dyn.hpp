@@ -34,6 +34,8 @@ struct Driver {
   SFX_DRV(cuEventCreate)
   SFX_DRV(cuEventDestroy)
   SFX_DRV(cuEventRecord)
+  SFX_DRV(cuEventSynchronize)
+  SFX_DRV(cuEventElapsedTime)
   SFX_DRV(cuModuleLoadData)
   SFX_DRV(cuModuleUnload)
   SFX_DRV(cuModuleGetFunction)

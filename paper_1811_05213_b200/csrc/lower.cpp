@@ -59,14 +59,19 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
 namespace {
 struct TunedParams {
   int rows_per_cta = 0, threads_per_row = 0, items_per_thread = 0, pipe_ctas_per_sm = 0;
-  std::string note;
+  std::string note, tuned_us, default_us, source;
 };
-const std::map<std::string, TunedParams>& template_params() {
+std::mutex g_tp_mu;  // guards the cache below after loading (template_param_put)
+bool g_tp_disabled = false;
+std::map<std::string, TunedParams>& template_params() {
   static std::map<std::string, TunedParams> m;
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = std::getenv("SFX_TEMPLATE_PARAMS");
-    if (e && e[0] == '0' && e[1] == 0) return;
+    if (e && e[0] == '0' && e[1] == 0) {
+      g_tp_disabled = true;
+      return;
+    }
     std::string path = e ? e : library_dir() + "/template_params.txt";
     std::ifstream in(path);
     std::string line;
@@ -83,6 +88,9 @@ const std::map<std::string, TunedParams>& template_params() {
       t.items_per_thread = std::atoi(f[3].c_str());
       t.pipe_ctas_per_sm = std::atoi(f[4].c_str());
       t.note = "tuned " + f[6] + " -> " + f[5] + " us";
+      t.tuned_us = f[5];
+      t.default_us = f[6];
+      t.source = f.size() > 7 ? f[7] : "";
       m[f[0]] = t;
     }
   });
@@ -96,21 +104,69 @@ bool default_knobs(const sfx_compile_opts& o) {
 
 KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o);
 
+std::string kernel_signature(const Graph& g, int pi, const sfx_compile_opts& o) {
+  KernelSource ks = lower_program_raw(g, pi, o);
+  char hex[32];
+  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(ks.code)));
+  return ks.entry + "-" + hex;
+}
+
+bool template_param_find(const std::string& sig) {
+  std::lock_guard<std::mutex> lock(g_tp_mu);
+  return template_params().count(sig) > 0;
+}
+
+void template_param_put(const std::string& sig, int rows_per_cta, int threads_per_row, int items_per_thread,
+                        int pipe_ctas_per_sm, double tuned_us, double default_us, const std::string& source) {
+  std::lock_guard<std::mutex> lock(g_tp_mu);
+  TunedParams t;
+  t.rows_per_cta = rows_per_cta;
+  t.threads_per_row = threads_per_row;
+  t.items_per_thread = items_per_thread;
+  t.pipe_ctas_per_sm = pipe_ctas_per_sm;
+  char a[32], b[32];
+  std::snprintf(a, sizeof a, "%.2f", tuned_us);
+  std::snprintf(b, sizeof b, "%.2f", default_us);
+  t.tuned_us = a;
+  t.default_us = b;
+  t.source = source;
+  t.note = "tuned " + t.default_us + " -> " + t.tuned_us + " us";
+  template_params()[sig] = t;
+}
+
+std::string template_params_text() {
+  std::lock_guard<std::mutex> lock(g_tp_mu);
+  std::ostringstream os;
+  os << "# signature|rows_per_cta|threads_per_row|items_per_thread|pipe_ctas_per_sm|tuned_us|default_us|source\n";
+  for (auto& [sig, t] : template_params())
+    os << sig << "|" << t.rows_per_cta << "|" << t.threads_per_row << "|" << t.items_per_thread << "|"
+       << t.pipe_ctas_per_sm << "|" << t.tuned_us << "|" << t.default_us << "|" << t.source << "\n";
+  return os.str();
+}
+
 KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   KernelSource ks = lower_program_raw(g, pi, o);
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(ks.code)));
   const std::string sig = ks.entry + "-" + hex;
   if (default_knobs(o)) {
-    auto it = template_params().find(sig);
-    if (it != template_params().end()) {
+    TunedParams tp;
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lock(g_tp_mu);
+      auto it = template_params().find(sig);
+      if (it != template_params().end()) tp = it->second, hit = true;
+    }
+    if (hit && (tp.rows_per_cta || tp.threads_per_row || tp.items_per_thread || tp.pipe_ctas_per_sm)) {
       sfx_compile_opts t = o;
-      t.rows_per_cta = it->second.rows_per_cta;
-      t.threads_per_row = it->second.threads_per_row;
-      t.items_per_thread = it->second.items_per_thread;
-      t.pipe_ctas_per_sm = it->second.pipe_ctas_per_sm;
+      t.rows_per_cta = tp.rows_per_cta;
+      t.threads_per_row = tp.threads_per_row;
+      t.items_per_thread = tp.items_per_thread;
+      t.pipe_ctas_per_sm = tp.pipe_ctas_per_sm;
       ks = lower_program_raw(g, pi, t);
-      ks.note += " [template_params: " + it->second.note + "]";
+      ks.note += " [template_params: " + tp.note + "]";
+    } else if (hit) {
+      ks.note += " [template_params: " + tp.note + "]";
     }
   }
   ks.note += " sig=" + sig;

@@ -67,6 +67,14 @@ struct KernelSource {
 
 KernelSource lower_program(const Graph& g, int program_index, const sfx_compile_opts& opts);
 
+// Template parameter cache (lower.cpp): the signature a group's default-option
+// kernel is filed under, lookups, in-process inserts and the text form.
+std::string kernel_signature(const Graph& g, int program_index, const sfx_compile_opts& opts);
+bool template_param_find(const std::string& sig);
+void template_param_put(const std::string& sig, int rows_per_cta, int threads_per_row, int items_per_thread,
+                        int pipe_ctas_per_sm, double tuned_us, double default_us, const std::string& source);
+std::string template_params_text();
+
 // Strategy the analyzer would pick (without generating code), with the reason
 // the faster templates were rejected.
 std::string choose_strategy(const Graph& g, int program_index, std::string* why);

@@ -8,6 +8,7 @@ import json
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -46,3 +47,47 @@ def test_reference_planner_consumes_measured_library(cfg):
     assert "NVIDIA B200" in header
     # chosen plans now cost the measured device time (microseconds, not the synthetic 500 GB/s model)
     assert all(k["cost_us"] < 1000 for k in d["kernels"])
+
+
+DEVICE_PARITY = os.path.join(T.ROOT, "oracle", "_ref", "device_parity")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(DEVICE_PARITY), reason="reference harness not built (needs /root/reference)")
+@pytest.mark.parametrize("name,sizes", [("C1", dict(R=64, C=1024)), ("C4", dict(B=2, S=64, H=16, D=64))])
+def test_perflib_misses_measured_on_device(tmp_path, name, sizes):
+    """The paper's library-miss path on the B200, through the
+    reference-side binding: every perf key the reference planner misses is timed
+    on the device (the instruction alone, literal tier, under that key's
+    schedule and block size) and recorded non-synthetic in the reference's own
+    format; re-planning then misses nothing.  The planned groups' template
+    parameters are measured on miss into the template cache (a second pass hits
+    everything), and a fresh process lowering with that cache uses them."""
+    from workloads import configs
+    graph = tmp_path / "g.json"
+    graph.write_text(configs.dumps(configs.build(name, **sizes)))
+    lib, tp = tmp_path / "measured.lib", tmp_path / "template_params.txt"
+    env = dict(os.environ, SFX_TEMPLATE_PARAMS=str(tmp_path / "none.txt"))
+    r = subprocess.run([DEVICE_PARITY, "perflib", str(graph), str(lib), str(tp)], capture_output=True, text=True,
+                       timeout=1500, env=env)
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.returncode == 0, d
+    assert d["keys_measured"] == d["keys_missed"] > 0 and d["replan_misses"] == 0
+    assert d["groups_tuned"] >= 1 and d["retune_groups_tuned"] == 0
+    # the stored library parses with the reference's format: every entry measured
+    entries = [l for l in open(lib) if l.strip() and not l.startswith("#")]
+    assert len(entries) == d["measured_entries"] and all(l.rstrip().endswith("|0") for l in entries)
+    # the template cache round-trips: a new process lowering with it finds every group
+    tpl = [l for l in open(tp) if not l.startswith("#")]
+    assert len(tpl) == d["groups_tuned"]
+    g = H.graph_from_json(json.loads(graph.read_text()))
+    bundle = json.loads(subprocess.run([T.REF_TOOL, "plan", str(graph)], capture_output=True, text=True).stdout) \
+        if os.path.exists(T.REF_TOOL) else None
+    if bundle is not None:
+        code = ("import sys, json; sys.path.insert(0, %r); import paper_1811_05213_b200 as P; "
+                "b = json.load(open(%r)); g = P.graph_from_json(b['graph']); r = P.CompileReport.from_bundle(b); "
+                "print('\\n'.join(P.codegen(g, k.program)[2] for k in r.kernels))") % (T.ROOT, str(tmp_path / "b.json"))
+        (tmp_path / "b.json").write_text(json.dumps(bundle))
+        notes = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                               env=dict(os.environ, SFX_TEMPLATE_PARAMS=str(tp))).stdout.splitlines()
+        assert sum("[template_params:" in n for n in notes) == d["groups_tuned"], notes
