@@ -111,7 +111,8 @@ EXPORTS = [
     "sfx_kernel_get_info", "sfx_kernel_input_instrs", "sfx_program_launch", "sfx_kernel_destroy",
     "sfx_graph_compile", "sfx_graph_param_instrs", "sfx_graph_kernel", "sfx_graph_kernel_count", "sfx_graph_run",
     "sfx_graph_run_host", "sfx_graph_destroy", "sfx_nccl_unique_id", "sfx_nccl_init",
-    "sfx_allreduce_sum_f32", "sfx_peer_create", "sfx_peer_open",
+    "sfx_allreduce_sum_f32", "sfx_peer_create", "sfx_peer_open", "sfx_program_time", "sfx_program_signature",
+    "sfx_template_param_has", "sfx_template_param_put", "sfx_template_params_text",
 ]
 ABI_VERSION = 2
 PEER_HANDLE_BYTES = 64
@@ -162,6 +163,12 @@ def lib():
         "sfx_allreduce_sum_f32": (i32, [vp, u64, u64, vp]),
         "sfx_peer_create": (i32, [vp, u64, vp]),
         "sfx_peer_open": (i32, [vp, vp, i32, i32]),
+        "sfx_program_time": (i32, [vp, C.POINTER(SfxGraphDesc), i32, C.POINTER(SfxCompileOpts), i32,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "sfx_program_signature": (i32, [C.POINTER(SfxGraphDesc), i32, C.POINTER(SfxCompileOpts), C.c_char_p, u64]),
+        "sfx_template_param_has": (i32, [C.c_char_p]),
+        "sfx_template_param_put": (i32, [C.c_char_p, i32, i32, i32, i32, C.c_double, C.c_double, C.c_char_p]),
+        "sfx_template_params_text": (i32, [C.c_char_p, u64, C.POINTER(u64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
