@@ -260,10 +260,11 @@ sfx_status sfx_graph_kernel_count(sfx_graph* g, int32_t* n_kernels, int32_t* n_p
  * sfx_graph_kernel.  use_cuda_graph=1 replays
  * a captured CUDA graph for this exact pointer set (captured on first use). */
 /* Concurrency: kernels that own a workspace (column / colbc cross-CTA
- * combine) get one workspace per stream, so launches of one kernel or graph on
- * different streams may run concurrently (each with its own buffers).  Every
- * CUDA graph captured by sfx_graph_run owns its workspaces (replays of one
- * capture are serialised by CUDA).  Exceptions: cross_rank kernels use one
+ * combine) get one workspace per stream, and a graph's intermediates (group
+ * roots consumed by later groups) are one set per stream, so launches of one
+ * kernel or graph on different streams may run concurrently (each with its own
+ * buffers).  Every CUDA graph captured by sfx_graph_run owns its workspaces and
+ * intermediates (replays of one capture are serialised by CUDA).  Exceptions: cross_rank kernels use one
  * workspace and one peer region and must run in the same order on every rank,
  * never concurrently with themselves; a launch captured by the CALLER's own
  * stream capture uses the kernel's default workspace, so such captured
@@ -276,6 +277,13 @@ sfx_status sfx_graph_run(sfx_graph* g, const uint64_t* params, int32_t n_params,
  * host->device, runs, copies outputs device->host, synchronizes the stream. */
 sfx_status sfx_graph_run_host(sfx_graph* g, const void* const* params, int32_t n_params,
                               void* const* outputs, int32_t n_outputs, void* stream);
+/* Read back a value the latest run on `stream` left in HBM: a group root that
+ * is not a graph output (an intermediate between groups) or a dense constant.
+ * This is how the binding returns run_compiled's full value map
+ * (pipeline.cpp:104-118: every parameter, constant, singleton and group root)
+ * without downloading intermediates on every run.  Synchronous.  Parameters,
+ * graph outputs and splat constants are rejected: the caller holds them. */
+sfx_status sfx_graph_fetch(sfx_graph* g, int32_t instr_index, void* host_out, uint64_t bytes, void* stream);
 sfx_status sfx_graph_destroy(sfx_graph* g);
 
 /* ---- collectives (batch-crossing column reduce) ---- */

@@ -9,6 +9,7 @@
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <variant>
 
@@ -320,6 +321,26 @@ std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const T
   for (const InstrId& o : graph.outputs()) values[o] = TensorValue::zeros(graph.at(o).shape);
   for (const InstrId& o : graph.outputs()) pout.push_back(host_data(values[o]));
   check(sfx_graph_run_host(g, pin.data(), n, pout.data(), static_cast<int32_t>(pout.size()), nullptr));
+  // The rest of the reference's map (pipeline.cpp:104-118): parameters and
+  // constants from the host, every other group root and unfused instruction
+  // read back from HBM (intermediates stay device-resident during the run).
+  std::set<InstrId> members;
+  for (const CompiledKernel& k : report.kernels) members.insert(k.comp.members.begin(), k.comp.members.end());
+  std::set<InstrId> roots;
+  for (const CompiledKernel& k : report.kernels) roots.insert(k.comp.roots.begin(), k.comp.roots.end());
+  for (const Instruction& ins : graph.instructions()) {
+    if (values.count(ins.id)) continue;
+    if (ins.opcode == Opcode::Parameter) {
+      values[ins.id] = inputs.at(ins.id);
+    } else if (ins.opcode == Opcode::Constant) {
+      values[ins.id] = constant_value(ins);
+    } else if (roots.count(ins.id) || !members.count(ins.id)) {
+      TensorValue v = TensorValue::zeros(ins.shape);
+      check(sfx_graph_fetch(g, d.index.at(ins.id), host_data(v), static_cast<uint64_t>(ins.shape.byte_size()),
+                            nullptr));
+      values[ins.id] = std::move(v);
+    }
+  }
   return values;
 }
 

@@ -29,7 +29,9 @@ std::vector<TensorValue> run_program(const KernelProgram& program, const TensorG
 
 // Device twin of stitchfuse::run_compiled (pipeline.hpp:50-51): one launch per
 // CompiledKernel in condensation order, intermediates resident in HBM.
-// Returns the graph outputs (the values callers of the reference read).
+// Returns the reference's whole map (pipeline.cpp:104-118): every parameter,
+// constant, unfused instruction and group root; the graph outputs come back
+// with the run, other roots are read back from HBM afterwards.
 std::map<InstrId, TensorValue> run_compiled(const CompileReport& report, const TensorGraph& graph,
                                             const std::map<InstrId, TensorValue>& inputs);
 

@@ -27,6 +27,7 @@
 #include <fstream>
 #include <iostream>
 #include <random>
+#include <set>
 #include <sstream>
 
 #include "../../integration/stitchfuse_device.hpp"
@@ -108,7 +109,7 @@ std::map<InstrId, TensorValue> interpret_fp64(const TensorGraph& g, const std::m
   gd.instrs = d.data();
   if (sfx_oracle_interpret(&gd, ptrs.data(), 1) != 0) throw std::runtime_error(sfx_oracle_error());
   std::map<InstrId, TensorValue> out;
-  for (const InstrId& o : g.outputs()) out[o] = vals[index.at(o)];
+  for (const auto& [id, i] : index) out[id] = vals[i];
   return out;
 }
 
@@ -129,8 +130,14 @@ bool compare(const TensorGraph& g, const std::map<InstrId, TensorValue>& ref, co
              const std::map<InstrId, TensorValue>& inputs, std::string* why) {
   std::map<InstrId, bool> memo;
   std::map<InstrId, TensorValue> exact;
-  for (const InstrId& o : g.outputs()) {
-    if (testsupport::values_close(dev.at(o), ref.at(o), 1e-5)) continue;
+  // every value of the map (graph outputs and the intermediates the binding
+  // reads back from HBM), against interpret's value of that instruction
+  for (const auto& [o, v] : dev) {
+    if (!ref.count(o)) {
+      *why = "unexpected key " + o;
+      return false;
+    }
+    if (testsupport::values_close(v, ref.at(o), 1e-5)) continue;
     if (reduce_dependent(g, o, memo)) {
       if (exact.empty()) exact = interpret_fp64(g, inputs);
       if (testsupport::values_close(dev.at(o), exact.at(o), 1e-5)) {
@@ -138,10 +145,23 @@ bool compare(const TensorGraph& g, const std::map<InstrId, TensorValue>& ref, co
         continue;
       }
     }
-    *why = "output " + o;
+    *why = "value " + o;
     return false;
   }
   return true;
+}
+
+// The key set of the reference's run_compiled map (pipeline.cpp:104-118):
+// every parameter, constant and unfused instruction, and every group root.
+std::set<InstrId> expected_keys(const TensorGraph& g, const CompileReport& report) {
+  std::set<InstrId> members, keys;
+  for (const CompiledKernel& k : report.kernels) {
+    members.insert(k.comp.members.begin(), k.comp.members.end());
+    keys.insert(k.comp.roots.begin(), k.comp.roots.end());
+  }
+  for (const Instruction& i : g.instructions())
+    if (!members.count(i.id)) keys.insert(i.id);
+  return keys;
 }
 
 // On failure with SFX_DUMP_DIR set: the graph, its inputs (parameters in
@@ -181,6 +201,12 @@ void run_case(const std::string& name, const TensorGraph& g, const CompileReport
       t.fail(name + ": launched " + std::to_string(launched) + " kernels for " +
              std::to_string(report.kernels.size()) + " fused groups + " +
              std::to_string(report.fusion.unfused.size()) + " unfused instructions");
+    } else if ([&] {
+                 std::set<InstrId> got;
+                 for (const auto& kv : dev) got.insert(kv.first);
+                 return got != expected_keys(g, report);
+               }()) {
+      t.fail(name + ": run_compiled map keys differ from the reference's");
     } else if (!compare(g, ref, dev, inputs, &why)) {
       t.fail(name + ": " + why);
       dump_case(name, g, inputs, ref, dev);

@@ -196,7 +196,16 @@ struct sfx_graph {
   int n_planned = 0;                 // programs that came from the CompileReport
   std::vector<int> order;            // program launch order (condensation Kahn order)
   std::vector<int> params;           // Parameter nodes, ascending id = param slot order
-  std::map<int, CUdeviceptr> owned;  // intermediates + dense constants (device-resident)
+  std::map<int, CUdeviceptr> owned;  // dense constants and splat outputs (device-resident)
+  // Intermediates (group roots that are not graph outputs, consumed by later
+  // groups) are per launch context, like the workspaces: one set per stream for
+  // eager runs (key {0, stream}) and one per captured pointer set (key {1,
+  // params..., outputs...}), so concurrent runs on different streams never
+  // share an intermediate buffer.  `last_mid[stream]` = the set the latest run
+  // on that stream wrote (what sfx_graph_fetch reads).
+  std::vector<int> mid_nodes;
+  std::map<std::vector<uint64_t>, std::map<int, CUdeviceptr>> mids;
+  std::map<CUstream, const std::map<int, CUdeviceptr>*> last_mid;
   std::map<std::vector<uint64_t>, std::pair<CUgraph, CUgraphExec>> captured;
   std::vector<CUdeviceptr> host_bufs;  // staging for sfx_graph_run_host (params then outputs)
   CUstream d2h = nullptr;              // host path: device->host copies overlap the next groups
@@ -525,8 +534,22 @@ std::vector<CUdeviceptr> gather_ptrs(const sfx_graph* G, const std::vector<int>&
   return v;
 }
 
-void graph_enqueue(sfx_graph* G, const uint64_t* params, const uint64_t* outputs, CUstream s) {
+// The intermediate set of launch context `key` (allocated on first use).
+const std::map<int, CUdeviceptr>& mids_for(sfx_graph* G, const std::vector<uint64_t>& key) {
+  auto it = G->mids.find(key);
+  if (it != G->mids.end()) return it->second;
+  std::map<int, CUdeviceptr>& m = G->mids[key];
+  for (int r : G->mid_nodes) m[r] = G->ctx->alloc(G->graph.nodes[r].numel() * 4);
+  return m;
+}
+
+std::vector<uint64_t> eager_key(CUstream s) { return {0, reinterpret_cast<uint64_t>(s)}; }
+
+void graph_enqueue(sfx_graph* G, const uint64_t* params, const uint64_t* outputs, CUstream s,
+                   const std::map<int, CUdeviceptr>& mid) {
   std::map<int, CUdeviceptr> where = G->owned;
+  where.insert(mid.begin(), mid.end());
+  G->last_mid[s] = &mid;
   for (size_t i = 0; i < G->params.size(); ++i) where[G->params[i]] = params[i];
   for (size_t i = 0; i < G->graph.outputs.size(); ++i) where[G->graph.outputs[i]] = outputs[i];
   const sfx::Driver& d = sfx::driver();
@@ -925,7 +948,7 @@ sfx_status sfx_graph_compile(sfx_ctx* ctx, const sfx_graph_desc* desc, const sfx
       const sfx::Driver& d = sfx::driver();
       for (const sfx::Program& p : g.programs)
         for (int r : p.roots)
-          if (!outs.count(r)) G->owned[r] = ctx->alloc(g.nodes[r].numel() * 4);
+          if (!outs.count(r)) G->mid_nodes.push_back(r);
       for (size_t i = 0; i < g.nodes.size(); ++i) {
         const sfx::Node& n = g.nodes[i];
         if (n.op != SFX_OP_CONSTANT || n.is_splat()) continue;
@@ -1009,12 +1032,16 @@ sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params,
     CUstream s = static_cast<CUstream>(stream);
     const sfx::Driver& d = sfx::driver();
     if (!use_cuda_graph) {
-      graph_enqueue(G, params, outputs, s);
+      graph_enqueue(G, params, outputs, s, mids_for(G, eager_key(s)));
       return;
     }
     if (!s) throw sfx::Error(SFX_ERR_INVALID, "CUDA-graph replay needs a non-default stream");
     std::vector<uint64_t> key(params, params + n_params);
     key.insert(key.end(), outputs, outputs + n_outputs);
+    std::vector<uint64_t> mkey{1};
+    mkey.insert(mkey.end(), key.begin(), key.end());
+    const std::map<int, CUdeviceptr>& mid = mids_for(G, mkey);
+    G->last_mid[s] = &mid;
     auto it = G->captured.find(key);
     if (it == G->captured.end()) {
       int64_t before = G->ctx->launches.load();
@@ -1033,7 +1060,7 @@ sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params,
       CUgraph graph = nullptr;
       t_capture_ws = &cws;
       try {
-        graph_enqueue(G, params, outputs, s);
+        graph_enqueue(G, params, outputs, s, mid);
         t_capture_ws = nullptr;
       } catch (...) {
         t_capture_ws = nullptr;
@@ -1118,6 +1145,9 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
       sfx::check_cu(d.cuStreamWaitEvent(st, ev_reset, 0), "cuStreamWaitEvent");
 
     std::map<int, CUdeviceptr> where = G->owned;
+    const std::map<int, CUdeviceptr>& mid = mids_for(G, eager_key(s));
+    where.insert(mid.begin(), mid.end());
+    G->last_mid[s] = &mid;
     std::map<int, int> param_slot, out_slot;
     for (int i = 0; i < n_params; ++i) where[G->params[i]] = dp[i], param_slot[G->params[i]] = i;
     for (int i = 0; i < n_outputs; ++i) where[g.outputs[i]] = dout[i], out_slot[g.outputs[i]] = i;
@@ -1251,6 +1281,38 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
   });
 }
 
+sfx_status sfx_graph_fetch(sfx_graph* G, int32_t instr_index, void* host_out, uint64_t bytes, void* stream) {
+  return guard([&] {
+    if (!G || !host_out) throw sfx::Error(SFX_ERR_INVALID, "null argument");
+    const sfx::Graph& g = G->graph;
+    if (instr_index < 0 || instr_index >= static_cast<int32_t>(g.nodes.size()))
+      throw sfx::Error(SFX_ERR_INVALID, "instruction index out of range");
+    const sfx::Node& n = g.nodes[instr_index];
+    if (bytes != static_cast<uint64_t>(n.numel()) * 4)
+      throw sfx::Error(SFX_ERR_INVALID, "fetch of " + n.id + ": expected " + std::to_string(n.numel() * 4) + " bytes");
+    std::lock_guard<std::mutex> lock(G->run_mu);
+    G->ctx->bind();
+    CUstream s = static_cast<CUstream>(stream);
+    CUdeviceptr src = 0;
+    auto own = G->owned.find(instr_index);
+    if (own != G->owned.end()) src = own->second;
+    auto last = G->last_mid.find(s);
+    if (!src && last != G->last_mid.end()) {
+      auto it = last->second->find(instr_index);
+      if (it != last->second->end()) src = it->second;
+    }
+    if (!src) {
+      bool mid = std::find(G->mid_nodes.begin(), G->mid_nodes.end(), instr_index) != G->mid_nodes.end();
+      throw sfx::Error(SFX_ERR_INVALID, mid ? "no run on this stream yet: " + n.id
+                                            : n.id + " is not device-resident in the graph (a parameter, a graph "
+                                                     "output or a folded splat: the caller holds it)");
+    }
+    const sfx::Driver& d = sfx::driver();
+    sfx::check_cu(d.cuMemcpyDtoHAsync(host_out, src, bytes, s), "cuMemcpyDtoHAsync");
+    sfx::check_cu(d.cuStreamSynchronize(s), "cuStreamSynchronize");
+  });
+}
+
 sfx_status sfx_graph_destroy(sfx_graph* G) {
   return guard([&] {
     if (!G) return;
@@ -1275,6 +1337,8 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
     for (sfx_kernel* k : G->kernels) destroy_kernel(k);
     for (sfx_kernel* k : G->host_kernels) destroy_kernel(k);
     for (auto& [n, p] : G->owned) G->ctx->release(p);
+    for (auto& [key, m] : G->mids)
+      for (auto& [n, p] : m) G->ctx->release(p);
     for (CUdeviceptr p : G->host_bufs) G->ctx->release(p);
     delete G;
   });

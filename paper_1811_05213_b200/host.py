@@ -112,7 +112,7 @@ EXPORTS = [
     "sfx_graph_compile", "sfx_graph_param_instrs", "sfx_graph_kernel", "sfx_graph_kernel_count", "sfx_graph_run",
     "sfx_graph_run_host", "sfx_graph_destroy", "sfx_nccl_unique_id", "sfx_nccl_init",
     "sfx_allreduce_sum_f32", "sfx_peer_create", "sfx_peer_open", "sfx_program_time", "sfx_program_signature",
-    "sfx_template_param_has", "sfx_template_param_put", "sfx_template_params_text",
+    "sfx_template_param_has", "sfx_template_param_put", "sfx_template_params_text", "sfx_graph_fetch",
 ]
 ABI_VERSION = 2
 PEER_HANDLE_BYTES = 64
@@ -169,6 +169,7 @@ def lib():
         "sfx_template_param_has": (i32, [C.c_char_p]),
         "sfx_template_param_put": (i32, [C.c_char_p, i32, i32, i32, i32, C.c_double, C.c_double, C.c_char_p]),
         "sfx_template_params_text": (i32, [C.c_char_p, u64, C.POINTER(u64)]),
+        "sfx_graph_fetch": (i32, [vp, i32, vp, u64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -653,10 +654,31 @@ class CompiledGraph:
         _check(lib().sfx_graph_run_host(self.h, pin, len(arrs), pout, len(self.graph.outputs), C.c_void_p(stream)))
         return outputs
 
+    def fetch(self, instr_id: str, stream=0) -> np.ndarray:
+        """A value the latest run on `stream` left in HBM (an intermediate group
+        root, or a dense constant): sfx_graph_fetch."""
+        ins = self.graph.at(instr_id)
+        a = np.empty(ins.shape, ins.np_dtype())
+        _check(lib().sfx_graph_fetch(self.h, self.graph.index[instr_id], C.c_void_p(a.ctypes.data), a.nbytes,
+                                     C.c_void_p(stream)))
+        return a
+
     def close(self):
         if self.h:
             lib().sfx_graph_destroy(self.h)
         self.h = None
+
+
+def constant_value(ins: Instruction) -> np.ndarray:
+    """stitchfuse::constant_value (exec.cpp:215-229): splat or dense literal,
+    each double narrowed to the element type."""
+    n = ins.numel()
+    lit = list(ins.value or [])
+    if len(lit) != 1 and len(lit) != n:
+        raise ExecError("constant literal size mismatch for " + ins.id)
+    raw = np.array(lit if len(lit) == n else lit * n, dtype=np.float64)
+    v = raw.astype(np.float32) if ins.dtype == "f32" else raw.astype(np.int64).astype(np.int32)
+    return v.reshape(ins.shape)
 
 
 def _to_device(ctx, arr):
@@ -694,15 +716,39 @@ def run_program(program: KernelProgram, graph: TensorGraph, externals: dict, str
         k.close()
 
 
-def run_compiled(report: CompileReport, graph: TensorGraph, inputs: dict, strategy="auto", ctx=None):
-    """Device twin of stitchfuse::run_compiled (pipeline.cpp:65-133); returns
-    the graph outputs (callers of the reference read only those)."""
+def run_compiled(report: CompileReport, graph: TensorGraph, inputs: dict, strategy="auto", ctx=None,
+                 values="outputs"):
+    """Device twin of stitchfuse::run_compiled (pipeline.cpp:65-133).
+
+    values="outputs": the graph outputs (what callers of the reference read,
+    stitchfuse.cpp:236-237).  values="all": the reference's whole map
+    (pipeline.cpp:104-118) — every parameter, constant, unfused instruction and
+    group root; intermediates are read back from HBM after the run
+    (sfx_graph_fetch)."""
+    if values not in ("outputs", "all"):
+        raise ValueError("values must be 'outputs' or 'all'")
     ctx = ctx or default_context()
     cg = CompiledGraph(ctx, graph, report, strategy)
     try:
         for p in cg.param_ids:
             if p not in inputs:
                 raise ExecError("missing input for parameter " + p)
-        return cg.run_host(inputs)
+        out = cg.run_host(inputs)
+        if values == "outputs":
+            return out
+        full = {}
+        roots = set(cg.unfused_ids)
+        for k in report.kernels:
+            roots.update(k.program.roots)
+        for ins in graph.instructions:
+            if ins.op == "parameter":
+                full[ins.id] = np.asarray(inputs[ins.id], dtype=ins.np_dtype()).reshape(ins.shape)
+            elif ins.op == "constant":
+                full[ins.id] = constant_value(ins)
+            elif ins.id in out:
+                full[ins.id] = out[ins.id]
+            elif ins.id in roots:
+                full[ins.id] = cg.fetch(ins.id)
+        return full
     finally:
         cg.close()

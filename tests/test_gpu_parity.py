@@ -481,3 +481,81 @@ def test_concurrent_launches_on_four_streams(ctx, cuda_graph):
                 assert torch.equal(st[1][0], ref)
     finally:
         cg.close()
+
+
+def _chain_close(got, r32, r64):
+    """A value of a matmul-chained graph: the reference's criterion against its
+    fp32 result or the fp64 value, or within twice the reference's own distance
+    from the fp64 value (see test_encoder_layer_small)."""
+    if got.dtype == np.int32:
+        return np.array_equal(got, r32)
+    if T.values_close(got, r32) or T.values_close(got, r64):
+        return True
+    g64, a32, a64 = got.astype(np.float64), r32.astype(np.float64), r64.astype(np.float64)
+    return np.abs(g64 - a64).max() <= 2 * np.abs(a32 - a64).max()
+
+
+def test_run_compiled_full_value_map(ctx):
+    """run_compiled(values="all") returns the reference's whole map
+    (pipeline.cpp:104-118): every parameter, constant, unfused instruction and
+    group root — the intermediates between C5L's groups are read back from HBM
+    (sfx_graph_fetch) — each matching the oracle's value of that instruction."""
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, "C5L.small.json"))
+    inputs = T.gen_inputs(g, 42, -1.0, 1.0)
+    full = H.run_compiled(rep, g, inputs, ctx=ctx, values="all")
+    members, keys = set(), set()
+    for k in rep.kernels:
+        members.update(k.program.members)
+        keys.update(k.program.roots)
+    keys.update(i.id for i in g.instructions if i.id not in members)
+    assert set(full) == keys
+    mids = keys - set(g.outputs) - {i.id for i in g.instructions if i.op in ("parameter", "constant")}
+    assert len(mids) >= 10  # intermediates really were fetched
+    r32, r64 = T.interpret(g, inputs, 0), T.interpret(g, inputs, 1)
+    bad = [k for k in sorted(keys) if not _chain_close(full[k], r32[k], r64[k])]
+    assert not bad, bad[:5]
+
+
+def test_concurrent_streams_with_intermediates(ctx):
+    """One compiled C5L graph (intermediates between its 24 launches) run on 4
+    streams at once with 4 input sets: each stream has its own intermediate
+    set, so every result equals the serial run of the same inputs; fetch reads
+    the intermediate of the run on that stream."""
+    import torch
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, "C5L.small.json"))
+    cg = H.CompiledGraph(ctx, g, rep)
+    try:
+        dev = torch.device("cuda", 0)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(5)
+        sets = []
+        for _ in range(4):
+            ins = [torch.rand(g.at(p).shape, generator=gen, device=dev) * 2 - 1 for p in cg.param_ids]
+            outs = [torch.empty(g.at(o).shape, device=dev) for o in g.outputs]
+            sets.append((ins, outs))
+        ptrs = lambda st: ([t.data_ptr() for t in st[0]], [t.data_ptr() for t in st[1]])  # noqa: E731
+        torch.cuda.synchronize()
+        mid = next(r for k in rep.kernels for r in k.program.roots if r not in g.outputs)
+        s0 = torch.cuda.Stream()
+        serial, serial_mid = [], []
+        for st in sets:
+            cg.run(*ptrs(st), stream=s0.cuda_stream)
+            s0.synchronize()
+            serial.append([t.clone() for t in st[1]])
+            serial_mid.append(cg.fetch(mid, stream=s0.cuda_stream))
+        streams = [torch.cuda.Stream() for _ in range(4)]
+        for rep_i in range(3):
+            for st in sets:
+                for t in st[1]:
+                    t.fill_(float("nan"))
+            torch.cuda.synchronize()
+            for s, st in zip(streams, sets):
+                cg.run(*ptrs(st), stream=s.cuda_stream, cuda_graph=rep_i == 2)
+            torch.cuda.synchronize()
+            for st, ref in zip(sets, serial):
+                for a, b in zip(st[1], ref):
+                    assert torch.equal(a, b)
+            for s, m in zip(streams, serial_mid):
+                assert np.array_equal(cg.fetch(mid, stream=s.cuda_stream), m)
+    finally:
+        cg.close()
