@@ -575,22 +575,47 @@ def run_ours(args):
     h2d = sum(t.numel() * 4 for t in pin_in)
     d2h = sum(t.numel() * 4 for t in pin_out.values())
 
+    # a second pinned output set: consecutive pipelined steps write different host buffers
+    pin_out2 = {o: torch.empty(g.at(o).shape, dtype=torch.float32).pin_memory() for o in g.outputs}
+    out_arr2 = (C.c_void_p * len(g.outputs))(*[pin_out2[o].data_ptr() for o in g.outputs])
+
     def e2e_step():
         H._check(H.lib().sfx_graph_run_host(cg.h, pin_arr, len(pin_in), out_arr, len(g.outputs),
                                              C.c_void_p(stream.cuda_stream)))
 
+    def e2e_step_async(i):
+        H._check(H.lib().sfx_graph_run_host_async(cg.h, pin_arr, len(pin_in), out_arr if i % 2 == 0 else out_arr2,
+                                                   len(g.outputs), C.c_void_p(stream.cuda_stream)))
+
+    def timed_max(fn, n):
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        fn(n)
+        sec = (time.perf_counter() - t0) / n
+        t = torch.tensor([sec], device=red_dev)
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sync_run(n):
+        for _ in range(n):
+            e2e_step()
+
+    def async_run(n):
+        for i in range(n):
+            e2e_step_async(i)
+        stream.synchronize()
+
     e2e_step()
-    if ws > 1:
-        dist.barrier()
+    async_run(2)
     e2e_steps = max(2, min(5, args.steps))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_t = torch.tensor([e2e_s], device=red_dev)
-    if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_s = float(e2e_t.item())
+    e2e_sync_s = timed_max(sync_run, e2e_steps)
+    # headline: consecutive steps pipelined through sfx_graph_run_host_async
+    # (step i+1's host->device copies overlap step i's kernels and copies back);
+    # every step still copies its inputs in and its outputs out
+    e2e_s = timed_max(async_run, max(4, min(10, args.steps)))
+    host_ok = all(torch.equal(pin_out[o], pin_out2[o]) for o in g.outputs)
 
     if rank != 0:
         if ws > 1:
@@ -633,7 +658,11 @@ def run_ours(args):
         "per_kernel": per_kernel,
         "e2e": {"value": total_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                "path": "sfx_graph_run_host (pinned host buffers, H2D + 1 launch per group + D2H)"},
+                "path": "sfx_graph_run_host_async, consecutive steps pipelined (pinned host buffers; every step: "
+                        "H2D of its inputs + 1 launch per group + D2H of its outputs)",
+                "ms_per_step_synchronous": e2e_sync_s * 1e3,
+                "value_synchronous": total_bytes / e2e_sync_s / 1e9,
+                "alternating_output_sets_identical": host_ok},
         "clocks": clocks,
         "cpu_baseline": cpu,
     }

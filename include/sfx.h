@@ -277,6 +277,14 @@ sfx_status sfx_graph_run(sfx_graph* g, const uint64_t* params, int32_t n_params,
  * host->device, runs, copies outputs device->host, synchronizes the stream. */
 sfx_status sfx_graph_run_host(sfx_graph* g, const void* const* params, int32_t n_params,
                               void* const* outputs, int32_t n_outputs, void* stream);
+/* The same run, enqueued without waiting: complete when `stream` is (every
+ * copy stream of the run is joined into it).  The graph stages host runs in
+ * two device slots used alternately, so consecutive async runs overlap (run
+ * i+1's host->device copies under run i's kernels and device->host copies).
+ * Host buffers must be pinned (sfx_host_alloc or cudaHostRegister'ed) and stay
+ * valid until the stream reaches the run. */
+sfx_status sfx_graph_run_host_async(sfx_graph* g, const void* const* params, int32_t n_params,
+                                    void* const* outputs, int32_t n_outputs, void* stream);
 /* Read back a value the latest run on `stream` left in HBM: a group root that
  * is not a graph output (an intermediate between groups) or a dense constant.
  * This is how the binding returns run_compiled's full value map

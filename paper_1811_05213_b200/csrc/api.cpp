@@ -207,14 +207,25 @@ struct sfx_graph {
   std::map<std::vector<uint64_t>, std::map<int, CUdeviceptr>> mids;
   std::map<CUstream, const std::map<int, CUdeviceptr>*> last_mid;
   std::map<std::vector<uint64_t>, std::pair<CUgraph, CUgraphExec>> captured;
-  std::vector<CUdeviceptr> host_bufs;  // staging for sfx_graph_run_host (params then outputs)
+  // Host path staging: two slots (params then outputs, plus the chunk flags),
+  // used alternately, so run i+1's host->device copies land in one slot while
+  // run i's kernels and copies back still use the other.  A slot is reused once
+  // every stream of its previous run is past its last use (free_ev).
+  struct HostSlot {
+    std::vector<CUdeviceptr> bufs;
+    CUdeviceptr flags = 0;          // per kernel: gate[kMaxChunks] + done[kMaxChunks]
+    CUevent free_ev = nullptr;
+    bool used = false;
+  };
+  HostSlot hslot[2];
+  int hnext = 0;
   CUstream d2h = nullptr;              // host path: device->host copies overlap the next groups
   CUstream h2d = nullptr, h2d2 = nullptr;  // host path: host->device copies (chunks alternate)
   CUstream d2h2 = nullptr;                 // second device->host stream (chunks alternate)
-  CUdeviceptr stream_flags = 0;        // per kernel: gate[kMaxChunks] + done[kMaxChunks]
   std::vector<CUstream> branch_streams;  // device path: independent groups run concurrently
   std::vector<CUevent> branch_events;    // per kernel completion, then fork / join
   std::vector<CUevent> events;
+  CUevent join_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // host path: copy streams -> `s`
   std::vector<int> host_order;
 };
 
@@ -1081,25 +1092,30 @@ sfx_status sfx_graph_run(sfx_graph* G, const uint64_t* params, int32_t n_params,
   });
 }
 
-sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n_params, void* const* outputs,
-                              int32_t n_outputs, void* stream) {
-  return guard([&] {
+namespace {
+
+// The host path (sfx_graph_run_host / _async): enqueues one run; on return
+// every stream of the run is joined into `s` (the run is complete when `s` is).
+void host_enqueue(sfx_graph* G, const void* const* params, int32_t n_params, void* const* outputs,
+                  int32_t n_outputs, CUstream s) {
     if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
     if (n_params != static_cast<int32_t>(G->params.size()) ||
         n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
       throw sfx::Error(SFX_ERR_INVALID, "param/output count mismatch");
-    std::lock_guard<std::mutex> lock(G->run_mu);
     G->ctx->bind();
     const sfx::Driver& d = sfx::driver();
-    CUstream s = static_cast<CUstream>(stream);
-    if (G->host_bufs.empty()) {
-      for (int p : G->params) G->host_bufs.push_back(G->ctx->alloc(G->graph.nodes[p].numel() * 4));
-      for (int o : G->graph.outputs) G->host_bufs.push_back(G->ctx->alloc(G->graph.nodes[o].numel() * 4));
-    }
-    std::vector<uint64_t> dp(G->host_bufs.begin(), G->host_bufs.begin() + n_params);
-    std::vector<uint64_t> dout(G->host_bufs.begin() + n_params, G->host_bufs.end());
     const sfx::Graph& g = G->graph;
     const int K = static_cast<int>(G->kernels.size());
+    sfx_graph::HostSlot& slot = G->hslot[G->hnext];
+    G->hnext ^= 1;
+    if (slot.bufs.empty()) {
+      for (int p : G->params) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[p].numel() * 4));
+      for (int o : G->graph.outputs) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[o].numel() * 4));
+      slot.flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
+      sfx::check_cu(d.cuEventCreate(&slot.free_ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    }
+    std::vector<uint64_t> dp(slot.bufs.begin(), slot.bufs.begin() + n_params);
+    std::vector<uint64_t> dout(slot.bufs.begin() + n_params, slot.bufs.end());
     if (!G->d2h) {
       sfx::check_cu(d.cuStreamCreate(&G->d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
       sfx::check_cu(d.cuStreamCreate(&G->h2d, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
@@ -1107,8 +1123,8 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
       sfx::check_cu(d.cuStreamCreate(&G->d2h2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
       G->events.resize(3 * K + 2);
       for (CUevent& e : G->events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+      for (CUevent& e : G->join_ev) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
       G->host_order = host_order(G);
-      G->stream_flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
       G->host_kernels.assign(K, nullptr);
       if (host_streaming() && !G->opts.debug_checks) {  // debug: every launch coverage-checked, whole copies
         sfx_compile_opts ho = G->opts;
@@ -1138,10 +1154,17 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
     // still ONE launch per group.  Other groups: whole copies, ordered by events.
     // Groups that return the most bytes go first (any dependency-respecting
     // order gives the same values).
-    sfx::check_cu(d.cuMemsetD32Async(G->stream_flags, 0, static_cast<size_t>(K) * kFlagWords, s), "cuMemsetD32Async");
+    // This slot's previous run (two runs ago) must be done with its buffers
+    // and flags before anything of this run touches them; the flags are reset
+    // on the first copy stream (not on `s`, whose previous run's kernels would
+    // otherwise hold back this run's copies), and every stream of the run
+    // starts behind the reset.
+    if (slot.used) sfx::check_cu(d.cuStreamWaitEvent(G->h2d, slot.free_ev, 0), "cuStreamWaitEvent");
+    slot.used = true;
+    sfx::check_cu(d.cuMemsetD32Async(slot.flags, 0, static_cast<size_t>(K) * kFlagWords, G->h2d), "cuMemsetD32Async");
     CUevent ev_reset = G->events[3 * K];
-    sfx::check_cu(d.cuEventRecord(ev_reset, s), "cuEventRecord");
-    for (CUstream st : {G->h2d, G->h2d2, G->d2h, G->d2h2})
+    sfx::check_cu(d.cuEventRecord(ev_reset, G->h2d), "cuEventRecord");
+    for (CUstream st : {s, G->h2d2, G->d2h, G->d2h2})
       sfx::check_cu(d.cuStreamWaitEvent(st, ev_reset, 0), "cuStreamWaitEvent");
 
     std::map<int, CUdeviceptr> where = G->owned;
@@ -1209,7 +1232,7 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
           copied[param_slot[in]] = true;
         }
       StreamArgs sa;
-      const CUdeviceptr gate = G->stream_flags + static_cast<uint64_t>(pi) * kFlagWords * 4;
+      const CUdeviceptr gate = slot.flags + static_cast<uint64_t>(pi) * kFlagWords * 4;
       if (streamed) {
         // the whole inputs above precede every chunk gate on both streams
         sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d), "cuEventRecord");
@@ -1276,8 +1299,34 @@ sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n
         sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
       }
     }
-    for (CUstream st : {G->h2d, G->h2d2, s, G->d2h, G->d2h2})
-      sfx::check_cu(d.cuStreamSynchronize(st), "cuStreamSynchronize");
+    // join: `s` waits for every copy stream; the slot is free once `s` is here
+    for (int j = 0; j < 4; ++j) {
+      CUstream st = j == 0 ? G->h2d : j == 1 ? G->h2d2 : j == 2 ? G->d2h : G->d2h2;
+      sfx::check_cu(d.cuEventRecord(G->join_ev[j], st), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(s, G->join_ev[j], 0), "cuStreamWaitEvent");
+    }
+    sfx::check_cu(d.cuEventRecord(slot.free_ev, s), "cuEventRecord");
+}
+
+}  // namespace
+
+sfx_status sfx_graph_run_host(sfx_graph* G, const void* const* params, int32_t n_params, void* const* outputs,
+                              int32_t n_outputs, void* stream) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    std::lock_guard<std::mutex> lock(G->run_mu);
+    CUstream s = static_cast<CUstream>(stream);
+    host_enqueue(G, params, n_params, outputs, n_outputs, s);
+    sfx::check_cu(sfx::driver().cuStreamSynchronize(s), "cuStreamSynchronize");
+  });
+}
+
+sfx_status sfx_graph_run_host_async(sfx_graph* G, const void* const* params, int32_t n_params,
+                                    void* const* outputs, int32_t n_outputs, void* stream) {
+  return guard([&] {
+    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+    std::lock_guard<std::mutex> lock(G->run_mu);
+    host_enqueue(G, params, n_params, outputs, n_outputs, static_cast<CUstream>(stream));
   });
 }
 
@@ -1324,6 +1373,10 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
         d.cuGraphDestroy(ge.first);
       }
       for (CUevent e : G->events) d.cuEventDestroy(e);
+      for (CUevent e : G->join_ev)
+        if (e) d.cuEventDestroy(e);
+      for (auto& sl : G->hslot)
+        if (sl.free_ev) d.cuEventDestroy(sl.free_ev);
       if (G->d2h) d.cuStreamDestroy(G->d2h);
       for (CUstream st : {G->h2d, G->h2d2, G->d2h2})
         if (st) d.cuStreamDestroy(st);
@@ -1331,7 +1384,10 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
       for (CUevent e : G->branch_events) d.cuEventDestroy(e);
     } catch (...) {
     }
-    if (G->stream_flags) G->ctx->release(G->stream_flags);
+    for (auto& sl : G->hslot) {
+      if (sl.flags) G->ctx->release(sl.flags);
+      for (CUdeviceptr p : sl.bufs) G->ctx->release(p);
+    }
     for (auto& [key, ws] : G->captured_ws)
       for (CUdeviceptr w : ws) G->ctx->release(w);
     for (sfx_kernel* k : G->kernels) destroy_kernel(k);
@@ -1339,7 +1395,6 @@ sfx_status sfx_graph_destroy(sfx_graph* G) {
     for (auto& [n, p] : G->owned) G->ctx->release(p);
     for (auto& [key, m] : G->mids)
       for (auto& [n, p] : m) G->ctx->release(p);
-    for (CUdeviceptr p : G->host_bufs) G->ctx->release(p);
     delete G;
   });
 }

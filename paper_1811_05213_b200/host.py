@@ -113,6 +113,7 @@ EXPORTS = [
     "sfx_graph_run_host", "sfx_graph_destroy", "sfx_nccl_unique_id", "sfx_nccl_init",
     "sfx_allreduce_sum_f32", "sfx_peer_create", "sfx_peer_open", "sfx_program_time", "sfx_program_signature",
     "sfx_template_param_has", "sfx_template_param_put", "sfx_template_params_text", "sfx_graph_fetch",
+    "sfx_graph_run_host_async",
 ]
 ABI_VERSION = 2
 PEER_HANDLE_BYTES = 64
@@ -170,6 +171,7 @@ def lib():
         "sfx_template_param_put": (i32, [C.c_char_p, i32, i32, i32, i32, C.c_double, C.c_double, C.c_char_p]),
         "sfx_template_params_text": (i32, [C.c_char_p, u64, C.POINTER(u64)]),
         "sfx_graph_fetch": (i32, [vp, i32, vp, u64, vp]),
+        "sfx_graph_run_host_async": (i32, [vp, C.POINTER(vp), i32, C.POINTER(vp), i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -653,6 +655,13 @@ class CompiledGraph:
         pout = (C.c_void_p * max(len(outputs), 1))(*[outputs[o].ctypes.data for o in self.graph.outputs])
         _check(lib().sfx_graph_run_host(self.h, pin, len(arrs), pout, len(self.graph.outputs), C.c_void_p(stream)))
         return outputs
+
+    def run_host_async(self, param_ptrs, out_ptrs, stream):
+        """sfx_graph_run_host_async: pinned host pointers (param slot order /
+        graph output order), complete when `stream` is."""
+        pin = (C.c_void_p * max(len(param_ptrs), 1))(*[int(p) for p in param_ptrs])
+        pout = (C.c_void_p * max(len(out_ptrs), 1))(*[int(p) for p in out_ptrs])
+        _check(lib().sfx_graph_run_host_async(self.h, pin, len(param_ptrs), pout, len(out_ptrs), C.c_void_p(stream)))
 
     def fetch(self, instr_id: str, stream=0) -> np.ndarray:
         """A value the latest run on `stream` left in HBM (an intermediate group
