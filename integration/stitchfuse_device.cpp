@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <set>
+#include <sstream>
 #include <string>
 #include <variant>
 
@@ -374,55 +375,66 @@ TensorGraph single_instruction_graph(const TensorGraph& g, const Instruction& in
 MeasureStats measure_misses(const TensorGraph& graph, const PipelineOptions& options, PerfLibrary& lib,
                             const CostModelParams& params, int reps, int max_keys) {
   MeasureStats st;
-  PerfLibrary probe = lib;
-  compile_graph(graph, options, probe, params);  // misses become synthetic entries
   sfx_ctx* ctx = context();
   sfx_compile_opts lit{};
   lit.strategy = SFX_STRATEGY_LITERAL;
-  for (const auto& [key, entry] : probe.entries()) {
-    const PerfEntry* have = lib.find(key);
-    if (!entry.synthetic || (have && !have->synthetic)) continue;
-    ++st.keys_missed;
-    if (max_keys >= 0 && st.keys_measured >= max_keys) continue;
-    const Instruction* ins = nullptr;
-    for (const Instruction& i : graph.instructions())
-      if (opcode_name(i) == key.opcode && i.shape.dims == key.shape) {
-        ins = &i;
-        break;
+  // Measured costs move the planner's tuned schedules, and a new schedule is a
+  // new key: re-plan with what was measured and measure the new misses, until a
+  // plan misses nothing new (every miss is measured once, as the paper's
+  // on-miss path does one key at a time).
+  std::set<PerfKey> tried;
+  for (int round = 0; round < 16; ++round) {
+    PerfLibrary probe = lib;
+    compile_graph(graph, options, probe, params);  // misses become synthetic entries
+    bool fresh = false;
+    for (const auto& [key, entry] : probe.entries()) {
+      const PerfEntry* have = lib.find(key);
+      if (!entry.synthetic || (have && !have->synthetic)) continue;
+      if (!tried.insert(key).second) continue;
+      fresh = true;
+      ++st.keys_missed;
+      if (max_keys >= 0 && st.keys_measured >= max_keys) continue;
+      const Instruction* ins = nullptr;
+      for (const Instruction& i : graph.instructions())
+        if (opcode_name(i) == key.opcode && i.shape.dims == key.shape) {
+          ins = &i;
+          break;
+        }
+      if (!ins) continue;
+      try {
+        TensorGraph g1 = single_instruction_graph(graph, *ins);
+        PipelineOptions o1 = options;
+        o1.fuse_dot = true;  // a lone BatchMatMul key is measured as its own group
+        FusionPlan fp = fuse_module(g1, o1);
+        const FusedComputation* comp = nullptr;
+        for (const FusedComputation& c : fp.computations)
+          if (c.members.count(ins->id)) comp = &c;
+        if (!comp) continue;
+        Schedule sched;
+        sched.split_dim = key.split_dim;
+        sched.sword = key.sword;
+        sched.type = key.sched_type;
+        ResolveResult r = resolve_schedule(*comp, g1, {{ins->id, sched}}, o1);
+        if (!r.ok()) continue;
+        SchedulePlan plan = *r.plan;
+        plan.block_threads = key.block_threads;
+        SpanMap sm = compute_span(g1);
+        SmemResult smem = plan_shared_memory(*comp, g1, sm, plan, o1);
+        if (!std::holds_alternative<SharedMemPlan>(smem)) continue;
+        KernelProgram prog = emit_program(*comp, g1, sm, plan, std::get<SharedMemPlan>(smem), o1);
+        Desc d(g1, {&prog});
+        double us = 0;
+        check(sfx_program_time(ctx, &d.desc, 0, &lit, reps, &us, nullptr));
+        PerfEntry e;
+        e.cost_us = us;
+        e.synthetic = false;
+        lib.insert(key, e);
+        ++st.keys_measured;
+      } catch (const std::exception& e) {
+        st.notes.push_back(key.opcode + ": " + e.what());
       }
-    if (!ins) continue;
-    try {
-      TensorGraph g1 = single_instruction_graph(graph, *ins);
-      PipelineOptions o1 = options;
-      o1.fuse_dot = true;  // a lone BatchMatMul key is measured as its own group
-      FusionPlan fp = fuse_module(g1, o1);
-      const FusedComputation* comp = nullptr;
-      for (const FusedComputation& c : fp.computations)
-        if (c.members.count(ins->id)) comp = &c;
-      if (!comp) continue;
-      Schedule sched;
-      sched.split_dim = key.split_dim;
-      sched.sword = key.sword;
-      sched.type = key.sched_type;
-      ResolveResult r = resolve_schedule(*comp, g1, {{ins->id, sched}}, o1);
-      if (!r.ok()) continue;
-      SchedulePlan plan = *r.plan;
-      plan.block_threads = key.block_threads;
-      SpanMap sm = compute_span(g1);
-      SmemResult smem = plan_shared_memory(*comp, g1, sm, plan, o1);
-      if (!std::holds_alternative<SharedMemPlan>(smem)) continue;
-      KernelProgram prog = emit_program(*comp, g1, sm, plan, std::get<SharedMemPlan>(smem), o1);
-      Desc d(g1, {&prog});
-      double us = 0;
-      check(sfx_program_time(ctx, &d.desc, 0, &lit, reps, &us, nullptr));
-      PerfEntry e;
-      e.cost_us = us;
-      e.synthetic = false;
-      lib.insert(key, e);
-      ++st.keys_measured;
-    } catch (const std::exception& e) {
-      st.notes.push_back(key.opcode + ": " + e.what());
     }
+    if (!fresh) break;
   }
   return st;
 }
