@@ -51,7 +51,7 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
 // Persisted, PerfLibrary-style text (reference tuning.cpp:41-125 stores measured
 // schedule costs the same way): one line per group signature
 //   signature|rows_per_cta|threads_per_row|items_per_thread|pipe_ctas_per_sm|tuned_us|default_us|source
-// where signature = <entry>-<fnv64 of the kernel the default options generate>.
+// where signature = sfx_<template>-<fnv64 of the group's structure> (group_signature).
 // tools/autotune.py measures candidate template parameters per group on the
 // B200 and writes the winners; lowering with default options looks the group up
 // and re-lowers with the recorded parameters.  SFX_TEMPLATE_PARAMS=<file>
@@ -104,11 +104,62 @@ bool default_knobs(const sfx_compile_opts& o) {
 
 KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o);
 
+// The cache key of a group: its template (the entry's sfx_<template> prefix)
+// and a hash of what the group computes — members in id order with their
+// opcodes, attributes, shapes and dtypes, operands as member / external slot
+// references, externals' shapes (splat values inline), roots and the
+// cross-rank flag.  Instruction names do not enter, and neither does the
+// generated code, so codegen changes keep the recorded parameters (bump
+// kTemplateParamsVersion when a template's knobs change meaning).
+constexpr const char* kTemplateParamsVersion = "tp2";
+
+std::string group_signature(const Graph& g, int pi, const sfx_compile_opts& o, const std::string& entry) {
+  const Program& p = g.programs.at(pi);
+  // graph instruction order (members / externals are sorted by name otherwise)
+  std::vector<int> members(p.members), externals(p.externals), roots;
+  std::sort(members.begin(), members.end());
+  std::sort(externals.begin(), externals.end());
+  std::map<int, int> local, ext;
+  for (size_t i = 0; i < members.size(); ++i) local[members[i]] = static_cast<int>(i);
+  for (size_t i = 0; i < externals.size(); ++i) ext[externals[i]] = static_cast<int>(i);
+  for (int r : p.roots) roots.push_back(local[r]);
+  std::sort(roots.begin(), roots.end());
+  std::ostringstream os;
+  os << kTemplateParamsVersion << ";x" << (o.cross_rank ? 1 : 0) << ";";
+  auto vec = [&](const std::vector<int64_t>& v) {
+    os << "[";
+    for (int64_t x : v) os << x << ",";
+    os << "]";
+  };
+  for (int e : externals) {
+    const Node& n = g.nodes[e];
+    os << "E" << n.dtype;
+    vec(n.dims);
+    if (n.is_splat()) os << "=" << std::hexfloat << n.literal[0] << std::defaultfloat;
+    os << ";";
+  }
+  for (int m : members) {
+    const Node& n = g.nodes[m];
+    os << "M" << n.op << "." << n.kind << "." << n.dtype << "." << n.reducer << "." << std::hexfloat << n.scalar
+       << std::defaultfloat;
+    vec(n.dims);
+    vec(n.perm);
+    vec(n.dim_map);
+    vec(n.reduce_dims);
+    for (int a : n.operands) os << (local.count(a) ? "m" + std::to_string(local[a]) : "e" + std::to_string(ext[a]));
+    os << ";";
+  }
+  os << "R";
+  for (int r : roots) os << r << ",";
+  const size_t cut = entry.find('_', 4);
+  char hex[32];
+  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(os.str())));
+  return entry.substr(0, cut) + "-" + hex;
+}
+
 std::string kernel_signature(const Graph& g, int pi, const sfx_compile_opts& o) {
   KernelSource ks = lower_program_raw(g, pi, o);
-  char hex[32];
-  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(ks.code)));
-  return ks.entry + "-" + hex;
+  return group_signature(g, pi, o, ks.entry);
 }
 
 bool template_param_find(const std::string& sig) {
@@ -146,9 +197,7 @@ std::string template_params_text() {
 
 KernelSource lower_program(const Graph& g, int pi, const sfx_compile_opts& o) {
   KernelSource ks = lower_program_raw(g, pi, o);
-  char hex[32];
-  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a64(ks.code)));
-  const std::string sig = ks.entry + "-" + hex;
+  const std::string sig = group_signature(g, pi, o, ks.entry);
   if (default_knobs(o)) {
     TunedParams tp;
     bool hit = false;

@@ -89,7 +89,7 @@ def test_degenerate_reduce_is_a_reshape():
 
 def test_template_parameter_cache(tmp_path):
     """The template parameter cache (tools/autotune.py output, PerfLibrary-style
-    text) is keyed by the default kernel's signature: a listed group is re-lowered
+    text) is keyed by the group signature (template + structure): a listed group is re-lowered
     with its recorded parameters, other shapes keep the defaults.  The committed
     cache is empty after the round-1 sweep (no candidate beat the defaults in the
     benchmark's mode), so the entry here is written for the test."""
@@ -146,3 +146,16 @@ def test_tiled_transpose_is_vectorised():
     assert sass.count("LDG.E.NA.128") == 4 and sass.count("STS.128") == 4 and sass.count("STG.E.EF.128") == 4
     _, _, note = _note(os.path.join(EXTRA, "tr_8x301x141.json"))
     assert "smem-tiled" in note and "XOR" not in note
+
+
+def test_template_cache_key_is_the_group_structure(tmp_path):
+    """The cache key is the group's template and structure (ops, shapes,
+    operand wiring, roots), not instruction names or generated code: renaming
+    every LayerNorm instruction keeps the key, a different shape changes it."""
+    text = open(os.path.join(T.PLANS, "C1.full.json")).read()
+    renamed = tmp_path / "renamed.json"
+    renamed.write_text(text.replace('"ln.', '"zz_norm.').replace("ln.", "zz_norm."))
+    sig = lambda p: _note(p)[2].rsplit("sig=", 1)[1].strip()  # noqa: E731
+    a, b = sig(os.path.join(T.PLANS, "C1.full.json")), sig(str(renamed))
+    assert a == b and a.startswith("sfx_row-"), (a, b)
+    assert sig(os.path.join(T.PLANS, "C1.small.json")) != a
