@@ -78,6 +78,15 @@ def main():
             torch.cuda.synchronize()
             ms = sorted(a.elapsed_time(b) for a, b in ev)
             med = ms[len(ms) // 2]
+            # back to back (PDL-chained launches, as in bench.py's per-kernel figure)
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(s)
+            for i in range(reps):
+                ins, outs = sets[i % nsets]
+                k.launch([t.data_ptr() for t in ins], [t.data_ptr() for t in outs], s.cuda_stream)
+            b1.record(s)
+            torch.cuda.synchronize()
+            b2b = b0.elapsed_time(b1) / reps
             gbs = k.info["algorithmic_bytes"] / (med * 1e-3) / 1e9
             # same-size copy (torch copy_ of half the algorithmic bytes each way),
             # the achievable single-launch bandwidth at this size
@@ -97,6 +106,8 @@ def main():
             print(json.dumps({"config": cfg, "variant": var, "group": kp.program.fusion_root,
                               "kernel": k.info["entry"], "regs": k.info["registers"], "grid": k.info["grid"],
                               "smem": k.info["smem_bytes"], "median_us": round(med * 1e3, 2),
+                              "b2b_us": round(b2b * 1e3, 2),
+                              "b2b_frac": round(k.info["algorithmic_bytes"] / (b2b * 1e-3) / 1e9 / peak, 3),
                               "gbs": round(gbs), "frac": round(gbs / peak, 3),
                               "same_size_copy_us": round(cmed * 1e3, 2),
                               "vs_same_size_copy": round(cmed / med, 3), "parity_ok": ok}), flush=True)
