@@ -48,7 +48,7 @@ extern "C" {
 #endif
 
 #define SFX_MAX_RANK 8
-#define SFX_ABI_VERSION 2
+#define SFX_ABI_VERSION 3
 
 typedef int32_t sfx_status; /* 0 = ok */
 enum {
@@ -113,6 +113,18 @@ typedef struct sfx_stmt {
   int32_t root_index; /* output */
 } sfx_stmt;
 
+/* The geometry the reference executor READS a materialised member with
+ * (exec.cpp:320-324): KernelProgram.arena_offsets and
+ * SchedulePlan.per_instruction.  Writes use the statement's own schedule and
+ * destination; a program whose reads and writes disagree is what the
+ * executor's stale-read / containment checks reject. */
+typedef struct sfx_member_plan {
+  int64_t arena_offset;  /* -1: not in the arena */
+  int64_t split_dim;
+  int64_t sword;
+  int32_t sched_type;    /* SFX_SCHED_* */
+} sfx_member_plan;
+
 typedef struct sfx_program {
   int32_t n_members;
   const int32_t* members;     /* FusedComputation.members */
@@ -124,6 +136,7 @@ typedef struct sfx_program {
   int64_t arena_bytes;        /* KernelProgram.arena_bytes */
   int32_t n_stmts;
   const sfx_stmt* stmts;      /* KernelProgram.statements */
+  const sfx_member_plan* member_plans; /* per member (members[] order); NULL = the statements' geometry */
 } sfx_program;
 
 typedef struct sfx_graph_desc {

@@ -50,6 +50,7 @@ struct Desc {
   std::vector<int32_t> outputs;
   std::vector<std::vector<int32_t>> members, roots;
   std::vector<std::vector<sfx_stmt>> stmts;
+  std::vector<std::vector<sfx_member_plan>> plans;
   std::vector<sfx_program> programs;
   std::map<InstrId, int32_t> index;
   sfx_graph_desc desc{};
@@ -132,6 +133,23 @@ struct Desc {
       sp.arena_bytes = p->arena_bytes;
       sp.n_stmts = static_cast<int32_t>(stmts[k].size());
       sp.stmts = stmts[k].data();
+      // the geometry reads use (exec.cpp:320-324), per member
+      plans.emplace_back();
+      for (const InstrId& m : p->comp.members) {
+        sfx_member_plan mp{};
+        auto off = p->arena_offsets.find(m);
+        mp.arena_offset = off == p->arena_offsets.end() ? -1 : off->second;
+        auto sc = p->plan.per_instruction.find(m);
+        if (sc != p->plan.per_instruction.end()) {
+          mp.split_dim = sc->second.split_dim;
+          mp.sword = sc->second.sword;
+          mp.sched_type = sc->second.type == SchedType::Row ? SFX_SCHED_ROW : SFX_SCHED_COL;
+        } else {
+          mp.sword = 1;
+        }
+        plans.back().push_back(mp);
+      }
+      sp.member_plans = plans.back().data();
       programs.push_back(sp);
     }
     desc.n_instrs = static_cast<int32_t>(instrs.size());
@@ -162,10 +180,12 @@ struct Desc {
       sfx_program sp = programs[p];
       sp.members = sp.roots = nullptr;
       sp.stmts = nullptr;
+      sp.member_plans = nullptr;
       put(&sp, sizeof sp);
       put(members[p].data(), members[p].size() * sizeof(int32_t));
       put(roots[p].data(), roots[p].size() * sizeof(int32_t));
       put(stmts[p].data(), stmts[p].size() * sizeof(sfx_stmt));
+      put(plans[p].data(), plans[p].size() * sizeof(sfx_member_plan));
     }
     return k;
   }

@@ -20,6 +20,9 @@
 //        the measured perf library: misses measured on the device, re-plan hits
 //   device_parity cache
 //        the binding's compiled-plan cache: one compile per plan signature
+//   device_parity selfchecks
+//        test_exec.cpp:157-194: the reference's corrupted programs throw
+//        ExecError from both executors, with the same message
 // Prints one JSON line; exit 0 iff every eligible case passed.
 #include <chrono>
 #include <cstdlib>
@@ -444,6 +447,71 @@ int cmd_cache() {
   return finish("binding cache", t, 0);
 }
 
+// The executor self-checks: each corrupted program (the reference's own two
+// from test_exec.cpp:157-194, plus an overlapping root write and a containment
+// violation) must make both run_program implementations throw ExecError, and
+// the device binding's message must carry the reference's.
+int cmd_selfchecks() {
+  Tally t;
+  CostModelParams params;
+  auto plan = [&](const std::string& fixture, bool fuse_dot) {
+    PipelineOptions o;
+    o.fuse_dot = fuse_dot;
+    PerfLibrary lib;
+    TensorGraph g = parse_graph(fixture_graphs().at(fixture));
+    return std::make_pair(g, compile_graph(g, o, lib, params));
+  };
+  auto expect = [&](const std::string& name, const TensorGraph& g, const KernelProgram& prog, uint64_t seed) {
+    ++t.cases;
+    std::mt19937_64 rng(seed);
+    auto inputs = testsupport::random_inputs(g, rng);
+    std::map<InstrId, TensorValue> ext;
+    for (const InstrId& m : prog.comp.members)
+      for (const InstrId& op : g.at(m).operands)
+        if (!prog.comp.members.count(op)) ext[op] = inputs.count(op) ? inputs.at(op) : constant_value(g.at(op));
+    std::string ref_msg, dev_msg;
+    try {
+      run_program(prog, g, ext);
+    } catch (const ExecError& e) {
+      ref_msg = e.what();
+    }
+    try {
+      stitchfuse_device::run_program(prog, g, ext);
+    } catch (const ExecError& e) {
+      dev_msg = e.what();
+    }
+    if (ref_msg.empty()) t.fail(name + ": the reference did not throw");
+    else if (dev_msg.find(ref_msg) == std::string::npos) t.fail(name + ": reference '" + ref_msg + "', device '" + dev_msg + "'");
+    else ++t.passed;
+  };
+  {
+    auto [g, rep] = plan("softmax_batchdot", true);
+    KernelProgram p = rep.kernels[0].program;
+    for (Statement& st : p.statements)  // test_exec.cpp:165-169
+      if (auto* mat = std::get_if<MaterializeStmt>(&st))
+        if (auto* sh = std::get_if<SharedDest>(&mat->dest))
+          if (mat->instr == "Reduce.1" || mat->instr == "Reduce.2") sh->offset = 0;
+    expect("stale arena read", g, p, 105);
+    KernelProgram q = rep.kernels[0].program;
+    q.plan.per_instruction.at("Exponential.1").sword *= 2;
+    expect("chunk containment", g, q, 105);
+  }
+  {
+    auto [g, rep] = plan("elementwise_chain", false);
+    KernelProgram p = rep.kernels[0].program;
+    for (Statement& st : p.statements)  // test_exec.cpp:183-187
+      if (auto* mat = std::get_if<MaterializeStmt>(&st))
+        if (std::holds_alternative<OutputDest>(mat->dest) && mat->schedule.sword > 1) mat->schedule.sword *= 2;
+    expect("incomplete coverage", g, p, 107);
+    KernelProgram q = rep.kernels[0].program;
+    for (Statement& st : q.statements)
+      if (auto* mat = std::get_if<MaterializeStmt>(&st))
+        if (std::holds_alternative<OutputDest>(mat->dest)) mat->schedule.sword /= 2;
+    expect("overlapping root write", g, q, 107);
+  }
+  return finish("executor self-checks", t, 0);
+}
+
 std::vector<std::pair<InstrId, std::set<InstrId>>> membership(const CompileReport& r) {
   std::vector<std::pair<InstrId, std::set<InstrId>>> m;
   for (const CompiledKernel& k : r.kernels) m.push_back({k.comp.fusion_root, k.comp.members});
@@ -507,6 +575,7 @@ int main(int argc, char** argv) {
     if (cmd == "crit9") return cmd_crit9();
     if (cmd == "crit7") return cmd_crit7();
     if (cmd == "cache") return cmd_cache();
+    if (cmd == "selfchecks") return cmd_selfchecks();
     if (cmd == "perflib")
       return cmd_perflib(pos.at(1), pos.at(2), pos.at(3), pos.size() > 4 ? std::stoi(pos[4]) : -1);
     if (cmd == "shrink") return cmd_shrink(pos.size() > 1 ? std::stoull(pos[1]) : 7, pos.size() > 2 ? std::stoi(pos[2]) : 30);

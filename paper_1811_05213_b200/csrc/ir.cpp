@@ -252,9 +252,119 @@ Graph graph_from_desc(const sfx_graph_desc* d) {
       available.insert(st.instr);
     }
     if (roots_written.size() != pr.roots.size()) bad("not all roots written");
+    for (const Stmt& st : pr.stmts)
+      if (st.kind == SFX_STMT_MATERIALIZE) {
+        Program::ReadPlan rp;
+        rp.offset = st.dest == SFX_DEST_SHARED ? st.offset : -1;
+        rp.split_dim = st.split_dim;
+        rp.sword = st.sword;
+        rp.sched = st.sched;
+        pr.reads[st.instr] = rp;
+      }
+    if (sp.member_plans)
+      for (int k = 0; k < sp.n_members; ++k) {
+        const sfx_member_plan& mp = sp.member_plans[k];
+        Program::ReadPlan rp;
+        rp.offset = mp.arena_offset;
+        rp.split_dim = mp.split_dim;
+        rp.sword = mp.sword;
+        rp.sched = mp.sched_type;
+        if (pr.reads.count(sp.members[k])) pr.reads[sp.members[k]] = rp;
+      }
+    check_executor_geometry(g, pr);
     g.programs.push_back(std::move(pr));
   }
   return g;
+}
+
+// The reference executor's run-time self-checks (exec.cpp:320-327, 399, 410)
+// depend only on the program's geometry, never on data, so they are decided
+// here, once, with the reference's messages and in the order its block loop
+// would hit them: reads of arena members in block 0 (containment, then stale
+// owner bytes), then a root overlap (a later block repeating a box), then
+// incomplete coverage after the last block.
+void check_executor_geometry(const Graph& g, const Program& pr) {
+  auto blocks_of = [&](const Node& n, int64_t sd, int64_t sword, int sched) {
+    int64_t prod = 1;
+    if (n.rank() == 0) return int64_t{1};
+    if (sched == SFX_SCHED_ROW)
+      for (int64_t i = 0; i < sd; ++i) prod *= n.dims[i];
+    else
+      for (int64_t i = sd + 1; i < n.rank(); ++i) prod *= n.dims[i];
+    return sword * prod;
+  };
+  auto box_elems = [&](const Node& n, int64_t sd, int64_t sword, int sched) {
+    if (n.rank() == 0) return int64_t{1};
+    int64_t e = n.dims[sd] / sword;
+    if (sched == SFX_SCHED_ROW)
+      for (int64_t i = sd + 1; i < n.rank(); ++i) e *= n.dims[i];
+    else
+      for (int64_t i = 0; i < sd; ++i) e *= n.dims[i];
+    return e;
+  };
+  for (const Stmt& st : pr.stmts) {
+    if (st.kind != SFX_STMT_MATERIALIZE) continue;
+    const Node& n = g.nodes[st.instr];
+    if (n.rank() > 0 && (st.split_dim < 0 || st.split_dim >= n.rank() || st.sword < 1))
+      throw Error(SFX_ERR_INVALID, "invalid schedule for " + n.id);
+  }
+  std::vector<int> owner(static_cast<size_t>(std::max<int64_t>(pr.arena_bytes, 0)), -1);
+  std::set<int> ready;
+  std::map<int, const Stmt*> written;  // the (shared) statement that materialised a ready member
+  std::string overlap, coverage;
+  for (const Stmt& st : pr.stmts) {
+    if (st.kind != SFX_STMT_MATERIALIZE) continue;
+    // ready members this statement's evaluation reads (eval_element recursion)
+    std::set<int> seen, reads;
+    std::vector<int> stack{st.instr};
+    while (!stack.empty()) {
+      int m = stack.back();
+      stack.pop_back();
+      if (!pr.is_member(m) || !seen.insert(m).second) continue;
+      if (ready.count(m)) {
+        reads.insert(m);
+        continue;
+      }
+      for (int op : g.nodes[m].operands) stack.push_back(op);
+    }
+    for (int r : reads) {
+      const Node& rn = g.nodes[r];
+      const Program::ReadPlan& rp = pr.reads.at(r);
+      const Stmt& wp = *written.at(r);
+      if (rp.split_dim != wp.split_dim || rp.sword != wp.sword || rp.sched != wp.sched)
+        throw Error(SFX_ERR_EXEC, "chunk containment violation reading " + rn.id);
+      const int64_t len = box_elems(rn, rp.split_dim, rp.sword, rp.sched) * 4;
+      if (rp.offset < 0 || rp.offset + len > static_cast<int64_t>(owner.size()))
+        throw Error(SFX_ERR_EXEC, "stale arena read of " + rn.id);
+      for (int64_t b = rp.offset; b < rp.offset + len; ++b)
+        if (owner[b] != r) throw Error(SFX_ERR_EXEC, "stale arena read of " + rn.id);
+    }
+    const Node& n = g.nodes[st.instr];
+    if (st.dest == SFX_DEST_SHARED) {
+      // a shared write drops ready members whose (read) buffers it overlaps
+      const int64_t bytes = box_elems(n, st.split_dim, st.sword, st.sched) * 4;
+      for (auto it = ready.begin(); it != ready.end();) {
+        const Program::ReadPlan& rp = pr.reads.at(*it);
+        const int64_t len = g.nodes[*it].numel() / pr.blocks * 4;
+        if (*it != st.instr && rp.offset < st.offset + bytes && st.offset < rp.offset + len)
+          it = ready.erase(it);
+        else
+          ++it;
+      }
+      if (st.offset + bytes > static_cast<int64_t>(owner.size()))
+        throw Error(SFX_ERR_INVALID, "arena overflow for " + n.id);
+      for (int64_t b = st.offset; b < st.offset + bytes; ++b) owner[b] = st.instr;
+      ready.insert(st.instr);
+      written[st.instr] = &st;
+    } else {
+      const int64_t nb = blocks_of(n, st.split_dim, st.sword, st.sched);
+      if (nb < pr.blocks && overlap.empty()) overlap = "overlapping write to root " + n.id;
+      if ((nb > pr.blocks || (n.rank() > 0 && n.dims[st.split_dim] % st.sword)) && coverage.empty())
+        coverage = "incomplete coverage of root " + n.id;
+    }
+  }
+  if (!overlap.empty()) throw Error(SFX_ERR_EXEC, overlap);
+  if (!coverage.empty()) throw Error(SFX_ERR_EXEC, coverage);
 }
 
 }  // namespace sfx

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -63,6 +64,13 @@ struct Program {
   // an unfused matmul barrier run as its own kernel (not a planned group;
   // members = roots = {the matmul}, no statements)
   bool barrier = false;
+  // read geometry per materialised member (sfx_member_plan; defaults to the
+  // member's statement): arena offset and schedule the executor reads with
+  struct ReadPlan {
+    int64_t offset = -1, split_dim = 0, sword = 1;
+    int sched = SFX_SCHED_ROW;
+  };
+  std::map<int, ReadPlan> reads;
   bool is_member(int n) const { return member_set.count(n) > 0; }
 };
 
@@ -76,6 +84,11 @@ struct Graph {
 // Builds and validates the internal graph (shape rules of reference ir.cpp:215-323,
 // program structure of kernelgen.cpp:75-104).  Throws sfx::Error.
 Graph graph_from_desc(const sfx_graph_desc* desc);
+
+// The reference executor's geometry self-checks (stale arena read, chunk
+// containment, overlapping root write, incomplete coverage; exec.cpp:320-327,
+// 399, 410), decided at lowering time.  Throws sfx::Error(SFX_ERR_EXEC).
+void check_executor_geometry(const Graph& g, const Program& p);
 
 const char* ew_name(int kind);
 int ew_arity(int kind);

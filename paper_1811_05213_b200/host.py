@@ -73,12 +73,16 @@ class SfxStmt(C.Structure):
     ]
 
 
+class SfxMemberPlan(C.Structure):
+    _fields_ = [("arena_offset", C.c_int64), ("split_dim", C.c_int64), ("sword", C.c_int64), ("sched_type", C.c_int32)]
+
+
 class SfxProgram(C.Structure):
     _fields_ = [
         ("n_members", C.c_int32), ("members", C.POINTER(C.c_int32)), ("n_roots", C.c_int32),
         ("roots", C.POINTER(C.c_int32)), ("fusion_root", C.c_int32), ("blocks", C.c_int64),
         ("block_threads", C.c_int32), ("arena_bytes", C.c_int64), ("n_stmts", C.c_int32),
-        ("stmts", C.POINTER(SfxStmt)),
+        ("stmts", C.POINTER(SfxStmt)), ("member_plans", C.POINTER(SfxMemberPlan)),
     ]
 
 
@@ -115,7 +119,7 @@ EXPORTS = [
     "sfx_template_param_has", "sfx_template_param_put", "sfx_template_params_text", "sfx_graph_fetch",
     "sfx_graph_run_host_async",
 ]
-ABI_VERSION = 2
+ABI_VERSION = 3
 PEER_HANDLE_BYTES = 64
 PEER_MAX_RANKS = 8
 
@@ -309,6 +313,11 @@ class KernelProgram:
     arena_bytes: int
     statements: list   # dicts as exported by ref_tool
     dump: str = ""
+    # the geometry the executor reads members with (KernelProgram.arena_offsets,
+    # SchedulePlan.per_instruction: id -> [split_dim, sword, "row"|"col"]); None =
+    # the statements' own
+    arena_offsets: dict | None = None
+    per_instruction: dict | None = None
 
 
 @dataclass
@@ -332,7 +341,8 @@ class CompileReport:
             ks.append(CompiledKernel(KernelProgram(
                 fusion_root=k["fusion_root"], members=list(k["members"]), roots=list(k["roots"]),
                 blocks=int(k["blocks"]), block_threads=int(k["block_threads"]),
-                arena_bytes=int(k["arena_bytes"]), statements=list(k["statements"]), dump=k.get("dump", ""))))
+                arena_bytes=int(k["arena_bytes"]), statements=list(k["statements"]), dump=k.get("dump", ""),
+                arena_offsets=k.get("arena_offsets"), per_instruction=k.get("per_instruction"))))
         return CompileReport(ks, bundle["baseline_kernels"], bundle["fused_kernels"], bundle["fusion_ratio"],
                              list(bundle.get("unfused", [])))
 
@@ -412,6 +422,15 @@ class GraphDesc:
                     else:
                         t.dest, t.root_index = 1, int(st["root_index"])
             self._keep += [mem, roots, stmts]
+            if prog.arena_offsets is not None and prog.per_instruction is not None:
+                plans = (SfxMemberPlan * len(prog.members))()
+                for mi, m in enumerate(prog.members):
+                    sd, sw, ty = prog.per_instruction.get(m, [0, 1, "row"])
+                    plans[mi].arena_offset = int(prog.arena_offsets.get(m, -1))
+                    plans[mi].split_dim, plans[mi].sword = int(sd), int(sw)
+                    plans[mi].sched_type = 0 if ty == "row" else 1
+                self._keep.append(plans)
+                sp.member_plans = C.cast(plans, C.POINTER(SfxMemberPlan))
             sp.n_members, sp.members = len(prog.members), C.cast(mem, C.POINTER(C.c_int32))
             sp.n_roots, sp.roots = len(prog.roots), C.cast(roots, C.POINTER(C.c_int32))
             sp.fusion_root = idx[prog.fusion_root] if prog.fusion_root in idx else -1

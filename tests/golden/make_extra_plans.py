@@ -150,20 +150,32 @@ def two_cross_rank_groups(rows=2048, cols=256, count=4096):
 XRANK = {"two_xrank_shard_2048x256": two_cross_rank_groups()}
 
 
+def fixture_plans():
+    """The reference's own fixture graphs (tests/golden/fixtures, fixtures.cpp)
+    as planned by its tests: softmax_batchdot with fuse_dot (test_exec.cpp:157-174),
+    elementwise_chain with default options (:176-194)."""
+    fix = os.path.join(HERE, "fixtures")
+    return {"softmax_batchdot_fusedot": (json.load(open(os.path.join(fix, "softmax_batchdot.json"))), ["--fuse-dot"]),
+            "elementwise_chain": (json.load(open(os.path.join(fix, "elementwise_chain.json"))), [])}
+
+
 def main():
     tool = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
-    for sub, table in (("plans_extra", EXTRA), ("plans_xrank", XRANK)):
+    for sub, table in (("plans_extra", EXTRA), ("plans_xrank", XRANK), ("plans_fixtures", fixture_plans())):
         export(tool, os.path.join(HERE, sub), table)
 
 
 def export(tool, out_dir, table):
     os.makedirs(out_dir, exist_ok=True)
     for name, doc in table.items():
+        flags = []
+        if isinstance(doc, tuple):
+            doc, flags = doc
         with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
             f.write(configs.dumps(doc))
             path = f.name
         try:
-            out = subprocess.run([tool, "plan", path], check=True, capture_output=True, text=True).stdout
+            out = subprocess.run([tool, "plan", path] + flags, check=True, capture_output=True, text=True).stdout
         finally:
             os.unlink(path)
         b = json.loads(out)

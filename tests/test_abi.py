@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", H.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sfx_\w+)", out))
     assert set(names) <= exported
-    assert L.sfx_abi_version() == H.ABI_VERSION == 2
+    assert L.sfx_abi_version() == H.ABI_VERSION == 3
 
 
 def test_ctx_create_without_gpu_fails_loudly():
@@ -241,7 +241,7 @@ def test_ctypes_mirror_matches_c_struct_layout(tmp_path):
     (sizes and offsets as the C compiler lays them out)."""
     import ctypes as C
     structs = {
-        "sfx_instr": H.SfxInstr, "sfx_stmt": H.SfxStmt, "sfx_program": H.SfxProgram,
+        "sfx_instr": H.SfxInstr, "sfx_stmt": H.SfxStmt, "sfx_program": H.SfxProgram, "sfx_member_plan": H.SfxMemberPlan,
         "sfx_graph_desc": H.SfxGraphDesc, "sfx_compile_opts": H.SfxCompileOpts, "sfx_kernel_info": H.SfxKernelInfo,
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sfx.h"', "int main(void) {"]

@@ -385,6 +385,7 @@ DEVICE_PARITY = os.path.join(T.ROOT, "oracle", "_ref", "device_parity")
     ["crit9"],                  # acceptance criterion 9: 50 fuse_dot runs, coverage-checked
     ["crit7"],                  # acceptance criterion 7: shrunk fuse_dot fixture
     ["cache"],                  # the binding compiles each plan once (signature cache)
+    ["selfchecks"],             # test_exec.cpp:157-194: corrupted programs throw, same messages
 ])
 def test_reference_suites_through_device_binding(args):
     """The reference's own test loops (its random graphs, its inputs, its
