@@ -487,7 +487,9 @@ MeasureStats tune_templates(const CompileReport& report, const TensorGraph& grap
       for (int u : {1, 2, 4, 8}) cand(0, 0, u, 0);
     } else if (strategy == "row") {
       for (int t : {32, 64, 128, 256}) cand(0, t, 0, 0);
-      for (int r : {1, 2}) cand(r, 0, 0, 0);
+      for (int r : {1, 2, 4}) cand(r, 0, 0, 0);
+      for (int t : {64, 128})
+        for (int r : {1, 4}) cand(r, t, 0, 0);
     } else if (strategy == "col") {
       cand(0, 0, 24, 1), cand(0, 0, 32, 1), cand(0, 0, 8, 2), cand(0, 0, 12, 3);
     } else {

@@ -24,7 +24,8 @@ from paper_1811_05213_b200 import host as H  # noqa: E402
 
 CANDIDATES = {
     "map": [dict(items_per_thread=u) for u in (1, 2, 4, 8)],
-    "row": [dict(threads_per_row=t) for t in (32, 64, 128, 256)] + [dict(rows_per_cta=r) for r in (1, 2)],
+    "row": [dict(threads_per_row=t) for t in (32, 64, 128, 256)] + [dict(rows_per_cta=r) for r in (1, 2, 4)]
+           + [dict(threads_per_row=t, rows_per_cta=r) for t in (64, 128) for r in (1, 4)],
     "col": [dict(pipe_ctas_per_sm=m, items_per_thread=u) for m, u in ((1, 24), (1, 32), (2, 8), (3, 12))],
 }
 
