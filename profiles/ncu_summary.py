@@ -39,6 +39,9 @@ METRICS = {
     "smem_wavefronts_ld": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
     "smem_wavefronts_st": "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
     "occ_theory": "sm__maximum_warps_per_active_cycle_pct",
+    # L2 write sectors from the SMs: the kernel's stores even when the output
+    # is still in L2 (not yet written back to DRAM) when the capture ends
+    "l2_wr_sectors": "lts__t_sectors_srcunit_tex_op_write.sum",
 }
 
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "ms": 1e3, "ns": 1e-3, "s": 1e6}
@@ -86,19 +89,25 @@ def main():
     lines = [f"# ncu --set full summary ({args.tag})", "",
              f"source: `{os.path.basename(args.rep)}` (ncu --set full --clock-control none, cold cache, "
              "serialised replay; compare shares, not absolutes)", "",
-             "| kernel | dur us | DRAM rd MB | DRAM wr MB | DRAM GB/s | traffic/algo | DRAM % | SM % | occupancy achieved / theoretical % | smem bank conflicts ld / st (wavefronts) | regs | grid | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "`L2 wr MB` = lts__t_sectors_srcunit_tex_op_write × 32 B: the kernel's stores as L2 sees them, "
+             "so `(DRAM rd + L2 wr) / algo` confirms full writes even when the output is still in L2 "
+             "(not yet in DRAM) when the capture ends.", "",
+             "| kernel | dur us | DRAM rd MB | DRAM wr MB | L2 wr MB | DRAM GB/s | traffic/algo | (DRAM rd + L2 wr)/algo | DRAM % | SM % | occupancy achieved / theoretical % | smem bank conflicts ld / st (wavefronts) | regs | grid | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic_path = os.path.join(HERE, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for d in rows:
         t = d.get("dram_rd", 0) + d.get("dram_wr", 0)
         a = algo.get(d["kernel"])
         ratio = f"{t / a:.3f}" if a else "-"
+        l2w = d.get("l2_wr_sectors", 0) * 32
+        ratio2 = f"{(d.get('dram_rd', 0) + l2w) / a:.3f}" if a else "-"
         gbs = t / (d["dur_us"] * 1e3) if d.get("dur_us") else 0.0
         bc = (f"{int(d.get('bank_conflicts_ld', 0))} / {int(d.get('bank_conflicts_st', 0))} "
               f"({int(d.get('smem_wavefronts_ld', 0))} / {int(d.get('smem_wavefronts_st', 0))})")
         lines.append(f"| {d['kernel']} | {d.get('dur_us', 0):.1f} | {d.get('dram_rd', 0) / 1e6:.1f} | "
-                     f"{d.get('dram_wr', 0) / 1e6:.1f} | {gbs:.0f} | {ratio} | {d.get('dram_pct', 0):.1f} | "
+                     f"{d.get('dram_wr', 0) / 1e6:.1f} | {l2w / 1e6:.1f} | {gbs:.0f} | {ratio} | {ratio2} | "
+                     f"{d.get('dram_pct', 0):.1f} | "
                      f"{d.get('sm_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} / {d.get('occ_theory', 0):.1f} | {bc} | "
                      f"{int(d.get('regs', 0))} | {int(d.get('grid', 0))} | "
                      + ", ".join(f"{k} {v:.1f}" for k, v in d["stalls"]) + " |")

@@ -91,8 +91,9 @@ def test_template_parameter_cache(tmp_path):
     """The template parameter cache (tools/autotune.py output, PerfLibrary-style
     text) is keyed by the group signature (template + structure): a listed group is re-lowered
     with its recorded parameters, other shapes keep the defaults.  The committed
-    cache is empty after the round-1 sweep (no candidate beat the defaults in the
-    benchmark's mode), so the entry here is written for the test."""
+    cache records the defaults as measured winners for every named group (no
+    candidate beat them in the benchmark's mode), so the entry here is written
+    for the test."""
     _, _, note = _note(os.path.join(T.PLANS, "C1.full.json"))
     sig = note.rsplit("sig=", 1)[1].strip()
     cache = tmp_path / "template_params.txt"

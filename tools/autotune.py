@@ -87,6 +87,7 @@ def main():
     lines = ["# template parameter cache: signature|rows_per_cta|threads_per_row|items_per_thread|"
              "pipe_ctas_per_sm|tuned_us|default_us|source",
              "# written by tools/autotune.py on one B200 (back-to-back launch averages, rotating buffer sets > 3x L2)"]
+    done = set()
     for cfg in configs:
         g, rep, _ = H.load_bundle(os.path.join(ROOT, "workloads", "plans", f"{cfg}.full.json"))
         for kp in rep.kernels:
@@ -94,8 +95,9 @@ def main():
             _, _, note = H.codegen(g, prog)
             strategy = note.split()[0]
             sig = note.rsplit("sig=", 1)[1].strip()
-            if strategy not in CANDIDATES:
+            if strategy not in CANDIDATES or sig in done:  # same group structure (C5 h1 / h2): measured once
                 continue
+            done.add(sig)
             base = H.Kernel(ctx, g, prog)
             ids = list(base.input_ids)
             per_set = sum(g.at(i).numel() * 4 for i in ids) + sum(g.at(r).numel() * 4 for r in prog.roots)
@@ -120,15 +122,18 @@ def main():
                 if same and t < best[0]:
                     best = (t, kw)
             # small groups run with instances in flight in the benchmark: the
-            # winner must not lose there (a kernel that is faster alone can draw
-            # more power and lose under the power cap)
+            # winner must win there too, by >= 1% in this short burst (a kernel
+            # that is faster alone can draw more power and lose under the
+            # sustained power cap: C1 at 4 warps per row ties here, 10.34 vs
+            # 10.40 us, and loses 3% of the benchmark value at an SM clock
+            # 100 MHz lower, profiles/README.md)
             if best[1] is not None and per_set < (512 << 20) and len(sets) >= 4:
                 k = H.Kernel(ctx, g, prog, **best[1])
                 ti_best, ti_base = timed_inflight(k, sets), timed_inflight(base, sets)
                 k.close()
                 print(cfg, prog.fusion_root, "in flight", best[1], round(ti_best, 2), "default", round(ti_base, 2),
                       flush=True)
-                if ti_best > 1.01 * ti_base:
+                if ti_best > 0.99 * ti_base:
                     best = (t0, None)
             base.close()
             if best[1] is not None and best[0] < 0.98 * t0:
