@@ -36,3 +36,24 @@ for case in P._eligible("pipeline")[:12]:
     assert not P._check(g, outs, inputs)
     n += 1
 print("random graphs", n, "ok")
+# round 2: pipelined host runs (two staging slots, flags reset on the copy
+# stream) and the full value map (intermediates read back from HBM)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+for name in ("C1.small", "C5.small"):
+    g, rep, _ = H.load_bundle(os.path.join(T.PLANS, name + ".json"))
+    cg = H.CompiledGraph(ctx, g, rep)
+    inp = T.gen_inputs(g, 3, -1.0, 1.0)
+    want = cg.run_host(inp)
+    pins = [torch.from_numpy(np.ascontiguousarray(inp[p], dtype=np.float32)).pin_memory() for p in cg.param_ids]
+    outs = [[torch.empty(g.at(o).shape).pin_memory() for o in g.outputs] for _ in range(2)]
+    st = torch.cuda.Stream()
+    for i in range(4):
+        cg.run_host_async([t.data_ptr() for t in pins], [t.data_ptr() for t in outs[i % 2]], st.cuda_stream)
+    st.synchronize()
+    assert all(np.array_equal(t.numpy(), want[o]) for ob in outs for o, t in zip(g.outputs, ob)), name
+    cg.close()
+    print(name, "pipelined host runs ok", flush=True)
+g, rep, _ = H.load_bundle(os.path.join(T.PLANS, "C5L.small.json"))
+full = H.run_compiled(rep, g, T.gen_inputs(g, 42, -1.0, 1.0), ctx=ctx, values="all")
+print("C5L value map", len(full), "keys ok", flush=True)
