@@ -590,3 +590,35 @@ def test_host_runs_pipelined(ctx, name):
                 assert np.array_equal(t.numpy(), w[o]), o
     finally:
         cg.close()
+
+
+@pytest.mark.parametrize("kw", [{}, {"row_pipeline": 1}, {"row_pipeline": 3}, {"row_pipeline": 4}, {"row_pipeline": 5}])
+def test_long_row_softmax_special_rows(ctx, kw):
+    """The long-row templates' online softmax pass (max and rescaled fp64 sum in
+    one pass, pairs combined across warps / cluster CTAs) against the
+    reference's two-pass fp32 semantics, row by row: finite, some -inf, all
+    -inf (NaN: exp(-inf - -inf)), one +inf (NaN: exp(inf - inf)), NaN first
+    (the max's NaN-first rule), NaN inside, -inf first, large values.  The
+    two-pass forms (row_pipeline 4 / 5) on the same rows."""
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", "softmax_r8_c131072.json"))
+    x = T.gen_inputs(g, 23, -1.0, 1.0)
+    (pid,) = [i.id for i in g.parameters()]
+    a = x[pid].reshape(8, -1)
+    C = a.shape[1]
+    a[1, 5::997] = -np.inf
+    a[2, :] = -np.inf
+    a[3, C // 3] = np.inf
+    a[4, 0] = np.nan
+    a[5, C // 2 + 7] = np.nan
+    a[6, 0] = -np.inf
+    a[7, :] = a[7, :] * 20 + 80
+    prog = rep.kernels[0].program
+    (y,) = H.run_program(prog, g, x, ctx=ctx, **kw)
+    ref32 = T.interpret(g, x, 0)[prog.roots[0]].reshape(8, -1)
+    ref64 = T.interpret(g, x, 1)[prog.roots[0]].reshape(8, -1)
+    y = y.reshape(8, -1)
+    assert np.array_equal(np.isnan(y), np.isnan(ref32))
+    assert np.isnan(y[2]).all() and np.isnan(y[3]).all() and np.isnan(y[4]).all() and np.isnan(y[5]).all()
+    for r in (0, 1, 6, 7):
+        assert T.values_close(y[r], ref32[r]) or T.values_close(y[r], ref64[r]), r
+        assert (y[r][np.isneginf(a[r])] == 0).all()
