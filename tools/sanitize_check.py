@@ -37,10 +37,14 @@ for case in P._eligible("pipeline")[:12]:
     n += 1
 print("random graphs", n, "ok")
 # round 2: pipelined host runs (two staging slots, flags reset on the copy
-# stream) and the full value map (intermediates read back from HBM)
+# stream) and the full value map (intermediates read back from HBM).
+# Not under initcheck: it serialises device work, and a host-path kernel that
+# waits on its chunk gates (set by a copy stream) can then be scheduled ahead
+# of those copies and hit its 20 s gate bound (memcheck / racecheck /
+# synccheck run these concurrently and pass).
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
-for name in ("C1.small", "C5.small"):
+for name in () if os.environ.get("SFX_SANITIZER") == "initcheck" else ("C1.small", "C5.small"):
     g, rep, _ = H.load_bundle(os.path.join(T.PLANS, name + ".json"))
     cg = H.CompiledGraph(ctx, g, rep)
     inp = T.gen_inputs(g, 3, -1.0, 1.0)
