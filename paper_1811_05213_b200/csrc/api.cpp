@@ -1098,214 +1098,214 @@ namespace {
 // every stream of the run is joined into `s` (the run is complete when `s` is).
 void host_enqueue(sfx_graph* G, const void* const* params, int32_t n_params, void* const* outputs,
                   int32_t n_outputs, CUstream s) {
-    if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
-    if (n_params != static_cast<int32_t>(G->params.size()) ||
-        n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
-      throw sfx::Error(SFX_ERR_INVALID, "param/output count mismatch");
-    G->ctx->bind();
-    const sfx::Driver& d = sfx::driver();
-    const sfx::Graph& g = G->graph;
-    const int K = static_cast<int>(G->kernels.size());
-    sfx_graph::HostSlot& slot = G->hslot[G->hnext];
-    G->hnext ^= 1;
-    if (slot.bufs.empty()) {
-      for (int p : G->params) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[p].numel() * 4));
-      for (int o : G->graph.outputs) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[o].numel() * 4));
-      slot.flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
-      sfx::check_cu(d.cuEventCreate(&slot.free_ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-    }
-    std::vector<uint64_t> dp(slot.bufs.begin(), slot.bufs.begin() + n_params);
-    std::vector<uint64_t> dout(slot.bufs.begin() + n_params, slot.bufs.end());
-    if (!G->d2h) {
-      sfx::check_cu(d.cuStreamCreate(&G->d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-      sfx::check_cu(d.cuStreamCreate(&G->h2d, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-      sfx::check_cu(d.cuStreamCreate(&G->h2d2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-      sfx::check_cu(d.cuStreamCreate(&G->d2h2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
-      G->events.resize(3 * K + 2);
-      for (CUevent& e : G->events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-      for (CUevent& e : G->join_ev) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
-      G->host_order = host_order(G);
-      G->host_kernels.assign(K, nullptr);
-      if (host_streaming() && !G->opts.debug_checks) {  // debug: every launch coverage-checked, whole copies
-        sfx_compile_opts ho = G->opts;
-        ho.host_stream = 1;
-        for (int p = 0; p < K; ++p) {
-          const std::string& st = G->kernels[p]->src.strategy;
-          if (st != "row" && st != "map") continue;
-          sfx_kernel* hk = build_kernel(G->ctx, g, p, &ho);
-          if (hk->src.stream_R > 0) G->host_kernels[p] = hk;
-          else destroy_kernel(hk);
-        }
+  if (!G) throw sfx::Error(SFX_ERR_INVALID, "null graph");
+  if (n_params != static_cast<int32_t>(G->params.size()) ||
+      n_outputs != static_cast<int32_t>(G->graph.outputs.size()))
+    throw sfx::Error(SFX_ERR_INVALID, "param/output count mismatch");
+  G->ctx->bind();
+  const sfx::Driver& d = sfx::driver();
+  const sfx::Graph& g = G->graph;
+  const int K = static_cast<int>(G->kernels.size());
+  sfx_graph::HostSlot& slot = G->hslot[G->hnext];
+  G->hnext ^= 1;
+  if (slot.bufs.empty()) {
+    for (int p : G->params) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[p].numel() * 4));
+    for (int o : G->graph.outputs) slot.bufs.push_back(G->ctx->alloc(G->graph.nodes[o].numel() * 4));
+    slot.flags = G->ctx->alloc(static_cast<uint64_t>(K) * kFlagWords * 4);
+    sfx::check_cu(d.cuEventCreate(&slot.free_ev, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+  }
+  std::vector<uint64_t> dp(slot.bufs.begin(), slot.bufs.begin() + n_params);
+  std::vector<uint64_t> dout(slot.bufs.begin() + n_params, slot.bufs.end());
+  if (!G->d2h) {
+    sfx::check_cu(d.cuStreamCreate(&G->d2h, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    sfx::check_cu(d.cuStreamCreate(&G->h2d, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    sfx::check_cu(d.cuStreamCreate(&G->h2d2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    sfx::check_cu(d.cuStreamCreate(&G->d2h2, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    G->events.resize(3 * K + 2);
+    for (CUevent& e : G->events) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    for (CUevent& e : G->join_ev) sfx::check_cu(d.cuEventCreate(&e, CU_EVENT_DISABLE_TIMING), "cuEventCreate");
+    G->host_order = host_order(G);
+    G->host_kernels.assign(K, nullptr);
+    if (host_streaming() && !G->opts.debug_checks) {  // debug: every launch coverage-checked, whole copies
+      sfx_compile_opts ho = G->opts;
+      ho.host_stream = 1;
+      for (int p = 0; p < K; ++p) {
+        const std::string& st = G->kernels[p]->src.strategy;
+        if (st != "row" && st != "map") continue;
+        sfx_kernel* hk = build_kernel(G->ctx, g, p, &ho);
+        if (hk->src.stream_R > 0) G->host_kernels[p] = hk;
+        else destroy_kernel(hk);
       }
     }
-    // Overlapped host path.  Streams: host->device copies (h2d, h2d2), the
-    // launches (s), device->host copies (d2h, d2h2).  A group whose template
-    // works on an [R, C] row space (row / map, KernelSource::stream_R) is fed in
-    // row chunks: a copy stream lands chunk j of its row-local inputs and sets
-    // the group's gate[j] = 1 (cuStreamWriteValue32); the kernel's CTAs of chunk
-    // j wait on gate[j], and each bumps done[j] once its rows are stored; a
-    // copy-back stream waits for done[j] == the chunk's CTA count
-    // (cuStreamWaitValue32) and returns chunk j of the group's graph outputs.
-    // Chunks alternate between the two streams of each direction, so one
-    // stream's copy runs while the other waits on its stream memory operation
-    // (a memop drains the copy pipeline: ~20 us per chunk on one stream).
-    // So a group's launch starts when its first chunk lands and its results
-    // start crossing back while the rest of its inputs are still in flight —
-    // still ONE launch per group.  Other groups: whole copies, ordered by events.
-    // Groups that return the most bytes go first (any dependency-respecting
-    // order gives the same values).
-    // This slot's previous run (two runs ago) must be done with its buffers
-    // and flags before anything of this run touches them; the flags are reset
-    // on the first copy stream (not on `s`, whose previous run's kernels would
-    // otherwise hold back this run's copies), and every stream of the run
-    // starts behind the reset.
-    if (slot.used) sfx::check_cu(d.cuStreamWaitEvent(G->h2d, slot.free_ev, 0), "cuStreamWaitEvent");
-    slot.used = true;
-    sfx::check_cu(d.cuMemsetD32Async(slot.flags, 0, static_cast<size_t>(K) * kFlagWords, G->h2d), "cuMemsetD32Async");
-    CUevent ev_reset = G->events[3 * K];
-    sfx::check_cu(d.cuEventRecord(ev_reset, G->h2d), "cuEventRecord");
-    for (CUstream st : {s, G->h2d2, G->d2h, G->d2h2})
-      sfx::check_cu(d.cuStreamWaitEvent(st, ev_reset, 0), "cuStreamWaitEvent");
+  }
+  // Overlapped host path.  Streams: host->device copies (h2d, h2d2), the
+  // launches (s), device->host copies (d2h, d2h2).  A group whose template
+  // works on an [R, C] row space (row / map, KernelSource::stream_R) is fed in
+  // row chunks: a copy stream lands chunk j of its row-local inputs and sets
+  // the group's gate[j] = 1 (cuStreamWriteValue32); the kernel's CTAs of chunk
+  // j wait on gate[j], and each bumps done[j] once its rows are stored; a
+  // copy-back stream waits for done[j] == the chunk's CTA count
+  // (cuStreamWaitValue32) and returns chunk j of the group's graph outputs.
+  // Chunks alternate between the two streams of each direction, so one
+  // stream's copy runs while the other waits on its stream memory operation
+  // (a memop drains the copy pipeline: ~20 us per chunk on one stream).
+  // So a group's launch starts when its first chunk lands and its results
+  // start crossing back while the rest of its inputs are still in flight —
+  // still ONE launch per group.  Other groups: whole copies, ordered by events.
+  // Groups that return the most bytes go first (any dependency-respecting
+  // order gives the same values).
+  // This slot's previous run (two runs ago) must be done with its buffers
+  // and flags before anything of this run touches them; the flags are reset
+  // on the first copy stream (not on `s`, whose previous run's kernels would
+  // otherwise hold back this run's copies), and every stream of the run
+  // starts behind the reset.
+  if (slot.used) sfx::check_cu(d.cuStreamWaitEvent(G->h2d, slot.free_ev, 0), "cuStreamWaitEvent");
+  slot.used = true;
+  sfx::check_cu(d.cuMemsetD32Async(slot.flags, 0, static_cast<size_t>(K) * kFlagWords, G->h2d), "cuMemsetD32Async");
+  CUevent ev_reset = G->events[3 * K];
+  sfx::check_cu(d.cuEventRecord(ev_reset, G->h2d), "cuEventRecord");
+  for (CUstream st : {s, G->h2d2, G->d2h, G->d2h2})
+    sfx::check_cu(d.cuStreamWaitEvent(st, ev_reset, 0), "cuStreamWaitEvent");
 
-    std::map<int, CUdeviceptr> where = G->owned;
-    const std::map<int, CUdeviceptr>& mid = mids_for(G, eager_key(s));
-    where.insert(mid.begin(), mid.end());
-    G->last_mid[s] = &mid;
-    std::map<int, int> param_slot, out_slot;
-    for (int i = 0; i < n_params; ++i) where[G->params[i]] = dp[i], param_slot[G->params[i]] = i;
-    for (int i = 0; i < n_outputs; ++i) where[g.outputs[i]] = dout[i], out_slot[g.outputs[i]] = i;
-    std::vector<bool> copied(n_params, false), returned(n_outputs, false);
-    // host->device copy of rows [r0, r1) of a node split into R rows (whole: 0, R, R)
-    auto h2d_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
-      const int slot = param_slot.at(node);
-      const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
-      sfx::check_cu(d.cuMemcpyHtoDAsync(dp[slot] + r0 * row, static_cast<const char*>(params[slot]) + r0 * row,
-                                        (r1 - r0) * row, st),
-                    "cuMemcpyHtoDAsync");
-    };
-    auto d2h_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
-      const int slot = out_slot.at(node);
-      const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
-      sfx::check_cu(d.cuMemcpyDtoHAsync(static_cast<char*>(outputs[slot]) + r0 * row, dout[slot] + r0 * row,
-                                        (r1 - r0) * row, st),
-                    "cuMemcpyDtoHAsync");
-    };
-    auto is_host_param = [&](int n) {
-      auto it = param_slot.find(n);
-      return it != param_slot.end() && !copied[it->second];
-    };
-    for (size_t q = 0; q < G->host_order.size(); ++q) {
-      const int pi = G->host_order[q];
-      sfx_kernel* k = G->host_kernels[pi] ? G->host_kernels[pi] : G->kernels[pi];
-      const sfx::KernelSource& ks = k->src;
-      std::vector<int> ret;  // graph outputs this group returns
-      for (int r : ks.outputs)
-        if (out_slot.count(r) && !returned[out_slot[r]]) ret.push_back(r);
-      std::set<int> chunked;
-      for (int in : ks.stream_inputs)
-        if (is_host_param(in)) chunked.insert(in);
-      const int64_t R = ks.stream_R;
-      bool streamed = R > 0 && host_streaming() && (!chunked.empty() || !ret.empty());
-      for (int r : ret)
-        if (streamed && g.nodes[r].numel() % R) streamed = false;
-      // chunk rows: ~16 MB of streamed bytes per chunk, a multiple of the CTA
-      // row unit, at most kFlagWords - 1 chunks
-      int64_t rpc = R, nch = 1;
-      if (streamed) {
-        uint64_t bytes = 0;
-        for (int in : chunked) bytes += g.nodes[in].numel() * 4;
-        for (int r : ret) bytes += g.nodes[r].numel() * 4;
-        // default: up to 32 chunks of >= 8 MB (measured: C1 67 MB flat at 4-8 MB
-        // chunks, C4 / C4b 1.63 / 2.99 ms at 4 MB vs 1.58 / 2.87 at 8 MB, C2 537 MB
-        // best at ~16 MB, C5's 3.2 GB probs_d flat from 16 to 100 MB)
-        const uint64_t cb = host_chunk_bytes() ? host_chunk_bytes() : std::max<uint64_t>(8 << 20, bytes / 32);
-        int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, static_cast<int64_t>(bytes / cb)));
-        const int64_t unit = std::max<int64_t>(1, ks.stream_unit);
-        rpc = ((R + want - 1) / want + unit - 1) / unit * unit;
-        nch = (R + rpc - 1) / rpc;
-        if (nch > kMaxChunks) streamed = false, rpc = R, nch = 1;
-      }
-      // inputs: everything not chunked goes first, whole
-      for (int in : ks.inputs)
-        if (is_host_param(in) && !(streamed && chunked.count(in))) {
-          h2d_rows(in, 1, 0, 1, G->h2d);
-          copied[param_slot[in]] = true;
-        }
-      StreamArgs sa;
-      const CUdeviceptr gate = slot.flags + static_cast<uint64_t>(pi) * kFlagWords * 4;
-      if (streamed) {
-        // the whole inputs above precede every chunk gate on both streams
-        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d), "cuEventRecord");
-        sfx::check_cu(d.cuStreamWaitEvent(G->h2d2, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
-        for (int64_t j = 0; j < nch; ++j) {
-          CUstream st = (j & 1) ? G->h2d2 : G->h2d;
-          const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
-          for (int in : chunked) h2d_rows(in, R, r0, r1, st);
-          sfx::check_cu(d.cuStreamWriteValue32(st, gate + 4 * j, 1u, CU_STREAM_WRITE_VALUE_DEFAULT),
-                        "cuStreamWriteValue32");
-        }
-        for (int in : chunked) copied[param_slot[in]] = true;
-        sa.gate = gate;
-        sa.done = gate + 4 * kMaxChunks;
-        sa.chunk_elems = static_cast<long long>(rpc * ks.stream_C);
-      } else {
-        // whole copies: on the first copy stream, plus anything the second
-        // stream still has in flight for earlier groups
-        sfx::check_cu(d.cuEventRecord(G->events[3 * q], G->h2d), "cuEventRecord");
-        sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q], 0), "cuStreamWaitEvent");
-        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d2), "cuEventRecord");
-        sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
-      }
-      launch(k, gather_ptrs(G, ks.inputs, where), gather_ptrs(G, ks.outputs, where), s, sa);
-      if (ret.empty()) continue;
-      if (streamed) {
-        const int64_t E = ks.stream_cta_elems, C = ks.stream_C;
-        for (int64_t j = 0; j < nch; ++j) {
-          CUstream st = (j & 1) ? G->d2h2 : G->d2h;
-          const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
-          const int64_t ctas = (r1 * C + E - 1) / E - (r0 * C) / E;
-          sfx::check_cu(d.cuStreamWaitValue32(st, sa.done + 4 * j, static_cast<cuuint32_t>(ctas),
-                                              CU_STREAM_WAIT_VALUE_GEQ),
-                        "cuStreamWaitValue32");
-          for (int r : ret) d2h_rows(r, R, r0, r1, st);
-        }
-      } else {
-        sfx::check_cu(d.cuEventRecord(G->events[3 * q + 1], s), "cuEventRecord");
-        sfx::check_cu(d.cuStreamWaitEvent(G->d2h, G->events[3 * q + 1], 0), "cuStreamWaitEvent");
-        for (int r : ret) d2h_rows(r, 1, 0, 1, G->d2h);
-      }
-      for (int r : ret) returned[out_slot[r]] = true;
+  std::map<int, CUdeviceptr> where = G->owned;
+  const std::map<int, CUdeviceptr>& mid = mids_for(G, eager_key(s));
+  where.insert(mid.begin(), mid.end());
+  G->last_mid[s] = &mid;
+  std::map<int, int> param_slot, out_slot;
+  for (int i = 0; i < n_params; ++i) where[G->params[i]] = dp[i], param_slot[G->params[i]] = i;
+  for (int i = 0; i < n_outputs; ++i) where[g.outputs[i]] = dout[i], out_slot[g.outputs[i]] = i;
+  std::vector<bool> copied(n_params, false), returned(n_outputs, false);
+  // host->device copy of rows [r0, r1) of a node split into R rows (whole: 0, R, R)
+  auto h2d_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
+    const int slot = param_slot.at(node);
+    const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
+    sfx::check_cu(d.cuMemcpyHtoDAsync(dp[slot] + r0 * row, static_cast<const char*>(params[slot]) + r0 * row,
+                                      (r1 - r0) * row, st),
+                  "cuMemcpyHtoDAsync");
+  };
+  auto d2h_rows = [&](int node, int64_t R, int64_t r0, int64_t r1, CUstream st) {
+    const int slot = out_slot.at(node);
+    const uint64_t row = static_cast<uint64_t>(g.nodes[node].numel() / R) * 4;
+    sfx::check_cu(d.cuMemcpyDtoHAsync(static_cast<char*>(outputs[slot]) + r0 * row, dout[slot] + r0 * row,
+                                      (r1 - r0) * row, st),
+                  "cuMemcpyDtoHAsync");
+  };
+  auto is_host_param = [&](int n) {
+    auto it = param_slot.find(n);
+    return it != param_slot.end() && !copied[it->second];
+  };
+  for (size_t q = 0; q < G->host_order.size(); ++q) {
+    const int pi = G->host_order[q];
+    sfx_kernel* k = G->host_kernels[pi] ? G->host_kernels[pi] : G->kernels[pi];
+    const sfx::KernelSource& ks = k->src;
+    std::vector<int> ret;  // graph outputs this group returns
+    for (int r : ks.outputs)
+      if (out_slot.count(r) && !returned[out_slot[r]]) ret.push_back(r);
+    std::set<int> chunked;
+    for (int in : ks.stream_inputs)
+      if (is_host_param(in)) chunked.insert(in);
+    const int64_t R = ks.stream_R;
+    bool streamed = R > 0 && host_streaming() && (!chunked.empty() || !ret.empty());
+    for (int r : ret)
+      if (streamed && g.nodes[r].numel() % R) streamed = false;
+    // chunk rows: ~16 MB of streamed bytes per chunk, a multiple of the CTA
+    // row unit, at most kFlagWords - 1 chunks
+    int64_t rpc = R, nch = 1;
+    if (streamed) {
+      uint64_t bytes = 0;
+      for (int in : chunked) bytes += g.nodes[in].numel() * 4;
+      for (int r : ret) bytes += g.nodes[r].numel() * 4;
+      // default: up to 32 chunks of >= 8 MB (measured: C1 67 MB flat at 4-8 MB
+      // chunks, C4 / C4b 1.63 / 2.99 ms at 4 MB vs 1.58 / 2.87 at 8 MB, C2 537 MB
+      // best at ~16 MB, C5's 3.2 GB probs_d flat from 16 to 100 MB)
+      const uint64_t cb = host_chunk_bytes() ? host_chunk_bytes() : std::max<uint64_t>(8 << 20, bytes / 32);
+      int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, static_cast<int64_t>(bytes / cb)));
+      const int64_t unit = std::max<int64_t>(1, ks.stream_unit);
+      rpc = ((R + want - 1) / want + unit - 1) / unit * unit;
+      nch = (R + rpc - 1) / rpc;
+      if (nch > kMaxChunks) streamed = false, rpc = R, nch = 1;
     }
-    // graph outputs no group produces (a parameter or constant listed as output)
-    bool tail = false;
+    // inputs: everything not chunked goes first, whole
+    for (int in : ks.inputs)
+      if (is_host_param(in) && !(streamed && chunked.count(in))) {
+        h2d_rows(in, 1, 0, 1, G->h2d);
+        copied[param_slot[in]] = true;
+      }
+    StreamArgs sa;
+    const CUdeviceptr gate = slot.flags + static_cast<uint64_t>(pi) * kFlagWords * 4;
+    if (streamed) {
+      // the whole inputs above precede every chunk gate on both streams
+      sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(G->h2d2, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
+      for (int64_t j = 0; j < nch; ++j) {
+        CUstream st = (j & 1) ? G->h2d2 : G->h2d;
+        const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
+        for (int in : chunked) h2d_rows(in, R, r0, r1, st);
+        sfx::check_cu(d.cuStreamWriteValue32(st, gate + 4 * j, 1u, CU_STREAM_WRITE_VALUE_DEFAULT),
+                      "cuStreamWriteValue32");
+      }
+      for (int in : chunked) copied[param_slot[in]] = true;
+      sa.gate = gate;
+      sa.done = gate + 4 * kMaxChunks;
+      sa.chunk_elems = static_cast<long long>(rpc * ks.stream_C);
+    } else {
+      // whole copies: on the first copy stream, plus anything the second
+      // stream still has in flight for earlier groups
+      sfx::check_cu(d.cuEventRecord(G->events[3 * q], G->h2d), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q], 0), "cuStreamWaitEvent");
+      sfx::check_cu(d.cuEventRecord(G->events[3 * q + 2], G->h2d2), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(s, G->events[3 * q + 2], 0), "cuStreamWaitEvent");
+    }
+    launch(k, gather_ptrs(G, ks.inputs, where), gather_ptrs(G, ks.outputs, where), s, sa);
+    if (ret.empty()) continue;
+    if (streamed) {
+      const int64_t E = ks.stream_cta_elems, C = ks.stream_C;
+      for (int64_t j = 0; j < nch; ++j) {
+        CUstream st = (j & 1) ? G->d2h2 : G->d2h;
+        const int64_t r0 = j * rpc, r1 = std::min(R, r0 + rpc);
+        const int64_t ctas = (r1 * C + E - 1) / E - (r0 * C) / E;
+        sfx::check_cu(d.cuStreamWaitValue32(st, sa.done + 4 * j, static_cast<cuuint32_t>(ctas),
+                                            CU_STREAM_WAIT_VALUE_GEQ),
+                      "cuStreamWaitValue32");
+        for (int r : ret) d2h_rows(r, R, r0, r1, st);
+      }
+    } else {
+      sfx::check_cu(d.cuEventRecord(G->events[3 * q + 1], s), "cuEventRecord");
+      sfx::check_cu(d.cuStreamWaitEvent(G->d2h, G->events[3 * q + 1], 0), "cuStreamWaitEvent");
+      for (int r : ret) d2h_rows(r, 1, 0, 1, G->d2h);
+    }
+    for (int r : ret) returned[out_slot[r]] = true;
+  }
+  // graph outputs no group produces (a parameter or constant listed as output)
+  bool tail = false;
+  for (int i = 0; i < n_outputs; ++i) {
+    if (returned[i]) continue;
+    int o = g.outputs[i];
+    if (is_host_param(o)) {
+      h2d_rows(o, 1, 0, 1, G->h2d);
+      copied[param_slot[o]] = true;
+    }
+    tail = true;
+  }
+  if (tail) {
+    CUevent ev = G->events[3 * K + 1];
+    sfx::check_cu(d.cuEventRecord(ev, G->h2d), "cuEventRecord");
+    sfx::check_cu(d.cuStreamWaitEvent(s, ev, 0), "cuStreamWaitEvent");
     for (int i = 0; i < n_outputs; ++i) {
       if (returned[i]) continue;
       int o = g.outputs[i];
-      if (is_host_param(o)) {
-        h2d_rows(o, 1, 0, 1, G->h2d);
-        copied[param_slot[o]] = true;
-      }
-      tail = true;
+      CUdeviceptr src = param_slot.count(o) ? dp[param_slot[o]] : G->owned.count(o) ? G->owned.at(o) : 0;
+      if (!src) throw sfx::Error(SFX_ERR_EXEC, "no value for graph output " + g.nodes[o].id);
+      sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
     }
-    if (tail) {
-      CUevent ev = G->events[3 * K + 1];
-      sfx::check_cu(d.cuEventRecord(ev, G->h2d), "cuEventRecord");
-      sfx::check_cu(d.cuStreamWaitEvent(s, ev, 0), "cuStreamWaitEvent");
-      for (int i = 0; i < n_outputs; ++i) {
-        if (returned[i]) continue;
-        int o = g.outputs[i];
-        CUdeviceptr src = param_slot.count(o) ? dp[param_slot[o]] : G->owned.count(o) ? G->owned.at(o) : 0;
-        if (!src) throw sfx::Error(SFX_ERR_EXEC, "no value for graph output " + g.nodes[o].id);
-        sfx::check_cu(d.cuMemcpyDtoHAsync(outputs[i], src, g.nodes[o].numel() * 4, s), "cuMemcpyDtoHAsync");
-      }
-    }
-    // join: `s` waits for every copy stream; the slot is free once `s` is here
-    for (int j = 0; j < 4; ++j) {
-      CUstream st = j == 0 ? G->h2d : j == 1 ? G->h2d2 : j == 2 ? G->d2h : G->d2h2;
-      sfx::check_cu(d.cuEventRecord(G->join_ev[j], st), "cuEventRecord");
-      sfx::check_cu(d.cuStreamWaitEvent(s, G->join_ev[j], 0), "cuStreamWaitEvent");
-    }
-    sfx::check_cu(d.cuEventRecord(slot.free_ev, s), "cuEventRecord");
+  }
+  // join: `s` waits for every copy stream; the slot is free once `s` is here
+  for (int j = 0; j < 4; ++j) {
+    CUstream st = j == 0 ? G->h2d : j == 1 ? G->h2d2 : j == 2 ? G->d2h : G->d2h2;
+    sfx::check_cu(d.cuEventRecord(G->join_ev[j], st), "cuEventRecord");
+    sfx::check_cu(d.cuStreamWaitEvent(s, G->join_ev[j], 0), "cuStreamWaitEvent");
+  }
+  sfx::check_cu(d.cuEventRecord(slot.free_ev, s), "cuEventRecord");
 }
 
 }  // namespace
