@@ -124,10 +124,10 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
 // inputs (mostly from L2).  f32 sums accumulate in fp64 per thread.
 // Softmax's two row levels — m = max_j x_j (level 1), s = sum_j exp(x_j - m)
 // (level 2) — recognised in a long-row group: *r1 = the max, *r2 = the sum.
-// The long-row templates then fold both in ONE pass over the row (online
-// softmax: a running max and a rescaled fp64 sum per thread, pairs combined
-// across warps / CTAs), one pass and one cross-CTA combine fewer; the sum
-// differs from the two-pass fp32 fold by rounding only (fp64 accumulation,
+// The cluster template then combines both across its CTAs at once: each
+// thread's (max, fp64 sum of exp(x - its max)) pair, rescaled when pairs meet
+// (online softmax), one block + cluster combine fewer per row; the sum differs
+// from the two-pass fp32 fold by rounding only (fp64 accumulation,
 // exp(x - m_partial) * exp(m_partial - M) instead of exp(x - M)).
 bool online_softmax(const Ctx& c, const RowPlan& rp, int* r1, int* r2) {
   const Graph& g = c.g;
@@ -167,8 +167,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   std::set<int> loc = row_local_inputs(c, rp);
   std::vector<int> staged(loc.begin(), loc.end());
   int CS = 1;
-  // row_pipeline=1 / 5: plain multi-pass (A/B), 5 and 4 without the online softmax pass
-  if (V == 4 && !staged.empty() && o.row_pipeline != 1 && o.row_pipeline != 5) {
+  if (V == 4 && !staged.empty() && o.row_pipeline != 1) {  // row_pipeline=1: plain multi-pass (A/B)
     const int64_t bytes = C * 4 * static_cast<int64_t>(staged.size());
     // (pipe_stages doubles as the largest cluster size to consider: 16 is the
     // non-portable maximum)
@@ -321,23 +320,31 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.indent--;
     body.line("}");
   };
-  // online softmax (row_pipeline=4 / 5 keep the two-pass form: A/B knob)
+  // softmax's two levels in one cross-CTA combine (cluster variant only: the
+  // plain multi-pass variant re-reads the row from L2 / HBM per pass, and a
+  // per-element online fold measured slower than its two passes;
+  // row_pipeline=4 keeps the two-level form: A/B knob)
   int osm_max = -1, osm_sum = -1;
-  const bool osm = o.row_pipeline != 4 && o.row_pipeline != 5 && online_softmax(c, rp, &osm_max, &osm_sum);
+  const bool osm = CS > 1 && o.row_pipeline != 4 && online_softmax(c, rp, &osm_max, &osm_sum);
   if (osm) {
     const std::string m = em.fresh("om"), sv = em.fresh("os");
     body.line("float " + m + " = sfx_bits_f(0xff800000);");
     body.line("double " + sv + " = 0.0;");
     const Node& rn = c.g.nodes[osm_max];
     const Node& in = c.g.nodes[rn.operands[0]];
-    row_loop([&](const std::string& cb) {
-      for (int lane = 0; lane < V; ++lane) {
-        em.lane = lane;
-        Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
-        std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, col));
-        body.line("sfx_osm_add(" + m + ", " + sv + ", " + v + ");");
-      }
-    });
+    // two passes over this CTA's slice in shared memory, no barrier between
+    for (int pass = 0; pass < 2; ++pass)
+      row_loop([&](const std::string& cb) {
+        for (int lane = 0; lane < V; ++lane) {
+          em.lane = lane;
+          Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
+          std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, col));
+          if (pass == 0)
+            body.line(m + " = fmaxf(" + m + ", " + v + ");");
+          else
+            body.line(sv + " += sfx_osm_term(" + v + ", " + m + ");");
+        }
+      });
     for (int k = 16; k >= 1; k /= 2)
       body.line("sfx_osm_combine(" + m + ", " + sv + ", __shfl_xor_sync(0xffffffffu, " + m + ", " + std::to_string(k) +
                 "), __shfl_xor_sync(0xffffffffu, " + sv + ", " + std::to_string(k) + "));");
@@ -535,9 +542,9 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
               std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "");
   else
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
-              " threads per row, multi-pass (" + std::to_string(rp.max_level - (osm ? 1 : 0) + (full_roots.empty() ? 0 : 1)) +
+              " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
               " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
-  if (osm) ks.note += " online softmax (max + rescaled sum in one pass)";
+  if (osm) ks.note += " softmax max + sum in one cluster combine";
   return ks;
 }
 

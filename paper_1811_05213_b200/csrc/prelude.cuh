@@ -75,17 +75,13 @@ __device__ __forceinline__ float sfx_fold_pmin(float a, float b) { return fminf(
 __device__ __forceinline__ int sfx_fold_pmax(int a, int b) { return a < b ? b : a; }
 __device__ __forceinline__ int sfx_fold_pmin(int a, int b) { return b < a ? b : a; }
 __device__ __forceinline__ float sfx_fold_first(float first, float acc) { return (first != first) ? first : acc; }
-// Online softmax statistics (long-row templates): a running (max m, sum s of
-// exp(x - m)) pair per thread, rescaled when the max moves; s in fp64.  The
-// special values follow the two-pass reference: -inf elements add exp(-inf - M)
-// = 0, NaN / +inf elements make the sum NaN (exp(NaN - M), exp(inf - inf)).
-__device__ __forceinline__ void sfx_osm_add(float& m, double& s, float x) {
-  if (x > m) {
-    s = s * (double)expf(__fsub_rn(m, x)) + (double)expf(__fsub_rn(x, x));
-    m = x;
-  } else if (x != __int_as_float(0xff800000)) {
-    s += (double)expf(__fsub_rn(x, m));
-  }
+// Softmax statistics of a long row in one cross-CTA combine (cluster
+// template): each thread folds its elements' max m, then s = sum exp(x - m) in
+// fp64 (-inf elements add 0, as exp(-inf - M) does for the row max M; NaN and
+// +inf elements make s NaN, as exp(NaN - M) / exp(inf - inf) do), and the
+// (m, s) pairs are combined with rescaling.
+__device__ __forceinline__ double sfx_osm_term(float x, float m) {
+  return x == __int_as_float(0xff800000) ? 0.0 : (double)expf(__fsub_rn(x, m));
 }
 __device__ __forceinline__ void sfx_osm_combine(float& m, double& s, float m2, double s2) {
   const float M = fmaxf(m, m2);
