@@ -122,42 +122,6 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
 // Plain variant (inputs too large for a cluster, odd widths): one CTA per row,
 // one pass over the row per level plus a final pass, re-reading the row's
 // inputs (mostly from L2).  f32 sums accumulate in fp64 per thread.
-// Softmax's two row levels — m = max_j x_j (level 1), s = sum_j exp(x_j - m)
-// (level 2) — recognised in a long-row group: *r1 = the max, *r2 = the sum.
-// The cluster template then combines both across its CTAs at once: each
-// thread's (max, fp64 sum of exp(x - its max)) pair, rescaled when pairs meet
-// (online softmax), one block + cluster combine fewer per row; the sum differs
-// from the two-pass fp32 fold by rounding only (fp64 accumulation,
-// exp(x - m_partial) * exp(m_partial - M) instead of exp(x - M)).
-bool online_softmax(const Ctx& c, const RowPlan& rp, int* r1, int* r2) {
-  const Graph& g = c.g;
-  if (rp.max_level != 2 || c.reduces.size() != 2) return false;
-  int a = -1, b = -1;
-  for (int r : c.reduces) (rp.level.at(r) == 1 ? a : b) = r;
-  if (a < 0 || b < 0) return false;
-  const Node& na = g.nodes[a];
-  const Node& nb = g.nodes[b];
-  if (na.reducer != SFX_REDUCE_MAX || nb.reducer != SFX_REDUCE_SUM || na.dtype != SFX_F32 ||
-      nb.dtype != SFX_F32 || degenerate_reduce(g, na) || degenerate_reduce(g, nb))
-    return false;
-  const int x = na.operands[0], e = nb.operands[0];
-  if (!c.p.is_member(e) || g.nodes[e].op != SFX_OP_ELEMENTWISE || g.nodes[e].kind != SFX_EW_EXP) return false;
-  const int d = g.nodes[e].operands[0];
-  if (!c.p.is_member(d) || g.nodes[d].op != SFX_OP_ELEMENTWISE || g.nodes[d].kind != SFX_EW_SUB ||
-      g.nodes[d].operands[0] != x)
-    return false;
-  const int bc = g.nodes[d].operands[1];
-  const Node& nbc = g.nodes[bc];
-  if (!c.p.is_member(bc) || nbc.op != SFX_OP_BROADCAST || nbc.operands[0] != a ||
-      nbc.numel() != g.nodes[x].numel() || g.nodes[x].numel() != rp.R * rp.C)
-    return false;
-  for (size_t j = 0; j < nbc.dim_map.size(); ++j)
-    if (nbc.dim_map[j] != static_cast<int64_t>(j)) return false;  // the row scalar along the row
-  *r1 = a;
-  *r2 = b;
-  return true;
-}
-
 KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
   KernelSource ks;
   ks.strategy = "row";
@@ -320,85 +284,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.indent--;
     body.line("}");
   };
-  // softmax's two levels in one cross-CTA combine (cluster variant only: the
-  // plain multi-pass variant re-reads the row from L2 / HBM per pass, and a
-  // per-element online fold measured slower than its two passes;
-  // row_pipeline=4 keeps the two-level form: A/B knob)
-  int osm_max = -1, osm_sum = -1;
-  const bool osm = CS > 1 && o.row_pipeline != 4 && online_softmax(c, rp, &osm_max, &osm_sum);
-  if (osm) {
-    const std::string m = em.fresh("om"), sv = em.fresh("os");
-    body.line("float " + m + " = sfx_bits_f(0xff800000);");
-    body.line("double " + sv + " = 0.0;");
-    const Node& rn = c.g.nodes[osm_max];
-    const Node& in = c.g.nodes[rn.operands[0]];
-    // two passes over this CTA's slice in shared memory, no barrier between
-    for (int pass = 0; pass < 2; ++pass)
-      row_loop([&](const std::string& cb) {
-        for (int lane = 0; lane < V; ++lane) {
-          em.lane = lane;
-          Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
-          std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, col));
-          if (pass == 0)
-            body.line(m + " = fmaxf(" + m + ", " + v + ");");
-          else
-            body.line(sv + " += sfx_osm_term(" + v + ", " + m + ");");
-        }
-      });
-    for (int k = 16; k >= 1; k /= 2)
-      body.line("sfx_osm_combine(" + m + ", " + sv + ", __shfl_xor_sync(0xffffffffu, " + m + ", " + std::to_string(k) +
-                "), __shfl_xor_sync(0xffffffffu, " + sv + ", " + std::to_string(k) + "));");
-    const std::string smm = em.fresh("osmm"), sms = em.fresh("osms");
-    body.line("__shared__ float " + smm + "[" + std::to_string(W) + "];");
-    body.line("__shared__ double " + sms + "[" + std::to_string(W) + "];");
-    body.line("if (lane == 0) { " + smm + "[warp] = " + m + "; " + sms + "[warp] = " + sv + "; }");
-    body.line("__syncthreads();");
-    body.line(m + " = " + smm + "[0];");
-    body.line(sv + " = " + sms + "[0];");
-    body.line("for (int w = 1; w < " + std::to_string(W) + "; ++w) sfx_osm_combine(" + m + ", " + sv + ", " + smm +
-              "[w], " + sms + "[w]);");
-    if (CS > 1) {
-      // cluster combine of the pairs, in rank order (double-buffered slots for
-      // the persistent variant, as below)
-      const std::string xm = em.fresh("xpm"), xs = em.fresh("xps"), rm = em.fresh("xrm"), rs = em.fresh("xrs");
-      const std::string ixm = persist ? xm + "[itr & 1]" : xm, ixs = persist ? xs + "[itr & 1]" : xs;
-      body.line("__shared__ float " + xm + (persist ? "[2]" : "") + ";");
-      body.line("__shared__ double " + xs + (persist ? "[2]" : "") + ";");
-      body.line("__shared__ float " + rm + ";");
-      body.line("__shared__ double " + rs + ";");
-      body.line("if (tid == 0) { " + ixm + " = " + m + "; " + ixs + " = " + sv + "; }");
-      body.line("sfx_cluster_sync();");
-      body.line("if (warp == 0) {");
-      body.line("  const float vm = lane < " + std::to_string(CS) + " ? sfx_dsmem_ld(&" + ixm + ", (unsigned)lane) : " +
-                ixm + ";");
-      body.line("  const double vs = lane < " + std::to_string(CS) + " ? sfx_dsmem_ld(&" + ixs + ", (unsigned)lane) : " +
-                ixs + ";");
-      body.line("  float am = __shfl_sync(0xffffffffu, vm, 0);");
-      body.line("  double as = __shfl_sync(0xffffffffu, vs, 0);");
-      body.line("  for (int r = 1; r < " + std::to_string(CS) +
-                "; ++r) sfx_osm_combine(am, as, __shfl_sync(0xffffffffu, vm, r), __shfl_sync(0xffffffffu, vs, r));");
-      body.line("  if (lane == 0) { " + rm + " = am; " + rs + " = as; }");
-      body.line("}");
-      body.line("__syncthreads();");
-      body.line(m + " = " + rm + ";");
-      body.line(sv + " = " + rs + ";");
-    }
-    // the max keeps the sequential fold's first-element rule; a row of -inf
-    // sums exp(-inf - -inf) = NaN in the reference
-    em.push();
-    em.staged.clear();
-    em.lane = 0;
-    std::string f0 = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, em.uni("0")));
-    const std::string fm = em.fresh("red"), fs = em.fresh("red");
-    body.line("const float " + fm + " = sfx_fold_first(" + f0 + ", " + m + ");");
-    em.staged = staged_map;
-    em.pop();
-    body.line("const float " + fs + " = " + m + " == sfx_bits_f(0xff800000) ? sfx_bits_f(0x7fc00000) : (float)" + sv +
-              ";");
-    reduced[osm_max] = fm;
-    reduced[osm_sum] = fs;
-  }
-  for (int lv = osm ? 3 : 1; lv <= rp.max_level; ++lv) {
+  for (int lv = 1; lv <= rp.max_level; ++lv) {
     std::vector<int> red;
     for (int r : c.reduces)
       if (rp.level.at(r) == lv) red.push_back(r);
@@ -544,7 +430,6 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
               " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
               " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
-  if (osm) ks.note += " softmax max + sum in one cluster combine";
   return ks;
 }
 

@@ -75,21 +75,6 @@ __device__ __forceinline__ float sfx_fold_pmin(float a, float b) { return fminf(
 __device__ __forceinline__ int sfx_fold_pmax(int a, int b) { return a < b ? b : a; }
 __device__ __forceinline__ int sfx_fold_pmin(int a, int b) { return b < a ? b : a; }
 __device__ __forceinline__ float sfx_fold_first(float first, float acc) { return (first != first) ? first : acc; }
-// Softmax statistics of a long row in one cross-CTA combine (cluster
-// template): each thread folds its elements' max m, then s = sum exp(x - m) in
-// fp64 (-inf elements add 0, as exp(-inf - M) does for the row max M; NaN and
-// +inf elements make s NaN, as exp(NaN - M) / exp(inf - inf) do), and the
-// (m, s) pairs are combined with rescaling.
-__device__ __forceinline__ double sfx_osm_term(float x, float m) {
-  return x == __int_as_float(0xff800000) ? 0.0 : (double)expf(__fsub_rn(x, m));
-}
-__device__ __forceinline__ void sfx_osm_combine(float& m, double& s, float m2, double s2) {
-  const float M = fmaxf(m, m2);
-  const double a = s == 0.0 ? 0.0 : s * (double)expf(__fsub_rn(m, M));
-  const double b = s2 == 0.0 ? 0.0 : s2 * (double)expf(__fsub_rn(m2, M));
-  m = M;
-  s = a + b;
-}
 __device__ __forceinline__ int sfx_fold_first(int first, int acc) { return acc; }
 
 // ---- memory ----

@@ -592,15 +592,13 @@ def test_host_runs_pipelined(ctx, name):
         cg.close()
 
 
-@pytest.mark.parametrize("kw", [{}, {"row_pipeline": 1}, {"row_pipeline": 3}, {"row_pipeline": 4}])
+@pytest.mark.parametrize("kw", [{}, {"row_pipeline": 1}, {"row_pipeline": 3}])
 def test_long_row_softmax_special_rows(ctx, kw):
-    """The cluster template's softmax statistics in one cross-CTA combine
-    (per-thread max and fp64 sum of exp, pairs rescaled when combined across
-    warps / cluster CTAs) against the reference's two-pass fp32 semantics, row
-    by row: finite, some -inf, all -inf (NaN: exp(-inf - -inf)), one +inf
-    (NaN: exp(inf - inf)), NaN first (the max's NaN-first rule), NaN inside,
-    -inf first, large values.  The two-level forms (plain multi-pass, the
-    persistent clusters, row_pipeline=4) on the same rows."""
+    """Softmax over long rows (the cluster template, the plain multi-pass
+    variant, persistent clusters) against the reference's two-pass fp32
+    semantics, row by row: finite, some -inf, all -inf (NaN: exp(-inf - -inf)),
+    one +inf (NaN: exp(inf - inf)), NaN first (the max's NaN-first rule), NaN
+    inside, -inf first, large values."""
     g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", "softmax_r8_c131072.json"))
     x = T.gen_inputs(g, 23, -1.0, 1.0)
     (pid,) = [i.id for i in g.parameters()]
