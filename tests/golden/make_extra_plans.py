@@ -63,7 +63,7 @@ EXTRA = {
     "softmax_r24_c4096": configs.c2_softmax(B=2, H=3, S=4, L=4096),
     # rows beyond the register-resident template: one CTA per row, multi-pass
     "softmax_r4_c131072": configs.c2_softmax(B=1, H=1, S=4, L=131072),
-    "softmax_r8_c131072": configs.c2_softmax(B=1, H=1, S=8, L=131072),  # online softmax special rows
+    "softmax_r8_c131072": configs.c2_softmax(B=1, H=1, S=8, L=131072),  # special-value long softmax rows
     "softmax_r2_c262144": configs.c2_softmax(B=1, H=1, S=2, L=262144),  # 16-CTA (non-portable) cluster
     "ln_r6_c98304": configs.c1_layernorm(R=6, C=98304),
     "ln_r5_c70001": configs.c1_layernorm(R=5, C=70001),
