@@ -287,6 +287,19 @@ std::string Emitter::seq_fold(int reducer, int dtype, const std::string& acc, co
   }
 }
 
+// A group member whose value depends on a (non-degenerate) reduction of the group.
+bool Emitter::reduce_dependent(int node) {
+  auto it = reduce_dep_.find(node);
+  if (it != reduce_dep_.end()) return it->second;
+  bool r = false;
+  if (p.is_member(node)) {
+    const Node& n = g.nodes[node];
+    r = n.op == SFX_OP_REDUCE;
+    for (int op : n.operands) r = r || reduce_dependent(op);
+  }
+  return reduce_dep_[node] = r;
+}
+
 std::string Emitter::ew_expr(const Node& n, const std::vector<std::string>& a) {
   switch (n.kind) {
     case SFX_EW_ADD: return "sfx_add(" + a[0] + ", " + a[1] + ")";
@@ -421,6 +434,17 @@ std::string Emitter::value(int node, const std::vector<Ix>& comps) {
       std::vector<std::string> a;
       for (int op : n.operands) a.push_back(value(op, comps));
       result = fresh("v");
+      if (rcp_reduced_divisors && n.kind == SFX_EW_DIVIDE && n.dtype == SFX_F32 && reduce_dependent(n.operands[1])) {
+        const std::string key = "rcp:" + a[1];
+        std::string r = find(key);
+        if (r.empty()) {
+          r = fresh("rcp");
+          code->line("const float " + r + " = sfx_rcp(" + a[1] + ");");
+          bind(key, r);
+        }
+        code->line(std::string("const ") + T + " " + result + " = sfx_div_rc(" + a[0] + ", " + a[1] + ", " + r + ");");
+        break;
+      }
       code->line(std::string("const ") + T + " " + result + " = " + ew_expr(n, a) + ";");
       break;
     }

@@ -78,6 +78,11 @@ class Emitter {
   // Strategy hook for member nodes: return a variable name to use instead of
   // evaluating the member's op, or "" to evaluate it inline.
   std::function<std::string(int node, const std::vector<Ix>& comps)> resolve;
+  // Divisions by a reduction-dependent value (softmax's e / sum) through the
+  // divisor's IEEE reciprocal (<= 1 ulp from the quotient; such outputs carry
+  // the reduction-order tolerance anyway).  Off in the literal tier, which
+  // keeps the reference's arithmetic.
+  bool rcp_reduced_divisors = false;
 
   std::string value(int node, const std::vector<Ix>& comps);
 
@@ -113,6 +118,8 @@ class Emitter {
   std::string load(int node, const std::vector<Ix>& comps);
   std::string reduce_loop(int node, const std::vector<Ix>& comps);
   std::string dot_loop(int node, const std::vector<Ix>& comps);
+  bool reduce_dependent(int node);
+  std::map<int, bool> reduce_dep_;
   std::vector<std::map<std::string, std::string>> scopes_;
   int next_ = 0;
 };

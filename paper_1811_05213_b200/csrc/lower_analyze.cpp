@@ -1,6 +1,8 @@
 // Group context, kernel scaffolding and the template analyses (GroupAnalyzer).
 #include "lower_impl.hpp"
 
+#include <cstdlib>
+
 namespace sfx {
 namespace lw {
 
@@ -55,6 +57,11 @@ Ctx make_ctx(const Graph& g, const Program& p) {
   c.wide = big >= (int64_t{1} << 30) || p.blocks >= (int64_t{1} << 30);
   c.name = sanitize(g.nodes[p.fusion_root >= 0 ? p.fusion_root : p.roots[0]].id);
   return c;
+}
+
+bool rcp_divisors() {
+  const char* e = std::getenv("SFX_EXACT_DIV");
+  return !(e && e[0] == '1');
 }
 
 // ---- kernel scaffolding ---------------------------------------------------

@@ -68,6 +68,7 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   const int NR = static_cast<int>(c.reduces.size());
 
   Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
   std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
   Code body;
   em.code = &body;
@@ -430,6 +431,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
   const int NR = static_cast<int>(c.reduces.size());
   Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
   std::string sig = signature(c, em, ks.entry, B, ctas_per_sm);
   Code body;
   em.code = &body;

@@ -38,6 +38,9 @@ struct Ctx {
 int64_t prod(const std::vector<int64_t>& d, size_t b, size_t e);
 std::string sanitize(const std::string& s);
 bool degenerate_reduce(const Graph& g, const Node& n);
+// Templates divide by reduction results through a reciprocal (Emitter::
+// rcp_reduced_divisors); SFX_EXACT_DIV=1 keeps the IEEE division (A/B).
+bool rcp_divisors();
 Ctx make_ctx(const Graph& g, const Program& p);
 
 // ---- kernel scaffolding (lower_analyze.cpp) ----

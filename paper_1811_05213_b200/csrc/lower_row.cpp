@@ -64,6 +64,7 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
     ks.stream_inputs.assign(loc.begin(), loc.end());
   }
   Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
   // (pipe_ctas_per_sm doubles as a __launch_bounds__ residency target here)
   std::string sig = signature(c, em, ks.entry, threads, o.pipe_ctas_per_sm, stream);
   Code body;
@@ -158,6 +159,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   // vectors per thread per loop iteration (independent loads in flight)
   const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 4;
   Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
   std::string sig = signature(c, em, ks.entry, B);
   if (CS > 1) {
     const std::string gv = "__global__ void ";
@@ -647,6 +649,7 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
   const int64_t grid = std::min<int64_t>((R + WARPS - 1) / WARPS, int64_t{kNumSMs} * ctas_per_sm);
 
   Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
   std::string sig = signature(c, em, ks.entry, WARPS * 32);
   Code body;
   em.code = &body;

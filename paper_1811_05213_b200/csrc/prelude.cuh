@@ -32,6 +32,13 @@ __device__ __forceinline__ float sfx_scale_2f(float a, float hi, float lo) {
 __device__ __forceinline__ float sfx_exp(float a) { return expf(a); }
 __device__ __forceinline__ float sfx_log(float a) { return logf(a); }
 __device__ __forceinline__ float sfx_div(float a, float b) { return __fdiv_rn(a, b); }
+// a / b for a divisor computed from a reduction (row / column constant): one
+// IEEE reciprocal per divisor value, then a multiply (<= 1 ulp from a / b);
+// zero, infinite, NaN or subnormal-range divisors take the IEEE division.
+__device__ __forceinline__ float sfx_rcp(float b) { return __frcp_rn(b); }
+__device__ __forceinline__ float sfx_div_rc(float a, float b, float r) {
+  return (fabsf(b) > 0x1p-126f && fabsf(b) < 0x1p126f) ? __fmul_rn(a, r) : __fdiv_rn(a, b);
+}
 __device__ __forceinline__ float sfx_pow(float a, float b) { return powf(a, b); }
 __device__ __forceinline__ float sfx_tanh(float a) { return tanhf(a); }
 __device__ __forceinline__ float sfx_sqrt(float a) { return __fsqrt_rn(a); }
