@@ -168,7 +168,7 @@ typedef struct sfx_compile_opts {
   int32_t rows_per_cta;  /* 0 = auto (row template) */
   int32_t threads_per_row; /* 0 = auto (row template) */
   int32_t items_per_thread; /* 0 = auto (map template: 128-bit vectors per thread) */
-  int32_t row_pipeline;     /* row template: 0 = auto, 1 = register-resident rows, 2 = TMA-staged pipeline where applicable */
+  int32_t row_pipeline;     /* row template: 0 = auto, 1 = register-resident rows, 2 = TMA-staged pipeline, 4 = resident rows (all of a CTA's rows staged at entry) where applicable */
   int32_t pipe_warps;       /* TMA row pipeline: warps per CTA (0 = auto) */
   int32_t pipe_stages;      /* TMA row pipeline: row buffers per warp (0 = auto) */
   int32_t pipe_ctas_per_sm; /* TMA row pipeline: persistent CTAs per SM (0 = auto) */

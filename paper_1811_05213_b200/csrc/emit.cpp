@@ -201,6 +201,38 @@ Ix Emitter::linearize(const std::vector<Ix>& comps, const std::vector<int64_t>& 
   return x;
 }
 
+// A value held in shared memory for the current row (an input staged by TMA,
+// or a member cached by an earlier pass over the row): `sp` points at the
+// row's slice, `rb` is the linear index of its first element.
+std::string Emitter::staged_load(int node, const std::vector<Ix>& comps) {
+  const Node& n = g.nodes[node];
+  Ix L = linearize(comps, n.dims);
+  const auto& st = staged.at(node);
+  const std::string& sp = st.first;
+  const std::string& rb = st.second;
+  if (L.kind == IX_PLUS && V == 4) {
+    std::string key = "sld4:" + sp + ":" + L.base;
+    std::string q = find(key);
+    if (q.empty()) {
+      q = fresh("q");
+      code->line("const sfx_f4 " + q + " = sfx_lds4(" + sp + " + (" + L.base + " - " + rb + "));");
+      bind(key, q);
+      ++loads_vec;
+    }
+    static const char* xyzw[] = {".x", ".y", ".z", ".w"};
+    return q + xyzw[lane];
+  }
+  std::string key = "sld:" + sp + ":" + L.e;
+  std::string v = find(key);
+  if (v.empty()) {
+    v = fresh("v");
+    code->line("const float " + v + " = " + sp + "[" + L.e + " - " + rb + "];");
+    bind(key, v);
+    ++loads_scalar;
+  }
+  return v;
+}
+
 std::string Emitter::load(int node, const std::vector<Ix>& comps) {
   const Node& n = g.nodes[node];
   auto pit = input_ptr.find(node);
@@ -227,33 +259,8 @@ std::string Emitter::load(int node, const std::vector<Ix>& comps) {
     }
     return v;
   }
+  if (staged.count(node)) return staged_load(node, comps);  // row staged in shared memory by TMA
   Ix L = linearize(comps, n.dims);
-  auto st = staged.find(node);
-  if (st != staged.end()) {  // row staged in shared memory by the TMA pipeline
-    const std::string& sp = st->second.first;
-    const std::string& rb = st->second.second;
-    if (L.kind == IX_PLUS && V == 4) {
-      std::string key = "sld4:" + sp + ":" + L.base;
-      std::string q = find(key);
-      if (q.empty()) {
-        q = fresh("q");
-        code->line("const sfx_f4 " + q + " = sfx_lds4(" + sp + " + (" + L.base + " - " + rb + "));");
-        bind(key, q);
-        ++loads_vec;
-      }
-      static const char* xyzw[] = {".x", ".y", ".z", ".w"};
-      return q + xyzw[lane];
-    }
-    std::string key = "sld:" + sp + ":" + L.e;
-    std::string v = find(key);
-    if (v.empty()) {
-      v = fresh("v");
-      code->line("const float " + v + " = " + sp + "[" + L.e + " - " + rb + "];");
-      bind(key, v);
-      ++loads_scalar;
-    }
-    return v;
-  }
   if (L.kind == IX_PLUS && V == 4) {
     std::string key = "ld4:" + ptr + ":" + L.base;
     std::string q = find(key);
@@ -416,6 +423,11 @@ std::string Emitter::value(int node, const std::vector<Ix>& comps) {
   if (!hit.empty()) return hit;
 
   std::string result;
+  if (p.is_member(node) && staged.count(node)) {  // cached in shared memory by an earlier pass
+    result = staged_load(node, comps);
+    bind(key, result);
+    return result;
+  }
   if (!p.is_member(node)) {
     result = load(node, comps);
     bind(key, result);

@@ -116,6 +116,7 @@ class Emitter {
 
  private:
   std::string load(int node, const std::vector<Ix>& comps);
+  std::string staged_load(int node, const std::vector<Ix>& comps);
   std::string reduce_loop(int node, const std::vector<Ix>& comps);
   std::string dot_loop(int node, const std::vector<Ix>& comps);
   bool reduce_dependent(int node);

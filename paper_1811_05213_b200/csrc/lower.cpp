@@ -310,11 +310,17 @@ KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o
       bool pipe_ok = !staged.empty() && rp.C % 128 == 0 && rp.C / 32 <= 64 &&
                      4 * 2 * rp.C * 4 * static_cast<int64_t>(staged.size()) <= 200 * 1024 &&
                      o.threads_per_row == 0 && o.rows_per_cta == 0;
+      // resident rows: every row of a CTA's range staged at once, one CTA per SM
+      const int64_t res_rows = (rp.R + kNumSMs - 1) / kNumSMs;
+      bool res_ok = !staged.empty() && rp.C % 128 == 0 && rp.C / 32 <= 64 && o.threads_per_row == 0 &&
+                    o.rows_per_cta == 0 && res_rows * (rp.C * 4 * static_cast<int64_t>(staged.size()) + 8) <= 227 * 1024;
       const int Vr = rp.C % 4 == 0 ? 4 : 1;
       if (rp.C / row_tpr(rp.C, Vr) > 64)
         ks = lower_row_mp(c, rp, o);  // longer than 1024 threads x 64 elements
       else if (pipe_ok && o.row_pipeline == 2)
         ks = lower_row_pipe(c, rp, staged, o);
+      else if (res_ok && o.row_pipeline == 4)
+        ks = lower_row_res(c, rp, staged, o);
       else
         ks = lower_row(c, rp, o);
       break;

@@ -103,6 +103,8 @@ KernelSource lower_map_tiled_v4(const Ctx& c, const TilePlan& tp, const sfx_comp
 int row_tpr(int64_t C, int V, int streams = 1);
 KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o);
 KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o);
+KernelSource lower_row_res(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs,
+                           const sfx_compile_opts& o);
 KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs,
                             const sfx_compile_opts& o);
 void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH);

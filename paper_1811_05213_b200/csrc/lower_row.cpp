@@ -107,6 +107,98 @@ KernelSource lower_row(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& 
   return ks;
 }
 
+// Members cached in shared memory between the passes of the cluster variant.
+// The final pass (roots) recomputes every inline member it needs from the
+// staged slices; a member that the LAST reduction pass already computes (it
+// lies under that pass's reduction operands) and whose expression holds an
+// expensive op (exp, log, div, pow, tanh, sqrt, rsqrt: ir.cpp's set, the
+// reference's `ir.cpp:32-45`) is instead written over a staged input's slice
+// in that pass, when the final pass no longer reads that input, and loaded
+// back in the final pass (softmax: e = exp(x - max) replaces x, so y = e / sum
+// costs one shared-memory load instead of a second exp).  The values are the
+// same bits either way.  Only for groups whose [R, C] values are all read at
+// the thread's own element (elementwise and reshape-like edges): every thread
+// then overwrites only slice elements it alone reads.  Returns member ->
+// staged input whose slice it takes.
+std::map<int, int> plan_row_cache(const Ctx& c, const RowPlan& rp, const std::vector<int>& staged) {
+  const Graph& g = c.g;
+  const int64_t RC = rp.R * rp.C;
+  std::map<int, int> none;
+  if (rp.max_level < 1 || staged.empty()) return none;
+  bool ok = true;
+  std::set<int> seen;
+  std::function<void(int)> check = [&](int n) {
+    if (!c.p.is_member(n) || !seen.insert(n).second) return;
+    const Node& m = g.nodes[n];
+    if (m.numel() == RC) {
+      switch (m.op) {
+        case SFX_OP_ELEMENTWISE: case SFX_OP_RESHAPE: case SFX_OP_BITCAST: case SFX_OP_BROADCAST:
+          break;
+        case SFX_OP_TRANSPOSE:
+          if (!transpose_is_reshape(m)) ok = false;
+          break;
+        case SFX_OP_REDUCE:
+          if (!degenerate_reduce(g, m)) ok = false;
+          break;
+        default:
+          ok = false;
+      }
+    }
+    for (int o : m.operands) check(o);
+  };
+  for (int r : c.p.roots) check(r);
+  if (!ok) return none;
+  // [R, C] members the last reduction pass computes
+  std::set<int> avail;
+  std::function<void(int)> under = [&](int n) {
+    if (!c.p.is_member(n) || avail.count(n)) return;
+    const Node& m = g.nodes[n];
+    if (m.op == SFX_OP_REDUCE && !degenerate_reduce(g, m)) return;
+    if (m.numel() == RC) avail.insert(n);
+    for (int o : m.operands) under(o);
+  };
+  for (int r : c.reduces)
+    if (rp.level.at(r) == rp.max_level) under(g.nodes[r].operands[0]);
+  std::map<int, bool> exp_memo;
+  std::function<bool(int)> costly = [&](int n) -> bool {
+    if (!c.p.is_member(n)) return false;
+    auto f = exp_memo.find(n);
+    if (f != exp_memo.end()) return f->second;
+    const Node& m = g.nodes[n];
+    bool r = false;
+    if (!(m.op == SFX_OP_REDUCE && !degenerate_reduce(g, m))) {
+      r = m.op == SFX_OP_ELEMENTWISE && m.kind >= SFX_EW_EXP;
+      for (int o : m.operands) r = r || costly(o);
+    }
+    return exp_memo[n] = r;
+  };
+  // the final pass's cut: cached members and the staged inputs still read
+  std::set<int> cuts, needs, walked;
+  std::function<void(int)> walk = [&](int n) {
+    if (!walked.insert(n).second) return;
+    if (!c.p.is_member(n)) {
+      if (std::find(staged.begin(), staged.end(), n) != staged.end()) needs.insert(n);
+      return;
+    }
+    const Node& m = g.nodes[n];
+    if (m.op == SFX_OP_REDUCE && !degenerate_reduce(g, m)) return;
+    if (avail.count(n) && m.dtype == SFX_F32 && costly(n)) {
+      cuts.insert(n);
+      return;
+    }
+    for (int o : m.operands) walk(o);
+  };
+  for (int r : c.p.roots) walk(r);
+  std::vector<int> freed;
+  for (int s : staged)
+    if (!needs.count(s)) freed.push_back(s);
+  if (cuts.empty() || cuts.size() > freed.size()) return none;
+  std::map<int, int> out;
+  size_t k = 0;
+  for (int m : cuts) out[m] = freed[k++];
+  return out;
+}
+
 // Rows too long to hold in registers (more than 1024 threads x 64 elements,
 // e.g. softmax / LayerNorm over 128K columns).
 //
@@ -243,6 +335,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     }
     em.staged = staged_map;
   }
+  // (row_pipeline=5: recompute instead of caching, A/B)
+  const std::map<int, int> cache = CS > 1 && o.row_pipeline != 5 ? plan_row_cache(c, rp, staged) : std::map<int, int>{};
   std::map<int, std::string> reduced;
   em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
     if (c.g.nodes[node].op != SFX_OP_REDUCE || degenerate_reduce(c.g, c.g.nodes[node])) return "";
@@ -310,6 +404,27 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
           body.line(acc[k] + " = " + fold_of(rn) + "(" + acc[k] + ", " + v + ");");
         }
       }
+      if (lv != rp.max_level) return;
+      // cached members overwrite their slice element after its last read
+      for (const auto& [m, x] : cache) {
+        const Node& mn = c.g.nodes[m];
+        const auto& slot = staged_map.at(x);
+        std::vector<std::string> vals(V);
+        Ix L0;
+        for (int lane = 0; lane < V; ++lane) {
+          em.lane = lane;
+          Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
+          std::vector<Ix> comps = rowcol_comps(em, mn.dims, R, C, rowix, col);
+          vals[lane] = em.value(m, comps);
+          if (lane == 0) L0 = em.linearize(comps, mn.dims);
+          if (V == 1 || L0.kind != IX_PLUS)
+            body.line("((float*)" + slot.first + ")[" + em.linearize(comps, mn.dims).e + " - " + slot.second +
+                      "] = " + vals[lane] + ";");
+        }
+        if (V == 4 && L0.kind == IX_PLUS)
+          body.line("sfx_sts4((float*)" + slot.first + " + (" + L0.base + " - " + slot.second + "), " + vals[0] +
+                    ", " + vals[1] + ", " + vals[2] + ", " + vals[3] + ");");
+      }
     });
     for (size_t k = 0; k < red.size(); ++k) {
       const Node& rn = c.g.nodes[red[k]];
@@ -374,6 +489,13 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   }
   std::vector<int> full_roots, row_roots;
   for (int r : c.p.roots) (c.g.nodes[r].numel() == R * C ? full_roots : row_roots).push_back(r);
+  if (!cache.empty()) {  // the final pass reads the cached members, not the inputs they replaced
+    em.staged = staged_map;
+    for (const auto& [m, x] : cache) {
+      em.staged[m] = staged_map.at(x);
+      em.staged.erase(x);
+    }
+  }
   if (!full_roots.empty())
     row_loop([&](const std::string& cb) {
       std::vector<std::vector<std::string>> vals(full_roots.size(), std::vector<std::string>(V));
@@ -426,7 +548,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   if (CS > 1)
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " cluster of " + std::to_string(CS) +
               " CTAs x " + std::to_string(B) + " threads per row, " + std::to_string(staged.size()) +
-              " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), DSMEM combine, levels=" +
+              " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), DSMEM combine, " +
+              (cache.empty() ? std::string() : std::to_string(cache.size()) + " member(s) cached over input slices, ") + "levels=" +
               std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "");
   else
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
@@ -717,6 +840,90 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
   ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " TMA-staged inputs=" +
             std::to_string(staged.size()) + " stages=" + std::to_string(NBUF) + " persistent grid=" +
             std::to_string(grid) + " levels=" + std::to_string(rp.max_level);
+  return ks;
+}
+
+// Resident rows (row_pipeline=4): for groups whose row-local inputs fit the
+// shared memory of the whole GPU (148 x ~220 KB), one CTA per SM owns a
+// contiguous, balanced range of rows (R/148 rounded either way) and its warps
+// have the TMA engine copy EVERY one of those rows into shared memory at entry
+// (one cp.async.bulk + mbarrier per row): the whole tensor is in flight at
+// once, so the launch never runs a second wave or a partial last wave, and
+// each warp starts a row as soon as that row has landed.  Rows are then
+// processed like the register template (one warp per row, values from
+// shared memory), roots stored straight from registers.
+KernelSource lower_row_res(const Ctx& c, const RowPlan& rp, const std::set<int>& staged_inputs,
+                           const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "row";
+  ks.entry = "sfx_rowr_" + c.name;
+  fill_common(c, ks);
+  const int64_t R = rp.R, C = rp.C;
+  const int V = 4, TPR = 32;
+  const int64_t NCH = C / (TPR * V);
+  std::vector<int> staged(staged_inputs.begin(), staged_inputs.end());
+  const int64_t row_bytes = C * 4;
+  const int64_t stage_bytes = row_bytes * static_cast<int64_t>(staged.size());
+  const int64_t G = std::min<int64_t>(R, kNumSMs);
+  const int64_t RPB = (R + G - 1) / G;  // most rows one CTA owns
+  const int64_t data_bytes = RPB * stage_bytes;
+  const int smem = static_cast<int>(data_bytes + RPB * 8);
+  if (smem > 227 * 1024) throw Error(SFX_ERR_UNSUPPORTED, "resident rows exceed the shared memory of one CTA per SM");
+  const int WARPS = static_cast<int>(std::min<int64_t>(RPB, o.pipe_warps > 0 ? std::min(o.pipe_warps, 32) : 32));
+
+  Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
+  std::string sig = signature(c, em, ks.entry, WARPS * 32);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
+  body.line("const int lr = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const sfx_u32 gmask = 0xffffffffu;");
+  body.line("const int gleader = 0;");
+  body.line("unsigned long long* bars = (unsigned long long*)(sfx_smem + " + fmt_i(data_bytes) + ");");
+  // balanced contiguous ranges: CTA b owns rows [b*R/G, (b+1)*R/G)
+  body.line("const " + it + " lo = (" + it + ")(((long long)blockIdx.x * " + fmt_i(R) + ") / " + fmt_i(G) + ");");
+  body.line("const int nrows = (int)((((long long)blockIdx.x + 1) * " + fmt_i(R) + ") / " + fmt_i(G) + " - lo);");
+  // every warp arms and issues its own rows (only that warp waits on them)
+  body.line("if (lr == 0) {");
+  body.line("  for (int j = warp; j < nrows; j += " + std::to_string(WARPS) + ") sfx_mbar_init(bars + j, 1);");
+  body.line("  sfx_fence_mbar_init();");
+  body.line("  for (int j = warp; j < nrows; j += " + std::to_string(WARPS) + ") {");
+  body.line("    sfx_mbar_expect_tx(bars + j, " + fmt_i(stage_bytes) + "u);");
+  for (size_t k = 0; k < staged.size(); ++k)
+    body.line("    sfx_bulk_g2s(sfx_smem + (" + it + ")j * " + fmt_i(stage_bytes) + " + " +
+              fmt_i(static_cast<int64_t>(k) * row_bytes) + ", " + em.input_ptr.at(staged[k]) + " + (lo + j) * " +
+              fmt_i(C) + ", " + fmt_i(row_bytes) + "u, bars + j);");
+  body.line("  }");
+  body.line("}");
+  body.line("__syncwarp();");
+  body.line("for (int j = warp; j < nrows; j += " + std::to_string(WARPS) + ") {");
+  body.indent++;
+  body.line("const " + it + " row = lo + j;");
+  body.line("sfx_mbar_wait(bars + j, 0u);");
+  em.push();
+  std::string rbase = em.ivar(Emitter::imul("row", C));
+  for (size_t k = 0; k < staged.size(); ++k) {
+    std::string p = em.fresh("st");
+    body.line("const float* " + p + " = (const float*)(sfx_smem + (" + it + ")j * " + fmt_i(stage_bytes) + " + " +
+              fmt_i(static_cast<int64_t>(k) * row_bytes) + ");");
+    em.staged[staged[k]] = {p, rbase};
+  }
+  emit_row_body(c, rp, em, body, TPR, V, NCH);
+  em.pop();
+  em.staged.clear();
+  body.indent--;
+  body.line("}");
+  ks.code = assemble(sig, body);
+  ks.block = WARPS * 32;
+  ks.grid_x = G;
+  ks.smem = smem;
+  ks.vector_width = V;
+  ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " resident rows: " + std::to_string(G) +
+            " CTAs x " + std::to_string(WARPS) + " warps, <= " + std::to_string(RPB) +
+            " rows per CTA copied into shared memory at entry (TMA), inputs=" + std::to_string(staged.size()) +
+            " levels=" + std::to_string(rp.max_level);
   return ks;
 }
 

@@ -102,6 +102,9 @@ __device__ __forceinline__ sfx_i4 sfx_ld4s(const int* p) {
   return v;
 }
 __device__ __forceinline__ sfx_f4 sfx_lds4(const float* p) { return *reinterpret_cast<const sfx_f4*>(p); }
+__device__ __forceinline__ void sfx_sts4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<sfx_f4*>(p) = sfx_f4{a, b, c, d};
+}
 
 // ---- cross-rank flags in peer memory (column combine over NVLink) ----
 __device__ __forceinline__ void sfx_st_release_sys(unsigned* p, unsigned v) {

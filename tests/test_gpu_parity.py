@@ -592,10 +592,11 @@ def test_host_runs_pipelined(ctx, name):
         cg.close()
 
 
-@pytest.mark.parametrize("kw", [{}, {"row_pipeline": 1}, {"row_pipeline": 3}])
+@pytest.mark.parametrize("kw", [{}, {"row_pipeline": 1}, {"row_pipeline": 3}, {"row_pipeline": 5}])
 def test_long_row_softmax_special_rows(ctx, kw):
-    """Softmax over long rows (the cluster template, the plain multi-pass
-    variant, persistent clusters) against the reference's two-pass fp32
+    """Softmax over long rows (the cluster template caching exp(x - max) in
+    shared memory, the plain multi-pass variant, persistent clusters, the
+    cluster template recomputing exp) against the reference's two-pass fp32
     semantics, row by row: finite, some -inf, all -inf (NaN: exp(-inf - -inf)),
     one +inf (NaN: exp(inf - inf)), NaN first (the max's NaN-first rule), NaN
     inside, -inf first, large values."""

@@ -47,6 +47,21 @@ def test_cluster_kernel_uses_tma_and_dsmem():
     assert "CGAERRBAR" in sass, "cluster barrier missing"
 
 
+def test_cluster_rows_cache_expensive_members():
+    """Long-row softmax: e = exp(x - max) is written over x's shared-memory
+    slice in the sum pass and read back by the final pass (one exp per
+    element, not two); LayerNorm's x - mean is cheap and stays recomputed;
+    row_pipeline=5 turns the cache off."""
+    src, _, note = _note(os.path.join(EXTRA, "softmax_r4_c131072.json"))
+    assert "1 member(s) cached" in note and "sfx_sts4((float*)" in src
+    # the prelude definition + the sum pass only: 4 unrolled vectors + the remainder, 4 lanes each
+    assert src.count("sfx_exp(") == 1 + (4 + 1) * 4
+    src, _, note = _note(os.path.join(EXTRA, "softmax_r4_c131072.json"), row_pipeline=5)
+    assert "cached" not in note and "sfx_sts4((float*)" not in src
+    src, _, note = _note(os.path.join(EXTRA, "ln_r6_c98304.json"))
+    assert "cached" not in note and "sfx_sts4((float*)" not in src
+
+
 def test_colbc_is_cooperative_with_grid_barriers():
     src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
     assert "sfx_grid_barrier(ws, 4u)" in src and "sfx_grid_exit(ws)" in src
