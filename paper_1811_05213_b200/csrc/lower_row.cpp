@@ -278,6 +278,33 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
                 fmt_i(static_cast<int64_t>(k) * slice_bytes) + ", " + em.input_ptr.at(staged[k]) + " + (" + r +
                 ") * " + fmt_i(C) + " + (" + it + ")q * " + fmt_i(SL) + ", " + fmt_i(slice_bytes) + "u, " + bar + ");");
   };
+  // Cluster combine protocol (default): every CTA pushes its partial of each
+  // reduction into slot [rank] of every peer's slot array with st.async, which
+  // completes the peer's per-level mbarrier, and folds its own slots in rank
+  // order once its mbarrier completes — one relaxed cluster barrier at entry
+  // (all mbarriers initialised before any push) instead of a release/acquire
+  // cluster barrier per level plus one at exit (each a GPU-scope MEMBAR that
+  // also waits for the CTA's outstanding stores, and an L1 invalidation).
+  // Persistent clusters double-buffer slots and mbarriers by row parity (a
+  // peer is at most one row ahead at any level).  SFX_CLUSTER_BARRIER_COMBINE=1:
+  // the barrier protocol (A/B).
+  const char* cbenv = std::getenv("SFX_CLUSTER_BARRIER_COMBINE");
+  const bool push = CS > 1 && !(cbenv && cbenv[0] == '1');
+  const int NPAR = persist ? 2 : 1;
+  std::vector<int64_t> level_bytes(rp.max_level + 1, 0);
+  for (int r : c.reduces) {
+    const Node& rn = c.g.nodes[r];
+    level_bytes[rp.level.at(r)] += CS * ((rn.reducer == SFX_REDUCE_SUM && rn.dtype == SFX_F32) ? 8 : 4);
+  }
+  auto arm_levels = [&](const std::string& ind) {
+    body.line(ind + "for (int b = 0; b < " + std::to_string(rp.max_level * NPAR) + "; ++b) sfx_mbar_init(cbar + b, 1);");
+    body.line(ind + "sfx_fence_mbar_init();");
+    for (int lv = 1; lv <= rp.max_level; ++lv)
+      for (int pp = 0; pp < NPAR; ++pp)
+        body.line(ind + "sfx_mbar_expect_tx(cbar + " + std::to_string((lv - 1) * NPAR + pp) + ", " +
+                  fmt_i(level_bytes[lv]) + "u);");
+  };
+  if (push) body.line("__shared__ __align__(8) unsigned long long cbar[" + std::to_string(rp.max_level * NPAR) + "];");
   if (CS > 1 && persist) {
     body.line("const unsigned q = sfx_cluster_rank();");
     body.line("const " + it + " cid = (" + it + ")blockIdx.x / " + std::to_string(CS) + ";");
@@ -286,6 +313,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.line("if (tid == 0) {");
     body.line("  sfx_mbar_init(sbar, 1);");
     body.line("  sfx_mbar_init(sbar + 1, 1);");
+    if (push) arm_levels("  ");
     body.line("  sfx_fence_mbar_init();");
     body.line("  if (cid < " + fmt_i(R) + ") {");
     issue("0", "cid", "sbar");
@@ -295,6 +323,10 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.line("  }");
     body.line("}");
     body.line("__syncthreads();");
+    if (push) {
+      body.line("sfx_cluster_arrive_relaxed();");
+      body.line("sfx_cluster_wait();");
+    }
     body.line("for (int itr = 0;; ++itr) {");
     body.line("const " + it + " row = cid + (" + it + ")itr * " + fmt_i(NCL) + ";");
     body.line("if (row >= " + fmt_i(R) + ") break;");
@@ -309,6 +341,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.line("unsigned long long* sbar = (unsigned long long*)(sfx_smem + " + fmt_i(bar_off) + ");");
     body.line("if (tid == 0) {");
     body.line("  sfx_mbar_init(sbar, 1);");
+    if (push) arm_levels("  ");
     body.line("  sfx_fence_mbar_init();");
     body.line("  sfx_mbar_expect_tx(sbar, " + fmt_i(bar_off) + "u);");
     for (size_t k = 0; k < staged.size(); ++k)
@@ -317,7 +350,9 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
                 fmt_i(slice_bytes) + "u, sbar);");
     body.line("}");
     body.line("__syncthreads();");
+    if (push) body.line("sfx_cluster_arrive_relaxed();");
     body.line("sfx_mbar_wait(sbar, 0);");
+    if (push) body.line("sfx_cluster_wait();  // every peer's mbarriers are initialised before the first push");
     ks.smem = static_cast<int>(bar_off + 16);
   } else {
     body.line("const " + it + " row = (" + it + ")blockIdx.x;");
@@ -426,6 +461,8 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
                     ", " + vals[1] + ", " + vals[2] + ", " + vals[3] + ");");
       }
     });
+    std::vector<std::string> slots(red.size());
+    const std::string cb_lv = "cbar + " + std::to_string((lv - 1) * NPAR) + (persist ? " + (itr & 1)" : "");
     for (size_t k = 0; k < red.size(); ++k) {
       const Node& rn = c.g.nodes[red[k]];
       const std::string T = acc_type(rn);
@@ -439,7 +476,13 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
       body.line(acc[k] + " = " + sm + "[0];");
       body.line("for (int w = 1; w < " + std::to_string(W) + "; ++w) " + acc[k] + " = " + fold_of(rn) + "(" + acc[k] +
                 ", " + sm + "[w]);");
-      if (CS > 1) {
+      if (push) {
+        slots[k] = em.fresh("xs");
+        body.line("__shared__ " + T + " " + slots[k] + "[" + std::to_string(NPAR) + "][" + std::to_string(CS) + "];");
+        body.line("if (tid == 0)");
+        body.line("  for (unsigned r = 0; r < " + std::to_string(CS) + "u; ++r) sfx_dsmem_push(&" + slots[k] + "[" +
+                  (persist ? "itr & 1" : "0") + "][q], " + acc[k] + ", " + cb_lv + ", r);");
+      } else if (CS > 1) {
         // cluster combine: every CTA folds the CS partials in rank order.  One
         // warp reads them (lane r from rank r, one DSMEM load each) and lane 0
         // folds them in order; the CTA reads the result from local smem (all
@@ -466,6 +509,20 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
         body.line("}");
         body.line("__syncthreads();");
         body.line(acc[k] + " = " + xr + ";");
+      }
+    }
+    if (push) {
+      body.line("sfx_mbar_wait_bounded(" + cb_lv + ", " + (persist ? "(unsigned)((itr >> 1) & 1)" : "0u") + ");");
+      if (persist) body.line("if (tid == 0) sfx_mbar_expect_tx(" + cb_lv + ", " + fmt_i(level_bytes[lv]) + "u);  // rearm for row itr + 2");
+    }
+    for (size_t k = 0; k < red.size(); ++k) {
+      const Node& rn = c.g.nodes[red[k]];
+      const std::string T = acc_type(rn);
+      if (push) {
+        const std::string sl = slots[k] + "[" + (persist ? "itr & 1" : "0") + "]";
+        body.line(acc[k] + " = " + sl + "[0];");
+        body.line("for (int r = 1; r < " + std::to_string(CS) + "; ++r) " + acc[k] + " = " + fold_of(rn) + "(" + acc[k] +
+                  ", " + sl + "[r]);");
       }
       std::string fin = acc[k];
       if (T == "double") {
@@ -537,7 +594,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.line("}");
     body.line("}");  // row loop
   }
-  if (CS > 1) body.line("sfx_cluster_sync();  // no CTA leaves while a peer may still read its partials");
+  if (CS > 1 && !push) body.line("sfx_cluster_sync();  // no CTA leaves while a peer may still read its partials");
   ks.code = assemble(sig, body);
   ks.block = B;
   ks.grid_x = (persist ? NCL : R) * CS;
@@ -548,7 +605,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   if (CS > 1)
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " cluster of " + std::to_string(CS) +
               " CTAs x " + std::to_string(B) + " threads per row, " + std::to_string(staged.size()) +
-              " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), DSMEM combine, " +
+              " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), " + (push ? "DSMEM push combine, " : "DSMEM combine, ") +
               (cache.empty() ? std::string() : std::to_string(cache.size()) + " member(s) cached over input slices, ") + "levels=" +
               std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "");
   else

@@ -232,6 +232,33 @@ __device__ __forceinline__ int sfx_dsmem_ld(const int* p, unsigned rank) {
   return v;
 }
 
+// Cluster combine by push: st.async writes a partial into `rank`'s copy of `p`
+// and completes that CTA's mbarrier transaction for its bytes, so a CTA waits
+// on its own mbarrier for all of the cluster's partials — no cluster barrier
+// (whose release / acquire is a GPU-scope MEMBAR + L1 invalidation) per
+// reduction level.
+__device__ __forceinline__ void sfx_dsmem_push(float* p, float v, unsigned long long* bar, unsigned rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+               :: "r"(sfx_dsmem_addr(p, rank)), "r"(__float_as_uint(v)), "r"(sfx_dsmem_addr(bar, rank)) : "memory");
+}
+__device__ __forceinline__ void sfx_dsmem_push(double* p, double v, unsigned long long* bar, unsigned rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :: "r"(sfx_dsmem_addr(p, rank)), "l"((unsigned long long)__double_as_longlong(v)),
+                  "r"(sfx_dsmem_addr(bar, rank)) : "memory");
+}
+__device__ __forceinline__ void sfx_dsmem_push(int* p, int v, unsigned long long* bar, unsigned rank) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+               :: "r"(sfx_dsmem_addr(p, rank)), "r"(v), "r"(sfx_dsmem_addr(bar, rank)) : "memory");
+}
+// split cluster barrier: a relaxed arrive (no memory ordering; the mbarrier
+// inits are published by fence.mbarrier_init) and the matching wait
+__device__ __forceinline__ void sfx_cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void sfx_cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // mbarrier phase wait that traps after 10 s instead of hanging the GPU
 __device__ __forceinline__ void sfx_mbar_wait_bounded(unsigned long long* bar, unsigned parity) {
   const unsigned long long t0 = sfx_globaltimer();
