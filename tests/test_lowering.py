@@ -44,7 +44,9 @@ def test_cluster_kernel_uses_tma_and_dsmem():
     sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass, "cp.async.bulk (TMA bulk copy) missing"
     assert "SYNCS" in sass, "mbarrier wait missing"
-    assert "CGAERRBAR" in sass, "cluster barrier missing"
+    assert "UCGABAR_ARV" in sass and "UCGABAR_WAIT" in sass, "entry cluster barrier missing"
+    assert "STAS" in sass, "st.async push of the partials into the peers' shared memory missing"
+    assert "MEMBAR" not in sass, "no GPU-scope fence in the push combine"
 
 
 def test_cluster_rows_cache_expensive_members():
