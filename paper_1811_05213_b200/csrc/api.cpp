@@ -249,7 +249,9 @@ sfx_kernel* build_kernel(sfx_ctx* ctx, const sfx::Graph& g, int pi, const sfx_co
   if (k->src.cluster > 8)
     sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1),
                   "cuFuncSetAttribute(non-portable cluster)");
-  if (k->src.smem > 48 * 1024)
+  int static_smem = 0;
+  d.cuFuncGetAttribute(&static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, k->fn);
+  if (k->src.smem + static_smem > 48 * 1024)  // the 48 KB default bounds static + dynamic
     sfx::check_cu(d.cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->src.smem),
                   "cuFuncSetAttribute(smem)");
   if (k->src.peer_bytes > 0) {

@@ -64,6 +64,49 @@ bool rcp_divisors() {
   return !(e && e[0] == '1');
 }
 
+// External f32 inputs with `full` elements that the group reads only at the
+// element being computed (every path from a root or a reduction's operand goes
+// through linear-index-preserving edges: elementwise, reshape / bitcast,
+// reshape-like broadcast / transpose, degenerate reduce) — safe to stage per
+// thread in shared memory at the thread's own element.
+std::set<int> identity_inputs(const Ctx& c, int64_t full) {
+  const Graph& g = c.g;
+  std::set<int> local, unsafe;
+  std::set<std::pair<int, bool>> seen;
+  std::function<void(int, bool)> walk = [&](int n, bool ok) {
+    if (!seen.insert({n, ok}).second) return;
+    const Node& m = g.nodes[n];
+    if (!c.p.is_member(n)) {
+      if (m.numel() == full) (ok ? local : unsafe).insert(n);
+      return;
+    }
+    if (m.op == SFX_OP_REDUCE && !degenerate_reduce(g, m)) {
+      for (int o : m.operands) walk(o, g.nodes[o].numel() == full);
+      return;
+    }
+    bool edge = false;
+    if (m.numel() == full) switch (m.op) {
+        case SFX_OP_ELEMENTWISE: case SFX_OP_RESHAPE: case SFX_OP_BITCAST: case SFX_OP_REDUCE:
+          edge = true;
+          break;
+        case SFX_OP_BROADCAST:
+          edge = bcast_is_reshape(m);
+          break;
+        case SFX_OP_TRANSPOSE:
+          edge = transpose_is_reshape(m);
+          break;
+        default:
+          break;
+      }
+    for (int o : m.operands) walk(o, ok && edge);
+  };
+  for (int r : c.p.roots) walk(r, g.nodes[r].numel() == full);
+  std::set<int> out;
+  for (int e : local)
+    if (!unsafe.count(e) && g.nodes[e].dtype == SFX_F32) out.insert(e);
+  return out;
+}
+
 // ---- kernel scaffolding ---------------------------------------------------
 
 std::string signature(const Ctx& c, Emitter& em, const std::string& entry, int block, int min_blocks,

@@ -497,12 +497,129 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     return f->second[em.lane];
   };
   // a pass over this CTA's stripe: UR rows per iteration (unguarded, loads in
-  // flight together), then the remainder
-  auto stripe_pass = [&](const std::function<void(const std::string&)>& row) {
+  // flight together), then the remainder.  Passes alternate direction: every
+  // CTA ends a pass on the rows it read last, which are the ones still in L2
+  // when the grid starts the next pass, so a stripe set larger than L2 re-reads
+  // its most recent rows from L2 instead of HBM (the fold order is the mirror
+  // image: deterministic, a reduction-order difference).  SFX_COLBC_FORWARD=1:
+  // every pass forward (A/B).
+  // Staged inputs (the [O, R, I] inputs read only at the thread's own element):
+  // a per-thread cp.async ring in dynamic shared memory keeps NS x UR rows of
+  // them in flight per thread without holding them in registers (the register
+  // passes are HBM/L2-latency bound at 2 CTAs/SM).  row_pipeline=1: register
+  // passes (A/B).
+  std::vector<int> stage_in;
+  int NS = 0;
+  if (V == 4 && o.row_pipeline != 1) {
+    for (int e : identity_inputs(c, O * R * I)) stage_in.push_back(e);
+    if (!stage_in.empty()) {
+      // static shared memory: per reduce [RSUB][TC] partials + small arrays
+      // (the CTA combine's partials live in the ring once a pass is done)
+      const int64_t part = static_cast<int64_t>(NR) * RSUB * TC * 8;
+      const int64_t budget = std::min<int64_t>(96 * 1024, (220 * 1024) / ctas_per_sm - 4096 - 1024);
+      const int64_t stage_bytes = static_cast<int64_t>(UR) * stage_in.size() * B * 16;
+      NS = static_cast<int>(std::min<int64_t>(4, budget / stage_bytes));
+      if (NS < 2 || NS * stage_bytes < part) {
+        NS = 0;
+        stage_in.clear();
+      } else {
+        ks.smem = static_cast<int>(NS * stage_bytes);
+      }
+    }
+  }
+  if (NS > 0) body.line("extern __shared__ __align__(128) unsigned char sfx_smem[];");
+  const char* fwenv = std::getenv("SFX_COLBC_FORWARD");
+  const bool alternate = !(fwenv && fwenv[0] == '1');
+  int pass_no = 0;
+  auto stripe_pass = [&](const std::function<void(const std::string&)>& row_fwd) {
+    const bool rev = alternate && (pass_no++ % 2 == 1);
+    auto row = [&](const std::string& rf) {
+      if (!rev) return row_fwd(rf);
+      const std::string rr = em.fresh("rr");
+      body.line("const " + it + " " + rr + " = r_begin + r_end - 1 - (" + rf + ");");
+      row_fwd(rr);
+    };
     body.line("if (cok) {");
     body.indent++;
     const std::string r = em.fresh("r");
     body.line(it + " " + r + " = r_begin + rsub;");
+    if (NS > 0) {
+      // cp.async ring: chunk j = this thread's UR rows r_begin + rsub + (j*UR + u)*RSUB;
+      // chunks j+1 .. j+NS-1 are in flight while chunk j is folded
+      const std::string nch = em.fresh("nch"), j = em.fresh("j");
+      body.line("const " + it + " " + nch + "_span = r_end - " + r + " - " + std::to_string((UR - 1) * RSUB) + ";");
+      body.line("const int " + nch + " = " + nch + "_span > 0 ? (int)((" + nch + "_span + " +
+                std::to_string(UR * RSUB - 1) + ") / " + std::to_string(UR * RSUB) + ") : 0;");
+      // linear index (lane 0) of staged input k at stripe row `rr` and this thread's column
+      auto base_of = [&](int k, const std::string& rr) {
+        const Node& in = c.g.nodes[stage_in[k]];
+        em.lane = 0;
+        Ix L = em.linearize(orc_comps(em, in.dims, O, R, I, em.uni("co"), em.uni(rr), inner_ix(0)), in.dims);
+        if (L.kind != IX_PLUS) throw Error(SFX_ERR_INVALID, "internal: colbc staged input is not vectorised");
+        return L.base;
+      };
+      auto slot_ptr = [&](const std::string& slot, int u, int k) {
+        return "(sfx_smem + ((((" + slot + ") * " + std::to_string(UR) + " + " + std::to_string(u) + ") * " +
+               std::to_string(stage_in.size()) + " + " + std::to_string(k) + ") * " + std::to_string(B) +
+               " + threadIdx.x) * 16)";
+      };
+      auto issue = [&](const std::string& jn) {
+        em.push();
+        for (int u = 0; u < UR; ++u) {
+          std::string rf = em.fresh("rf");
+          body.line("const " + it + " " + rf + " = " + r + " + ((" + it + ")(" + jn + ") * " + std::to_string(UR) + " + " +
+                    std::to_string(u) + ") * " + std::to_string(RSUB) + ";");
+          std::string rr = rf;
+          if (rev) {
+            rr = em.fresh("rr");
+            body.line("const " + it + " " + rr + " = r_begin + r_end - 1 - (" + rf + ");");
+          }
+          for (size_t k = 0; k < stage_in.size(); ++k)
+            body.line("sfx_cp_async16(" + slot_ptr("(" + jn + ") % " + std::to_string(NS), u, static_cast<int>(k)) +
+                      ", " + em.input_ptr.at(stage_in[k]) + " + " + base_of(static_cast<int>(k), rr) + ");");
+        }
+        em.pop();
+      };
+      for (int k = 0; k < NS - 1; ++k) {
+        body.line("if (" + std::to_string(k) + " < " + nch + ") {");
+        body.indent++;
+        issue(std::to_string(k));
+        body.indent--;
+        body.line("}");
+        body.line("sfx_cp_async_commit();");
+      }
+      body.line("for (int " + j + " = 0; " + j + " < " + nch + "; ++" + j + ") {");
+      body.indent++;
+      body.line("if (" + j + " + " + std::to_string(NS - 1) + " < " + nch + ") {");
+      body.indent++;
+      issue(j + " + " + std::to_string(NS - 1));
+      body.indent--;
+      body.line("}");
+      body.line("sfx_cp_async_commit();");
+      body.line("sfx_cp_async_wait<" + std::to_string(NS - 1) + ">();  // chunk " + j + " landed (own copies only)");
+      em.push();
+      for (int u = 0; u < UR; ++u) {
+        std::string rf = em.fresh("ru");
+        body.line("const " + it + " " + rf + " = " + r + " + ((" + it + ")" + j + " * " + std::to_string(UR) + " + " +
+                  std::to_string(u) + ") * " + std::to_string(RSUB) + ";");
+        std::string rr = rf;
+        if (rev) {
+          rr = em.fresh("rr");
+          body.line("const " + it + " " + rr + " = r_begin + r_end - 1 - (" + rf + ");");
+        }
+        for (size_t k = 0; k < stage_in.size(); ++k) {
+          std::string sp = em.fresh("sp");
+          body.line("const float* " + sp + " = (const float*)" + slot_ptr(j + " % " + std::to_string(NS), u, static_cast<int>(k)) + ";");
+          em.staged[stage_in[k]] = {sp, base_of(static_cast<int>(k), rr)};
+        }
+        row_fwd(rr);
+        em.staged.clear();
+      }
+      em.pop();
+      body.indent--;
+      body.line("}");
+      body.line(r + " += (" + it + ")" + nch + " * " + std::to_string(UR * RSUB) + ";");
+    } else {
     body.line("for (; " + r + " + " + std::to_string((UR - 1) * RSUB) + " < r_end; " + r + " += " +
               std::to_string(UR * RSUB) + ") {");
     body.indent++;
@@ -515,6 +632,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     em.pop();
     body.indent--;
     body.line("}");
+    }
     body.line("for (; " + r + " < r_end; " + r + " += " + std::to_string(RSUB) + ") {");
     body.indent++;
     em.push();
@@ -556,7 +674,16 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     for (size_t k = 0; k < red.size(); ++k) {
       const std::string T = acc_t(red[k]);
       const std::string sp = em.fresh("sp");
-      body.line("__shared__ " + T + " " + sp + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
+      if (NS > 0) {
+        // the CTA combine reuses the (now idle) cp.async ring: reduction k's
+        // [RSUB][TC] partials at k * RSUB * TC * 8 bytes; the barrier keeps
+        // slower threads' last ring reads ahead of the partial writes
+        if (k == 0) body.line("__syncthreads();");
+        body.line(T + " (*" + sp + ")[" + fmt_i(TC) + "] = reinterpret_cast<" + T + " (*)[" + fmt_i(TC) +
+                  "]>(sfx_smem + " + fmt_i(static_cast<int64_t>(k) * RSUB * TC * 8) + ");");
+      } else {
+        body.line("__shared__ " + T + " " + sp + "[" + std::to_string(RSUB) + "][" + fmt_i(TC) + "];");
+      }
       for (int l = 0; l < V; ++l)
         body.line(sp + "[rsub][cl * " + std::to_string(V) + " + " + std::to_string(l) + "] = " + acc[k][l] + ";");
       body.line("__syncthreads();");
@@ -741,7 +868,8 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   ks.vector_width = V;
   ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
             " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " levels=" +
-            std::to_string(bp.max_level) + " (grid barriers, cooperative launch)";
+            std::to_string(bp.max_level) + " (grid barriers, cooperative launch)" +
+            (NS > 0 ? ", cp.async ring " + std::to_string(NS) + " x " + std::to_string(UR) + " rows" : "");
   return ks;
 }
 

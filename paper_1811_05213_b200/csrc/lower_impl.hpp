@@ -109,6 +109,7 @@ KernelSource lower_row_pipe(const Ctx& c, const RowPlan& rp, const std::set<int>
                             const sfx_compile_opts& o);
 void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH);
 std::set<int> row_local_inputs(const Ctx& c, const RowPlan& rp);
+std::set<int> identity_inputs(const Ctx& c, int64_t full);
 
 // ---- column templates (lower_col.cpp) ----
 std::vector<Ix> orc_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t O, int64_t R, int64_t I,

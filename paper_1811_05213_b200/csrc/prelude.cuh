@@ -250,6 +250,14 @@ __device__ __forceinline__ void sfx_dsmem_push(int* p, int v, unsigned long long
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
                :: "r"(sfx_dsmem_addr(p, rank)), "r"(v), "r"(sfx_dsmem_addr(bar, rank)) : "memory");
 }
+// Per-thread asynchronous global -> shared copies (LDGSTS, L2 only): a thread
+// reads back only what it copied itself, after cp.async.wait_group.
+__device__ __forceinline__ void sfx_cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sfx_smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void sfx_cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void sfx_cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 // split cluster barrier: a relaxed arrive (no memory ordering; the mbarrier
 // inits are published by fence.mbarrier_init) and the matching wait
 __device__ __forceinline__ void sfx_cluster_arrive_relaxed() {

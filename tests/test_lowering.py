@@ -64,6 +64,20 @@ def test_cluster_rows_cache_expensive_members():
     assert "cached" not in note and "sfx_sts4((float*)" not in src
 
 
+def test_colbc_stages_stripes_through_a_cp_async_ring():
+    """Batch-norm passes keep their stripe rows in flight through a per-thread
+    cp.async ring in dynamic shared memory (LDGSTS in SASS); row_pipeline=1
+    keeps the register passes."""
+    src, cubin, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
+    assert "cp.async ring 3 x 8 rows" in note and "sfx_cp_async_wait<2>()" in src
+    sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
+    assert "LDGSTS" in sass and "LDGDEPBAR" in sass
+    src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"), row_pipeline=1)
+    assert "cp.async ring" not in note and "sfx_cp_async16((" not in src
+    _, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"), items_per_thread=4)
+    assert "cp.async ring 4 x 4 rows" in note
+
+
 def test_colbc_is_cooperative_with_grid_barriers():
     src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
     assert "sfx_grid_barrier(ws, 4u)" in src and "sfx_grid_exit(ws)" in src

@@ -39,7 +39,7 @@ for name, doc in CASES.items():
     bpath = os.path.join(tempfile.gettempdir(), name + ".json")
     open(bpath, "w").write(out)
     g, rep, b = H.load_bundle(bpath)
-    variants = [{}] + ([{"pipe_ctas_per_sm": 3}, {"pipe_ctas_per_sm": 4}, {"pipe_ctas_per_sm": 4, "items_per_thread": 4}, {"pipe_ctas_per_sm": 1, "items_per_thread": 16}] if name.startswith("batchnorm") else [{"row_pipeline": 1}, {"pipe_stages": 8}, {"row_pipeline": 5}, {"row_pipeline": 3}])
+    variants = [{}] + ([{"row_pipeline": 1}, {"items_per_thread": 4}, {"items_per_thread": 2}, {"pipe_ctas_per_sm": 1}, {"pipe_ctas_per_sm": 3}] if name.startswith("batchnorm") else [{"row_pipeline": 1}, {"pipe_stages": 8}, {"row_pipeline": 5}, {"row_pipeline": 3}])
     if "--literal" in sys.argv:
         variants.append({"strategy": "literal"})
     pick = [a[len("--variant="):] for a in sys.argv if a.startswith("--variant=")]
