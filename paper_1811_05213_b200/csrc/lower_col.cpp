@@ -428,7 +428,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   S = std::min<int64_t>(S, std::max<int64_t>(1, R / RSUB));
   S = std::max<int64_t>(1, std::min<int64_t>(S, kNumSMs * ctas_per_sm / tiles));
   const int64_t RS = (R + S - 1) / S;
-  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
+  int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
   const int NR = static_cast<int>(c.reduces.size());
   Emitter em(c.g, c.p, V, c.wide);
   em.rcp_reduced_divisors = rcp_divisors();
@@ -517,8 +517,14 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
       // (the CTA combine's partials live in the ring once a pass is done)
       const int64_t part = static_cast<int64_t>(NR) * RSUB * TC * 8;
       const int64_t budget = std::min<int64_t>(96 * 1024, (220 * 1024) / ctas_per_sm - 4096 - 1024);
-      const int64_t stage_bytes = static_cast<int64_t>(UR) * stage_in.size() * B * 16;
+      int64_t stage_bytes = static_cast<int64_t>(UR) * stage_in.size() * B * 16;
       NS = static_cast<int>(std::min<int64_t>(4, budget / stage_bytes));
+      // several staged inputs: fewer rows per stage, same rows in flight
+      while (NS < 2 && UR > 2 && o.items_per_thread == 0) {
+        UR /= 2;
+        stage_bytes /= 2;
+        NS = static_cast<int>(std::min<int64_t>(4, budget / stage_bytes));
+      }
       if (NS < 2 || NS * stage_bytes < part) {
         NS = 0;
         stage_in.clear();

@@ -83,6 +83,35 @@ EXTRA = {
         {"id": "gb", "op": "broadcast", "operands": ["g"], "shape": [80, 98304], "broadcast_dim_map": [1]},
         {"id": "n", "op": "mul", "operands": ["x", "rb"], "shape": [80, 98304]},
         {"id": "y", "op": "mul", "operands": ["n", "gb"], "shape": [80, 98304]}], "outputs": ["y"]},
+    # masked softmax over long rows with e also output (2e): two staged inputs, the
+    # cached member e (written over x's slice) feeds two roots of the final pass
+    "softmaxmask_r4_c131072": {"instructions": [
+        {"id": "x", "op": "parameter", "shape": [4, 131072]},
+        {"id": "mask", "op": "parameter", "shape": [4, 131072]},
+        {"id": "xm", "op": "add", "operands": ["x", "mask"], "shape": [4, 131072]},
+        {"id": "mx", "op": "reduce", "operands": ["xm"], "shape": [4], "reduce_dims": [1], "reducer": "max"},
+        {"id": "mxb", "op": "broadcast", "operands": ["mx"], "shape": [4, 131072], "broadcast_dim_map": [0]},
+        {"id": "z", "op": "sub", "operands": ["xm", "mxb"], "shape": [4, 131072]},
+        {"id": "e", "op": "exp", "operands": ["z"], "shape": [4, 131072]},
+        {"id": "s", "op": "reduce", "operands": ["e"], "shape": [4], "reduce_dims": [1], "reducer": "sum"},
+        {"id": "sb", "op": "broadcast", "operands": ["s"], "shape": [4, 131072], "broadcast_dim_map": [0]},
+        {"id": "y", "op": "div", "operands": ["e", "sb"], "shape": [4, 131072]},
+        {"id": "e_out", "op": "scale", "operands": ["e"], "shape": [4, 131072], "scalar": 2.0}], "outputs": ["y", "e_out"]},
+    # batch-norm backward-like: two column sums of two streamed inputs (dy, x)
+    # broadcast back — the colbc cp.async ring with two staged inputs
+    "bnbwd_4096x256": {"instructions": [
+        {"id": "dy", "op": "parameter", "shape": [4096, 256]},
+        {"id": "x", "op": "parameter", "shape": [4096, 256]},
+        {"id": "s1", "op": "reduce", "operands": ["dy"], "shape": [256], "reduce_dims": [0], "reducer": "sum"},
+        {"id": "dyx", "op": "mul", "operands": ["dy", "x"], "shape": [4096, 256]},
+        {"id": "s2", "op": "reduce", "operands": ["dyx"], "shape": [256], "reduce_dims": [0], "reducer": "sum"},
+        {"id": "m1", "op": "scale", "operands": ["s1"], "shape": [256], "scalar": 1.0 / 4096},
+        {"id": "m2", "op": "scale", "operands": ["s2"], "shape": [256], "scalar": 1.0 / 4096},
+        {"id": "m1b", "op": "broadcast", "operands": ["m1"], "shape": [4096, 256], "broadcast_dim_map": [1]},
+        {"id": "m2b", "op": "broadcast", "operands": ["m2"], "shape": [4096, 256], "broadcast_dim_map": [1]},
+        {"id": "t1", "op": "sub", "operands": ["dy", "m1b"], "shape": [4096, 256]},
+        {"id": "t2", "op": "mul", "operands": ["x", "m2b"], "shape": [4096, 256]},
+        {"id": "dx", "op": "sub", "operands": ["t1", "t2"], "shape": [4096, 256]}], "outputs": ["dx"]},
     # innermost-moving transposes with ragged 64x64 tiles: the 128-bit swizzled
     # tile (both axes multiples of 4) and the scalar tile (odd extents)
     "tr_8x300x140": {"instructions": [

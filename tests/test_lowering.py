@@ -62,6 +62,9 @@ def test_cluster_rows_cache_expensive_members():
     assert "cached" not in note and "sfx_sts4((float*)" not in src
     src, _, note = _note(os.path.join(EXTRA, "ln_r6_c98304.json"))
     assert "cached" not in note and "sfx_sts4((float*)" not in src
+    # masked softmax: two staged inputs, e cached over x's slice, read by both roots
+    src, _, note = _note(os.path.join(EXTRA, "softmaxmask_r4_c131072.json"))
+    assert "2 input slice(s)" in note and "1 member(s) cached" in note
 
 
 def test_colbc_stages_stripes_through_a_cp_async_ring():
@@ -76,6 +79,9 @@ def test_colbc_stages_stripes_through_a_cp_async_ring():
     assert "cp.async ring" not in note and "sfx_cp_async16((" not in src
     _, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"), items_per_thread=4)
     assert "cp.async ring 4 x 4 rows" in note
+    # two staged inputs (dy, x): half the rows per stage
+    _, _, note = _note(os.path.join(EXTRA, "bnbwd_4096x256.json"))
+    assert "cp.async ring 3 x 4 rows" in note
 
 
 def test_colbc_is_cooperative_with_grid_barriers():
