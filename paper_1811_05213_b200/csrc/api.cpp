@@ -279,6 +279,34 @@ struct StreamArgs {
   long long chunk_elems = 0;
 };
 
+// Per-group launch log (metrics): SFX_LAUNCH_LOG=stderr|<path> writes
+// one line per launch — kernel, template, grid / block / dynamic smem /
+// registers, algorithmic bytes — and, outside stream capture, the launch's
+// device time from CUDA events around it (the log synchronises every launch:
+// a diagnostic mode, not for benchmarking), its GB/s and the fraction of
+// SFX_PEAK_GBS (default 6538.6 GB/s, the measured B200 copy peak).  Launches
+// recorded into a CUDA graph are logged as "captured", untimed.
+struct LaunchLog {
+  FILE* f = nullptr;
+  double peak = 6538.6;
+  std::mutex mu;
+};
+LaunchLog* launch_log() {
+  static LaunchLog* log = []() -> LaunchLog* {
+    const char* e = std::getenv("SFX_LAUNCH_LOG");
+    if (!e || !e[0]) return nullptr;
+    auto* L = new LaunchLog;
+    L->f = std::strcmp(e, "stderr") == 0 ? stderr : std::fopen(e, "a");
+    if (!L->f) {
+      delete L;
+      return nullptr;
+    }
+    if (const char* pk = std::getenv("SFX_PEAK_GBS")) L->peak = std::atof(pk) > 0 ? std::atof(pk) : L->peak;
+    return L;
+  }();
+  return log;
+}
+
 void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::vector<CUdeviceptr>& out, CUstream s,
                 const StreamArgs& sa, bool drop_last_cta);
 
@@ -425,8 +453,40 @@ void launch_raw(sfx_kernel* k, const std::vector<CUdeviceptr>& in, const std::ve
   cfg.numAttrs = n_attr;
   // one NVTX range per group launch, named by its kernel (ncu --nvtx / nsys timelines)
   nvtxRangePushA(k->src.entry.c_str());
+  LaunchLog* log = launch_log();
+  CUevent ev[2] = {nullptr, nullptr};
+  if (log) {
+    CUstreamCaptureStatus cs = CU_STREAM_CAPTURE_STATUS_NONE;
+    sfx::driver().cuStreamIsCapturing(s, &cs);
+    if (cs == CU_STREAM_CAPTURE_STATUS_NONE) {
+      sfx::driver().cuEventCreate(&ev[0], CU_EVENT_DEFAULT);
+      sfx::driver().cuEventCreate(&ev[1], CU_EVENT_DEFAULT);
+      sfx::driver().cuEventRecord(ev[0], s);
+    }
+  }
   CUresult lr = sfx::driver().cuLaunchKernelEx(&cfg, k->fn, args.data(), nullptr);
   nvtxRangePop();
+  if (log) {
+    float ms = -1.0f;
+    if (ev[0]) {
+      sfx::driver().cuEventRecord(ev[1], s);
+      if (lr == CUDA_SUCCESS && sfx::driver().cuEventSynchronize(ev[1]) == CUDA_SUCCESS)
+        sfx::driver().cuEventElapsedTime(&ms, ev[0], ev[1]);
+      sfx::driver().cuEventDestroy(ev[0]);
+      sfx::driver().cuEventDestroy(ev[1]);
+    }
+    std::lock_guard<std::mutex> g(log->mu);
+    std::fprintf(log->f, "sfx launch %s strategy=%s grid=%ux%u block=%u smem=%d regs=%d bytes=%lld", k->src.entry.c_str(),
+                 k->src.strategy.c_str(), cfg.gridDimX, cfg.gridDimY, cfg.blockDimX, k->src.smem, k->regs,
+                 static_cast<long long>(k->src.algorithmic_bytes));
+    if (ms > 0.0f) {
+      const double gbs = static_cast<double>(k->src.algorithmic_bytes) / (ms * 1e-3) / 1e9;
+      std::fprintf(log->f, " us=%.2f GB/s=%.0f peak_frac=%.3f\n", ms * 1e3, gbs, gbs / log->peak);
+    } else {
+      std::fprintf(log->f, " %s\n", ev[0] ? "untimed" : "captured");
+    }
+    std::fflush(log->f);
+  }
   sfx::check_cu(lr, "cuLaunchKernelEx");
   k->ctx->launches.fetch_add(1);
 }
