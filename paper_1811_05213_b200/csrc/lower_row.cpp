@@ -289,7 +289,7 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
   // peer is at most one row ahead at any level).  SFX_CLUSTER_BARRIER_COMBINE=1:
   // the barrier protocol (A/B).
   const char* cbenv = std::getenv("SFX_CLUSTER_BARRIER_COMBINE");
-  const bool push = CS > 1 && !(cbenv && cbenv[0] == '1');
+  const bool push = CS > 1 && rp.max_level > 0 && !(cbenv && cbenv[0] == '1');
   const int NPAR = persist ? 2 : 1;
   std::vector<int64_t> level_bytes(rp.max_level + 1, 0);
   for (int r : c.reduces) {

@@ -152,18 +152,34 @@ def test_encoder_layer_head_split_full_size(ctx, root):
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C5"])
-def test_tma_row_pipeline_small(ctx, name):
-    """The TMA-staged (cp.async.bulk + mbarrier) row template, where applicable."""
+@pytest.mark.parametrize("pipe,prefix", [(2, "sfx_rowp_"), (4, "sfx_rowr_")])
+def test_tma_row_pipeline_small(ctx, name, pipe, prefix):
+    """The TMA-staged (cp.async.bulk + mbarrier) row templates, where applicable:
+    the per-warp pipeline (row_pipeline=2) and resident rows (row_pipeline=4,
+    every row of a CTA's range staged at entry)."""
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
     inputs = T.gen_inputs(g, 43, -1.0, 1.0)
-    cg = H.CompiledGraph(ctx, g, rep, row_pipeline=2)
+    cg = H.CompiledGraph(ctx, g, rep, row_pipeline=pipe)
     try:
         entries = [k.info["entry"] for k in cg.kernels]
         outs = cg.run_host(inputs)
     finally:
         cg.close()
-    assert any(e.startswith("sfx_rowp_") for e in entries), entries
+    assert any(e.startswith(prefix) for e in entries), entries
     assert not _check(g, outs, inputs, strict=True)
+
+
+def test_resident_rows_full_c1(ctx):
+    """Resident rows at C1's full size: 148 CTAs of up to 56 rows (224 KB of
+    shared memory each) — bit-identical to the register-row template (same
+    per-thread fold order), which test_configs_full_size checks against the
+    fp64 restatement."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C1.full.json"))
+    prog = rep.kernels[0].program
+    inputs = T.gen_inputs_fast(g, 5, -1.0, 1.0)
+    (y,) = H.run_program(prog, g, inputs, ctx=ctx, row_pipeline=4)
+    (ref,) = H.run_program(prog, g, inputs, ctx=ctx)
+    assert np.array_equal(y, ref)
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t"])
