@@ -34,7 +34,8 @@ def test_launch_log(tmp_path):
     assert r.returncode == 0, r.stderr[-2000:]
     n = int(r.stdout.split("launches")[1].split()[0])
     lines = [l for l in log.read_text().splitlines() if l.startswith("sfx launch ")]
-    assert len(lines) == n == 5, lines
+    # C5.small plans 4 groups (h1 and h2 merge below the 64 MiB footprint cap)
+    assert len(lines) == n == 4, (n, log.read_text(), r.stderr[-2000:])
     for l in lines:
         f = dict(kv.split("=", 1) for kv in l.split()[3:] if "=" in kv)
         assert f["strategy"] in ("map", "row", "col") and int(f["bytes"]) > 0 and int(f["regs"]) > 0, l
