@@ -171,15 +171,17 @@ def test_tma_row_pipeline_small(ctx, name, pipe, prefix):
 
 def test_resident_rows_full_c1(ctx):
     """Resident rows at C1's full size: 148 CTAs of up to 56 rows (224 KB of
-    shared memory each) — bit-identical to the register-row template (same
-    per-thread fold order), which test_configs_full_size checks against the
-    fp64 restatement."""
+    shared memory each) — bit-identical to the one-warp-per-row register
+    template (same per-thread fold order); test_configs_full_size checks the
+    tuned template against the fp64 restatement."""
     g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C1.full.json"))
     prog = rep.kernels[0].program
     inputs = T.gen_inputs_fast(g, 5, -1.0, 1.0)
     (y,) = H.run_program(prog, g, inputs, ctx=ctx, row_pipeline=4)
-    (ref,) = H.run_program(prog, g, inputs, ctx=ctx)
+    (ref,) = H.run_program(prog, g, inputs, ctx=ctx, threads_per_row=32)  # one warp per row, like rowr
     assert np.array_equal(y, ref)
+    (tuned,) = H.run_program(prog, g, inputs, ctx=ctx)  # the cache's 4-warp rows: another fold order
+    assert T.strict_close(y, tuned)
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t"])
