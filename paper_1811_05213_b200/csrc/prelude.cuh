@@ -288,7 +288,13 @@ __device__ __forceinline__ int sfx_ld(const int* p) { return __ldg(p); }
 // once and the inputs still streaming in keep the L2 (measured on B200:
 // probs_d 463 -> 449 us, ctx_r 37.2 -> 35.3 us, h1 66.0 -> 63.9 us).
 __device__ __forceinline__ void sfx_st4(float* p, float a, float b, float c, float d) {
+#if defined(SFX_EXP_WB_STORES)  // A/B: default write-back stores
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+#elif defined(SFX_EXP_ST_NOCLOBBER)  // A/B: no compiler memory barrier at each store
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d));
+#else
   asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+#endif
 }
 __device__ __forceinline__ void sfx_st4(int* p, int a, int b, int c, int d) {
   asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
