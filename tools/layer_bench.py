@@ -12,6 +12,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import torch
 
@@ -63,31 +64,45 @@ def main():
             scratch[node] = torch.empty(g.at(node).shape, device=dev)
         return scratch[node].data_ptr()
 
+    from bench import Clocks  # nvidia-smi sampler (clocks under load)
+    clocks = Clocks(0).start()
     rows = []
     for k, kind in kernels:
         out_ids = k.roots
         ip = [buf(i) for i in k.input_ids]
         op = [buf(o) for o in out_ids]
+        reps = 40 if k.info["strategy"] == "dot" else 5  # matmuls: >= 100 ms, several clock samples
         with torch.cuda.stream(s):
             for _ in range(2):
                 k.launch(ip, op, stream=s.cuda_stream)
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
             a.record(s)
-            for _ in range(5):
+            for _ in range(reps):
                 k.launch(ip, op, stream=s.cuda_stream)
             z.record(s)
             s.synchronize()
-        t = a.elapsed_time(z) / 5
+            t1 = time.perf_counter()
+        t = a.elapsed_time(z) / reps
         row = {"kernel": k.info["entry"], "kind": kind, "strategy": k.info["strategy"], "ms": round(t, 4)}
         if k.info["strategy"] == "dot":
             node = g.at(out_ids[0])
             K = g.at(node.operands[0]).shape[-1]
             row["tflops"] = round(2.0 * node.numel() * K / t / 1e9, 2)
+            # the SIMT ceiling at the clock the matmul actually ran at: 148 SMs x 128
+            # FP32 lanes, one FMUL + one FADD per multiply-add (2 flops / 2 issues)
+            ck = clocks.summary(t0, t1)
+            row["clocks"] = ck
+            if ck.get("sm_mhz"):
+                ceil = 148 * 128 * ck["sm_mhz"] * 1e6 / 1e12
+                row["simt_ceiling_tflops_at_clock"] = round(ceil, 2)
+                row["frac_of_ceiling_at_clock"] = round(row["tflops"] / ceil, 3)
         else:
             row["gbs"] = round(k.info["algorithmic_bytes"] / t / 1e6, 1)
         rows.append(row)
     dot_ms = sum(r["ms"] for r in rows if r["strategy"] == "dot")
     other_ms = sum(r["ms"] for r in rows if r["strategy"] != "dot")
+    clocks.stop()
     print(json.dumps({"config": args.config, "layer_ms": round(ms, 3), "launches_per_layer": launched,
                       "sum_kernel_ms": round(dot_ms + other_ms, 3), "matmul_ms": round(dot_ms, 3),
                       "non_matmul_ms": round(other_ms, 3), "kernels": rows}), flush=True)
