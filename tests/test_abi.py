@@ -124,6 +124,20 @@ def test_matmul_groups_lower():
     assert seen == {"dot", "literal"}
 
 
+def _assert_no_contraction(sass):
+    """Every multiply-add of the dot kernel rounds twice: FMUL + FADD, or the
+    packed FFMA2 whose addend is the same run-time zero pair in every
+    instruction (the product alone) followed by FADD2; never a scalar FFMA."""
+    import re
+    lines = [l for l in sass.splitlines() if re.search(r"\bFFMA2?\b", l)]
+    assert not [l for l in lines if re.search(r"\bFFMA\b", l)], "scalar FFMA contracts a multiply-add"
+    addends = {re.split(r",\s*", l.split("FFMA2", 1)[1].split(";")[0])[-1].split(".")[0].strip() for l in lines}
+    if lines:
+        assert len(addends) == 1 and "FADD2" in sass, addends
+    else:
+        assert "FMUL" in sass and "FADD" in sass
+
+
 def test_unfused_instructions_lower():
     """Instructions no group took (run by the reference through eval_dense)
     compile to one kernel each; matmuls to the dot kernel, whose fp32 loop has
@@ -140,7 +154,7 @@ def test_unfused_instructions_lower():
                     assert note.startswith("dot matmul barrier"), note
                     if g.at(u).dtype == "f32" and n["dot"] < 8:
                         sass = subprocess.run(["cuobjdump", "-sass", cubin], capture_output=True, text=True).stdout
-                        assert "FMUL" in sass and "FFMA" not in sass
+                        _assert_no_contraction(sass)
                     n["dot"] += 1
                 else:
                     n["other"] += 1

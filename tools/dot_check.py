@@ -21,7 +21,9 @@ SHAPES = [  # (name, batch dims, M, K, N, op)
     ("ffn_up", [], 32768, 768, 3072, "library_call"),
     ("qkv", [], 32768, 768, 768, "library_call"),
     ("scores", [768], 512, 64, 512, "batch_matmul"),
-    ("ragged", [3], 1000, 77, 333, "batch_matmul"),
+    ("ctx", [768], 512, 512, 64, "batch_matmul"),
+    ("ragged", [3], 1000, 77, 333, "batch_matmul"),        # K % 4 != 0: the FMUL + FADD kernel
+    ("ragged_packed", [3], 1000, 76, 332, "batch_matmul"),  # ragged tiles on the packed kernel
 ]
 
 
@@ -75,7 +77,8 @@ def main():
             exact += int(np.float32(got).tobytes() == want.tobytes())
         print(json.dumps({"shape": name, "batch": batch, "M": M, "K": K, "N": N, "ms": round(ms, 4),
                           "tflops": round(flops / ms / 1e9, 2), "bit_exact_samples": f"{exact}/{samples}",
-                          "registers": k.info["registers"], "grid": k.info["grid"]}), flush=True)
+                          "registers": k.info["registers"], "grid": k.info["grid"],
+                          "packed": k.info["smem_bytes"] > 48 * 1024}), flush=True)
         cg.close()
         del a, b, c
     ctx.close()
