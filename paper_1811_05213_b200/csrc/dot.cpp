@@ -29,6 +29,7 @@
 
 #include "emit.hpp"
 #include "lower.hpp"
+#include "lower_impl.hpp"
 
 namespace sfx {
 
@@ -97,6 +98,9 @@ const char* kDotKernel = R"SFXDOT(
 #define NT ((BM / TM) * (BN / TN))
 #define LA ((BM * BK) / NT)
 #define LB ((BK * BN) / NT)
+#define A_KFAST $A_KFAST
+#define B_KFAST $B_KFAST
+#define PACKED $PACKED
 typedef $T T;
 typedef $T4 T4;
 
@@ -104,6 +108,7 @@ extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const long long M = $M, N = $N, K = $K;
+$PROLOGUE
   __shared__ __align__(16) T As[2][BK][BM + 4];
   __shared__ __align__(16) T Bs[2][BK][BN + 4];
   const int tid = threadIdx.x;
@@ -115,16 +120,22 @@ extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
   const long long b = t / $TILES_M;
   const long long m0 = mb * BM, n0 = nb * BN;
   T ra[LA], rb[LB];
+  // staging order: consecutive threads take consecutive k (A_KFAST / B_KFAST)
+  // or consecutive m / n, whichever is contiguous in the operand's source memory
+#define A_ROW(e) (A_KFAST ? (e) / BK : (e) % BM)
+#define A_KK(e) (A_KFAST ? (e) % BK : (e) / BM)
+#define B_KK(e) (B_KFAST ? (e) % BK : (e) / BN)
+#define B_COL(e) (B_KFAST ? (e) / BK : (e) % BN)
   auto fetch = [&](long long k0) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
-      const int e = tid + i * NT, row = e / BK, kk = e % BK;
+      const int e = tid + i * NT, row = A_ROW(e), kk = A_KK(e);
       const long long m = m0 + row, k = k0 + kk;
       ra[i] = (m < M && k < K) ? $LOAD_A(b * M * K + m * K + k) : T(0);
     }
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
-      const int e = tid + i * NT, kk = e / BN, col = e % BN;
+      const int e = tid + i * NT, kk = B_KK(e), col = B_COL(e);
       const long long k = k0 + kk, n = n0 + col;
       rb[i] = (k < K && n < N) ? $LOAD_B(b * K * N + k * N + n) : T(0);
     }
@@ -133,19 +144,35 @@ extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const int e = tid + i * NT;
-      As[buf][e % BK][e / BK] = ra[i];
+      As[buf][A_KK(e)][A_ROW(e)] = ra[i];
     }
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
       const int e = tid + i * NT;
-      Bs[buf][e / BN][e % BN] = rb[i];
+      Bs[buf][B_KK(e)][B_COL(e)] = rb[i];
     }
   };
+#if PACKED
+  // f32 on the packed fp32x2 datapath (see kDotKernel2): t = fma(a, b, Z),
+  // acc = acc + t, Z a zero ptxas cannot see
+  typedef unsigned long long u64;
+  unsigned dsz;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+  const float zf = __uint_as_float(dsz >> 20);
+  u64 Z;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(Z) : "f"(zf), "f"(zf));
+  u64 acc2[TM][TN / 2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN / 2; ++j) acc2[i][j] = 0ull;
+#else
   T acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+#endif
   fetch(0);
   stash(0);
   __syncthreads();
@@ -176,10 +203,27 @@ extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
 #pragma unroll
       for (int j = 0; j < TN; ++j) v[j] = Bs[buf][kk][tx * TN + j];
 #endif
+#if PACKED
+      u64 vp[TN / 2];
+#pragma unroll
+      for (int j = 0; j < TN / 2; ++j) asm("mov.b64 %0, {%1, %2};" : "=l"(vp[j]) : "f"(v[2 * j]), "f"(v[2 * j + 1]));
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        u64 ap;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(ap) : "f"(a[i]), "f"(a[i]));
+#pragma unroll
+        for (int j = 0; j < TN / 2; ++j) {
+          u64 pr;
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pr) : "l"(ap), "l"(vp[j]), "l"(Z));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[i][j]) : "l"(acc2[i][j]), "l"(pr));
+        }
+      }
+#else
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = sfx_add(acc[i][j], sfx_mul(a[i], v[j]));
+#endif
     }
     if (more) stash(buf ^ 1);
     __syncthreads();
@@ -190,10 +234,18 @@ extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
     const long long m = m0 + ty * TM + i;
     if (m >= M) continue;
     T* row = out0 + b * M * N + m * N;
+#if PACKED
+    T accr[TN];
+#pragma unroll
+    for (int j = 0; j < TN / 2; ++j)
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(accr[2 * j]), "=f"(accr[2 * j + 1]) : "l"(acc2[i][j]));
+#else
+    const T* accr = acc[i];
+#endif
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const long long n = n0 + tx * TN + j;
-      if (n < N) row[n] = acc[i][j];
+      if (n < N) row[n] = accr[j];
     }
   }
 }
@@ -419,7 +471,11 @@ KernelSource lower_dot(const Graph& g, const Program& p) {
                                         {"$PARAMS", params},
                                         {"$M", fmt_i(M)},
                                         {"$N", fmt_i(N)},
-                                        {"$K", fmt_i(K)}});
+                                        {"$K", fmt_i(K)},
+                                        {"$PROLOGUE", ""},
+                                        {"$A_KFAST", "1"},
+                                        {"$B_KFAST", "0"},
+                                        {"$PACKED", f32 && TN % 2 == 0 && dot_packed() ? "1" : "0"}});
   // $LOAD_A(expr) -> __ldg(inK + (expr)), or the literal of a splat constant
   auto expand = [&](const std::string& key, int operand) {
     const Node& o = g.nodes[operand];
@@ -447,6 +503,213 @@ KernelSource lower_dot(const Graph& g, const Program& p) {
   std::ostringstream note;
   note << (p.barrier ? "matmul barrier [" : "matmul group [") << batch << " x " << M << " x " << K << "] @ [" << K << " x " << N << "]: tile " << BM
        << "x" << BN << "x16, " << TM << "x" << TN << " per thread, " << grid << " CTAs; sequential-k fp32 (bit-exact)";
+  ks.note = note.str();
+  return ks;
+}
+
+
+// fuse_dot groups whose only root is the matmul and whose other members are
+// elementwise / layout ops producing its operands (the reference planner with
+// fuse_dot stitches e.g. bias add + head reshape + transpose into Q K^T, or the
+// softmax normalisation x dropout mask into P V; fusion.cpp / span.cpp): the
+// register-staged SIMT matmul above, with each operand element computed from the
+// group's externals where the tile is staged (one generated expression per
+// operand, the map template's index algebra) instead of read from a
+// materialised tensor.  Same k order, same roundings: bit-identical to the
+// reference's dot_loop over the stitched operands.
+bool dot_prologue_ok(const Graph& g, const Program& p, std::string* why) {
+  auto fail = [&](const std::string& w) {
+    if (why) *why = w;
+    return false;
+  };
+  int dot = -1;
+  for (int m : p.members) {
+    const Node& n = g.nodes[m];
+    if (is_matmul(n)) {
+      if (dot >= 0) return fail("more than one matmul");
+      dot = m;
+      continue;
+    }
+    switch (n.op) {
+      case SFX_OP_ELEMENTWISE: case SFX_OP_RESHAPE: case SFX_OP_BITCAST: case SFX_OP_TRANSPOSE: case SFX_OP_BROADCAST:
+        break;
+      case SFX_OP_REDUCE:
+        if (n.reduce_dims.empty() || n.numel() == g.nodes[n.operands[0]].numel()) break;
+        return fail("a reduction feeds the matmul");
+      default:
+        return fail("unsupported member " + n.id);
+    }
+  }
+  if (dot < 0) return fail("no matmul");
+  if (p.roots.size() != 1 || p.roots[0] != dot) return fail("the matmul is not the only root");
+  if (g.nodes[dot].op != SFX_OP_BATCH_MATMUL) return fail("library call");
+  return true;
+}
+
+// Host-side index map of a stitched operand: follows layout members
+// (reshape / bitcast / transpose / broadcast / degenerate reduce) and the
+// first full-size operand of elementwise members down to an external, and
+// returns that external's linear index for element `idx` of `node` (-1 if the
+// chain ends in a splat or a smaller tensor).
+int64_t source_index(const Graph& g, const Program& p, int node, std::vector<int64_t> idx) {
+  for (int guard = 0; guard < 256; ++guard) {
+    const Node& n = g.nodes[node];
+    auto linear = [](const std::vector<int64_t>& d, const std::vector<int64_t>& i) {
+      int64_t l = 0;
+      for (size_t k = 0; k < d.size(); ++k) l = l * d[k] + i[k];
+      return l;
+    };
+    auto delinear = [](const std::vector<int64_t>& d, int64_t l) {
+      std::vector<int64_t> i(d.size());
+      for (size_t k = d.size(); k-- > 0;) {
+        i[k] = l % d[k];
+        l /= d[k];
+      }
+      return i;
+    };
+    if (!p.is_member(node)) return n.is_splat() ? -1 : linear(n.dims, idx);
+    if (n.operands.empty()) return -1;
+    switch (n.op) {
+      case SFX_OP_ELEMENTWISE: {
+        int next = -1;
+        for (int o : n.operands)
+          if (g.nodes[o].numel() == n.numel() && !g.nodes[o].is_splat()) {
+            next = o;
+            break;
+          }
+        if (next < 0) return -1;
+        node = next;
+        break;
+      }
+      case SFX_OP_RESHAPE: case SFX_OP_BITCAST: case SFX_OP_REDUCE:  // (degenerate reduce: a reshape)
+        idx = delinear(g.nodes[n.operands[0]].dims, linear(n.dims, idx));
+        node = n.operands[0];
+        break;
+      case SFX_OP_TRANSPOSE: {  // out[i] = in[perm applied]: in index j = out index at perm^-1
+        std::vector<int64_t> in(idx.size());
+        for (size_t k = 0; k < n.perm.size(); ++k) in[n.perm[k]] = idx[k];
+        idx = in;
+        node = n.operands[0];
+        break;
+      }
+      case SFX_OP_BROADCAST: {
+        std::vector<int64_t> in;
+        for (int64_t d : n.dim_map) in.push_back(idx[d]);
+        idx = in;
+        node = n.operands[0];
+        break;
+      }
+      default:
+        return -1;
+    }
+  }
+  return -1;
+}
+
+// true: the operand's source is contiguous along the contraction axis k (stage
+// k-fastest); false: along m / n.  A is [.., M, K] (k last), B [.., K, N].
+bool k_contiguous(const Graph& g, const Program& p, int operand, bool is_a) {
+  const Node& o = g.nodes[operand];
+  const int r = o.rank();
+  if (r < 2) return is_a;
+  std::vector<int64_t> base(r, 0);
+  const int kd = is_a ? r - 1 : r - 2, md = is_a ? r - 2 : r - 1;
+  if (o.dims[kd] < 2 || o.dims[md] < 2) return is_a;
+  std::vector<int64_t> pk = base, pm = base;
+  pk[kd] = 1;
+  pm[md] = 1;
+  const int64_t s0 = source_index(g, p, operand, base), sk = source_index(g, p, operand, pk),
+                sm = source_index(g, p, operand, pm);
+  if (s0 < 0 || sk < 0 || sm < 0) return is_a;
+  const int64_t dk = std::llabs(sk - s0), dm = std::llabs(sm - s0);
+  return dk == 1 ? true : dm == 1 ? false : is_a;
+}
+
+KernelSource lower_dot_prologue(const Graph& g, const Program& p) {
+  std::string why;
+  if (!dot_prologue_ok(g, p, &why)) throw Error(SFX_ERR_UNSUPPORTED, "dot prologue: " + why);
+  const int node = p.roots[0];
+  const Node& n = g.nodes[node];
+  const Node& A = g.nodes[n.operands[0]];
+  const Node& Bn = g.nodes[n.operands[1]];
+  const int r = n.rank();
+  const int64_t M = n.dims[r - 2], N = n.dims[r - 1], K = A.dims[r - 1];
+  int64_t batch = 1;
+  for (int i = 0; i < r - 2; ++i) batch *= n.dims[i];
+  int BM, BN, TM, TN;
+  if (M >= 128 && N >= 128) BM = 128, BN = 128, TM = 8, TN = 8;
+  else if (M >= 64 && N >= 64) BM = 64, BN = 64, TM = 4, TN = 4;
+  else if (N <= 16) BM = 256, BN = 16, TM = 4, TN = 4;
+  else BM = 32, BN = 32, TM = 2, TN = 2;
+  const int64_t tiles_n = (N + BN - 1) / BN, tiles_m = (M + BM - 1) / BM;
+  const int64_t grid = tiles_n * tiles_m * batch;
+  if (grid >= (int64_t{1} << 31)) throw Error(SFX_ERR_UNSUPPORTED, "matmul " + n.id + " needs more than 2^31 CTAs");
+  lw::Ctx c = lw::make_ctx(g, p);
+  KernelSource ks;
+  ks.strategy = "dot";
+  ks.entry = "sfx_dotp_" + c.name.substr(0, 40);
+  ks.inputs = p.inputs;
+  ks.outputs = p.roots;
+  int64_t bytes = n.numel() * 4;
+  for (int e : p.inputs) bytes += g.nodes[e].numel() * 4;
+  ks.algorithmic_bytes = bytes;
+  ks.grid_x = grid;
+  ks.block = (BM / TM) * (BN / TN);
+  ks.smem = 0;
+  ks.vector_width = 1;
+  const bool f32 = n.dtype == SFX_F32;
+  std::string params;
+  Emitter em(g, p, 1, c.wide);
+  em.rcp_reduced_divisors = false;  // no reductions in the group: plain IEEE division
+  for (size_t k = 0; k < p.inputs.size(); ++k) {
+    em.input_ptr[p.inputs[k]] = "in" + std::to_string(k);
+    params += std::string("const ") + ctype(g.nodes[p.inputs[k]].dtype) + "* __restrict__ in" + std::to_string(k) + ", ";
+  }
+  params += std::string(ctype(n.dtype)) + "* __restrict__ out0, unsigned* __restrict__ ws";
+  Code pro;
+  em.code = &pro;
+  pro.indent = 1;
+  auto operand = [&](const char* fn, const Node& op, int opnode) {
+    pro.line(std::string("auto ") + fn + " = [&](long long L) -> " + ctype(n.dtype) + " {");
+    pro.indent++;
+    em.push();
+    const std::string L = c.wide ? "L" : "((int)L)";
+    std::string v = em.value(opnode, em.from_linear(em.uni(L), op.dims));
+    pro.line("return " + v + ";");
+    em.pop();
+    pro.indent--;
+    pro.line("};");
+  };
+  operand("sfx_opA", A, n.operands[0]);
+  operand("sfx_opB", Bn, n.operands[1]);
+  // stage each operand along the axis its main source is contiguous in
+  const bool a_kfast = k_contiguous(g, p, n.operands[0], true);
+  const bool b_kfast = k_contiguous(g, p, n.operands[1], false);
+  std::string body = subst(kDotKernel, {{"$TILES_N", fmt_i(tiles_n)},
+                                        {"$TILES_M", fmt_i(tiles_m)},
+                                        {"$BM", std::to_string(BM)},
+                                        {"$BN", std::to_string(BN)},
+                                        {"$TM", std::to_string(TM)},
+                                        {"$TN", std::to_string(TN)},
+                                        {"$T4", f32 ? "float4" : "int4"},
+                                        {"$T", f32 ? "float" : "int"},
+                                        {"$ENTRY", ks.entry},
+                                        {"$PARAMS", params},
+                                        {"$M", fmt_i(M)},
+                                        {"$N", fmt_i(N)},
+                                        {"$K", fmt_i(K)},
+                                        {"$PROLOGUE", pro.text},
+                                        {"$A_KFAST", a_kfast ? "1" : "0"},
+                                        {"$B_KFAST", b_kfast ? "1" : "0"},
+                                        {"$PACKED", f32 && TN % 2 == 0 && dot_packed() ? "1" : "0"},
+                                        {"$LOAD_A(", "sfx_opA("},
+                                        {"$LOAD_B(", "sfx_opB("}});
+  ks.code = std::string(kPrelude) + "\n" + body;
+  std::ostringstream note;
+  note << "fuse_dot group [" << batch << " x " << M << " x " << K << "] @ [" << K << " x " << N
+       << "] with " << (p.members.size() - 1) << " stitched operand member(s) computed where the tiles are staged: tile "
+       << BM << "x" << BN << "x16, " << TM << "x" << TN << " per thread, " << grid
+       << " CTAs; sequential-k fp32 (bit-exact)";
   ks.note = note.str();
   return ks;
 }

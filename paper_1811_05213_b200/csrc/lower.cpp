@@ -23,6 +23,7 @@ using namespace lw;
 std::string choose_strategy(const Graph& g, int pi, std::string* why) {
   const Program& p = g.programs.at(pi);
   if (dot_alone(g, p)) return "dot";
+  if (dot_prologue_ok(g, p, nullptr)) return "dotp";
   Ctx c = make_ctx(g, p);
   std::string w;
   if (analyze_map(c, &w)) return "map";
@@ -283,6 +284,7 @@ KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o
   if (strat == SFX_STRATEGY_AUTO) {
     std::string s = choose_strategy(g, pi, &why);
     if (s == "dot") return lower_dot(g, p);
+    if (s == "dotp") return lower_dot_prologue(g, p);
     strat = s == "map" ? SFX_STRATEGY_MAP : s == "row" ? SFX_STRATEGY_ROW : s == "col" ? SFX_STRATEGY_COL
             : s == "colbc" ? SFX_STRATEGY_COLBC : SFX_STRATEGY_LITERAL;
   }

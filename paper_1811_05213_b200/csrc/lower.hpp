@@ -81,6 +81,10 @@ std::string choose_strategy(const Graph& g, int program_index, std::string* why)
 
 // The matmul barrier kernel (dot.cpp).
 KernelSource lower_dot(const Graph& g, const Program& p);
+// fuse_dot group: a matmul (only root) whose operands are stitched elementwise / layout
+// members, computed where the operand tiles are staged
+bool dot_prologue_ok(const Graph& g, const Program& p, std::string* why);
+KernelSource lower_dot_prologue(const Graph& g, const Program& p);
 
 // A program whose only member is a matmul: an unfused barrier, or a fuse_dot
 // group with nothing stitched to the BatchMatMul.  Runs the dot kernel.

@@ -4,6 +4,8 @@ rejects, and every committed reference plan lowers to CUDA that NVRTC compiles
 to sm_100a SASS (no GPU needed for that)."""
 
 import os
+
+import numpy as np
 import re
 import subprocess
 
@@ -105,8 +107,11 @@ def test_random_graph_groups_lower_and_compile():
 
 
 def test_matmul_groups_lower():
-    """fuse_dot groups: a lone BatchMatMul uses the dot kernel, a BatchMatMul
-    stitched to other members the literal tier (dot_loop in reference k order)."""
+    """fuse_dot groups: a lone BatchMatMul uses the dot kernel; a BatchMatMul that
+    is the group's only root, stitched to elementwise / layout members producing
+    its operands, the dot kernel with those members computed where its tiles are
+    staged ("fuse_dot group"); anything else (reductions feeding it, other roots)
+    the literal tier (dot_loop in reference k order)."""
     d = T.load_json(os.path.join(T.GOLDEN, "random_acceptance.json"))
     seen = set()
     for case in d["cases"]:
@@ -118,10 +123,20 @@ def test_matmul_groups_lower():
             if not any(g.at(m).op == "batch_matmul" for m in k.program.members):
                 continue
             _, cubin, note = H.codegen(g, k.program)
-            kind = "dot" if len(k.program.members) == 1 else "literal"
-            assert note.split()[0] == kind, note
+            members = [g.at(m) for m in k.program.members]
+            dots = [m for m in members if m.op == "batch_matmul"]
+            prologue = (len(dots) == 1 and list(k.program.roots) == [dots[0].id] and
+                        all(m.op in ("batch_matmul", "reshape", "bitcast", "transpose", "broadcast") or
+                            m.op not in ("reduce", "library_call", "parameter", "constant") for m in members) and
+                        not any(m.op == "reduce" and int(np.prod(m.shape or [1])) != int(np.prod(g.at(m.operands[0]).shape or [1]))
+                                for m in members))
+            kind = "dot" if len(members) == 1 else "dotp" if prologue else "literal"
+            if kind == "dotp":
+                assert note.startswith("dot fuse_dot group"), note
+            else:
+                assert note.split()[0] == kind, note
             seen.add(kind)
-    assert seen == {"dot", "literal"}
+    assert seen == {"dot", "dotp", "literal"}, seen
 
 
 def _assert_no_contraction(sass):

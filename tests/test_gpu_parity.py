@@ -125,6 +125,47 @@ def test_encoder_layer_small(ctx, strategy):
     assert ours <= 2 * theirs, (ours, theirs)
 
 
+@pytest.mark.parametrize("strategy", ["auto", "literal"])
+def test_encoder_layer_fuse_dot_small(ctx, strategy):
+    """C5LF: the BERT layer planned with the reference's fuse_dot option — the
+    attention matmuls stitched with the bias add / head split / transpose (Q K^T)
+    and the softmax normalisation x dropout mask (P V) that produce their
+    operands.  Those two groups run as the dot kernel with the stitched members
+    computed where the tiles are staged (auto) or on the literal tier; same
+    criteria as C5L."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C5LF.small.json"))
+    inputs = T.gen_inputs(g, 42, -1.0, 1.0)
+    outs, launched, strategies = _run(ctx, g, rep, inputs, strategy)
+    assert launched == len(rep.kernels) + len(T.unfused_kernels(g, rep))
+    if strategy == "auto":  # the two fuse_dot groups (the unfused matmuls are barrier kernels)
+        assert strategies.count("dot") == 2, strategies
+    ref32 = T.interpret(g, inputs, 0)["h2"].astype(np.float64)
+    ref64 = T.interpret(g, inputs, 1)["h2"].astype(np.float64)
+    got = outs["h2"].astype(np.float64)
+    assert T.values_close(outs["h2"], ref32.astype(np.float32)), T.mismatch_report(got, ref32)
+    ours, theirs = np.abs(got - ref64).max(), np.abs(ref32 - ref64).max()
+    assert ours <= 2 * theirs, (ours, theirs)
+
+
+def test_fuse_dot_groups_bit_exact_small(ctx):
+    """The two fuse_dot groups of C5LF alone: the prologue-fused dot kernel
+    against the literal tier (the reference's dot_loop order) — bit for bit."""
+    g, rep, b = H.load_bundle(os.path.join(T.PLANS, "C5LF.small.json"))
+    inputs = T.gen_inputs(g, 7, -1.0, 1.0)
+    ref = T.interpret(g, inputs, 0)
+    full = dict(inputs)
+    full.update({k: v for k, v in ref.items() if k not in full})
+    n = 0
+    for kp in rep.kernels:
+        if not any(g.at(m).op == "batch_matmul" for m in kp.program.members):
+            continue
+        (a,) = H.run_program(kp.program, g, full, ctx=ctx)
+        (l,) = H.run_program(kp.program, g, full, ctx=ctx, strategy="literal")
+        assert np.array_equal(a.view(np.uint32), l.view(np.uint32)), kp.program.fusion_root
+        n += 1
+    assert n == 2
+
+
 @pytest.mark.parametrize("root", ["k_t", "q_t", "v_t"])
 def test_encoder_layer_head_split_full_size(ctx, root):
     """C5L's head split at b64 s512: bias add on [T, Hd], reshape to

@@ -24,20 +24,39 @@ from workloads import configs  # noqa: E402
 REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
 
 
-def plan_bundle(doc: dict) -> dict:
+def plan_bundle(doc: dict, flags=()) -> dict:
     with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
         f.write(configs.dumps(doc))
         path = f.name
     try:
-        out = subprocess.run([REF_TOOL, "plan", path], check=True, capture_output=True, text=True)
+        out = subprocess.run([REF_TOOL, "plan", path, *flags], check=True, capture_output=True, text=True)
     finally:
         os.unlink(path)
     return json.loads(out.stdout)
 
 
+def fuse_dot_plans(outdir):
+    """C5LF: the whole BERT layer (C5L's graph) planned with the reference's
+    fuse_dot option (PipelineOptions::fuse_dot, `stitchfuse --fuse-dot`): the
+    attention matmuls are stitched with the bias add / head split / transpose
+    and the softmax normalisation x dropout mask that produce their operands."""
+    for size_name, table in (("full", configs.FULL), ("small", configs.SMALL)):
+        sizes = table["C5L"]
+        bundle = plan_bundle(configs.build("C5L", **sizes), ["--fuse-dot"])
+        for k in bundle["kernels"]:
+            k.pop("dump", None)
+        bundle["workload"] = {"name": "C5LF", "size": size_name, "sizes": sizes, "options": "--fuse-dot"}
+        path = os.path.join(outdir, f"C5LF.{size_name}.json")
+        with open(path, "w") as f:
+            json.dump(bundle, f, separators=(",", ":"))
+            f.write("\n")
+        print(f"{path}: fused={bundle['fused_kernels']} groups={[k['fusion_root'] for k in bundle['kernels']]}")
+
+
 def main():
     outdir = os.path.join(HERE, "plans")
     os.makedirs(outdir, exist_ok=True)
+    fuse_dot_plans(outdir)
     for size_name, table in (("full", configs.FULL), ("small", configs.SMALL)):
         for name, sizes in table.items():
             bundle = plan_bundle(configs.build(name, **sizes))
