@@ -54,6 +54,9 @@ EXPECTED = {  # strategy the GroupAnalyzer must pick at full size
     ("C5L", "h2"): "row", ("C5L", "gelu"): "map", ("C5L", "h1"): "row", ("C5L", "ctx_r"): "map",
     ("C5L", "probs_d"): "map", ("C5L", "v_t"): "map", ("C5L", "sm.e"): "row", ("C5L", "k_t"): "map",
     ("C5L", "q_t"): "map",
+    # C5L planned with fuse_dot: the attention matmuls stitched with their operand producers
+    ("C5LF", "h2"): "row", ("C5LF", "gelu"): "map", ("C5LF", "h1"): "row", ("C5LF", "ctx_r"): "map",
+    ("C5LF", "ctx"): "dot", ("C5LF", "sm.e"): "row", ("C5LF", "scores"): "dot",
 }
 
 
