@@ -12,13 +12,15 @@ from paper_1811_05213_b200 import host as H  # noqa: E402
 import test_gpu_parity as P  # noqa: E402
 
 ctx = H.Context(0)
-names = (sys.argv[1].split(",") if sys.argv[1] != "none" else []) if len(sys.argv) > 1 else ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t", "C5"]
+names = (sys.argv[1].split(",") if sys.argv[1] != "none" else []) if len(sys.argv) > 1 else ["C1", "C2", "C3", "C3b", "C4", "C4b", "C4t", "C5", "C5L", "C5LF"]
 for name in names:
     g, rep, _ = H.load_bundle(os.path.join(T.PLANS, f"{name}.small.json"))
     inputs = T.gen_inputs(g, 42, -1.0, 1.0)
     for strategy in ("auto", "literal"):
         outs, _, strat = P._run(ctx, g, rep, inputs, strategy)
-        assert not P._check(g, outs, inputs, strict=True, literal=strategy == "literal"), (name, strategy)
+        # (C5L / C5LF chain a whole layer: the reference's own criterion, as
+        # test_encoder_layer_small, not the stricter named-config bounds)
+        assert not P._check(g, outs, inputs, strict=not name.startswith("C5L"), literal=strategy == "literal"), (name, strategy)
         print(name, strategy, strat, flush=True)
 for name in ("softmax_r4_c131072", "softmax_r2_c262144", "ln_r6_c98304", "ln_r5_c70001", "softmax_r16_c16384",  # long rows
              "softmaxmask_r4_c131072", "bnbwd_4096x256",  # cached member with two slices; two-input cp.async ring
