@@ -101,10 +101,11 @@ const char* kDotKernel = R"SFXDOT(
 #define A_KFAST $A_KFAST
 #define B_KFAST $B_KFAST
 #define PACKED $PACKED
+#define VEC $VEC
 typedef $T T;
 typedef $T4 T4;
 
-extern "C" __global__ void __launch_bounds__(NT) $ENTRY($PARAMS) {
+extern "C" __global__ void __launch_bounds__(NT, NT >= 256 ? 2 : 1) $ENTRY($PARAMS) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const long long M = $M, N = $N, K = $K;
@@ -119,6 +120,53 @@ $PROLOGUE
   const long long mb = t % $TILES_M;
   const long long b = t / $TILES_M;
   const long long m0 = mb * BM, n0 = nb * BN;
+#if VEC
+  // stitched operands evaluated 4 elements at a time along their contiguous
+  // axis (sfx_opA4 / sfx_opB4: 128-bit loads where the sources allow)
+  float4 ra[LA / 4], rb[LB / 4];
+  auto fetch = [&](long long k0) {
+#pragma unroll
+    for (int i = 0; i < LA / 4; ++i) {
+      const int e = tid + i * NT;
+      const int row = A_KFAST ? e / (BK / 4) : (e % (BM / 4)) * 4;
+      const int kk = A_KFAST ? (e % (BK / 4)) * 4 : e / (BM / 4);
+      const long long m = m0 + row, k = k0 + kk;
+      ra[i] = (m < M && k < K) ? sfx_opA4(b, m, k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < LB / 4; ++i) {
+      const int e = tid + i * NT;
+      const int kk = B_KFAST ? (e % (BK / 4)) * 4 : e / (BN / 4);
+      const int col = B_KFAST ? e / (BK / 4) : (e % (BN / 4)) * 4;
+      const long long k = k0 + kk, n = n0 + col;
+      rb[i] = (k < K && n < N) ? sfx_opB4(b, k, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < LA / 4; ++i) {
+      const int e = tid + i * NT;
+      if (A_KFAST) {
+        const int row = e / (BK / 4), kk = (e % (BK / 4)) * 4;
+        As[buf][kk][row] = ra[i].x; As[buf][kk + 1][row] = ra[i].y;
+        As[buf][kk + 2][row] = ra[i].z; As[buf][kk + 3][row] = ra[i].w;
+      } else {
+        *reinterpret_cast<float4*>(&As[buf][e / (BM / 4)][(e % (BM / 4)) * 4]) = ra[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < LB / 4; ++i) {
+      const int e = tid + i * NT;
+      if (B_KFAST) {
+        const int col = e / (BK / 4), kk = (e % (BK / 4)) * 4;
+        Bs[buf][kk][col] = rb[i].x; Bs[buf][kk + 1][col] = rb[i].y;
+        Bs[buf][kk + 2][col] = rb[i].z; Bs[buf][kk + 3][col] = rb[i].w;
+      } else {
+        *reinterpret_cast<float4*>(&Bs[buf][e / (BN / 4)][(e % (BN / 4)) * 4]) = rb[i];
+      }
+    }
+  };
+#else
   T ra[LA], rb[LB];
   // staging order: consecutive threads take consecutive k (A_KFAST / B_KFAST)
   // or consecutive m / n, whichever is contiguous in the operand's source memory
@@ -152,6 +200,7 @@ $PROLOGUE
       Bs[buf][B_KK(e)][B_COL(e)] = rb[i];
     }
   };
+#endif
 #if PACKED
   // f32 on the packed fp32x2 datapath (see kDotKernel2): t = fma(a, b, Z),
   // acc = acc + t, Z a zero ptxas cannot see
@@ -475,7 +524,8 @@ KernelSource lower_dot(const Graph& g, const Program& p) {
                                         {"$PROLOGUE", ""},
                                         {"$A_KFAST", "1"},
                                         {"$B_KFAST", "0"},
-                                        {"$PACKED", f32 && TN % 2 == 0 && dot_packed() ? "1" : "0"}});
+                                        {"$PACKED", f32 && TN % 2 == 0 && dot_packed() ? "1" : "0"},
+                                        {"$VEC", "0"}});
   // $LOAD_A(expr) -> __ldg(inK + (expr)), or the literal of a splat constant
   auto expand = [&](const std::string& key, int operand) {
     const Node& o = g.nodes[operand];
@@ -685,6 +735,41 @@ KernelSource lower_dot_prologue(const Graph& g, const Program& p) {
   // stage each operand along the axis its main source is contiguous in
   const bool a_kfast = k_contiguous(g, p, n.operands[0], true);
   const bool b_kfast = k_contiguous(g, p, n.operands[1], false);
+  // 4-wide evaluation along the staging axis when its extents allow
+  const int NTT = (BM / TM) * (BN / TN);
+  const int LAe = BM * 16 / NTT, LBe = 16 * BN / NTT;
+  const bool vec = f32 && LAe % 4 == 0 && LBe % 4 == 0 && (a_kfast ? K % 4 == 0 : M % 4 == 0) &&
+                   (b_kfast ? K % 4 == 0 : N % 4 == 0) && (a_kfast ? 16 % 4 == 0 : BM % 4 == 0) && dot_packed();
+  if (vec) {
+    Emitter em4(g, p, 4, c.wide);
+    em4.rcp_reduced_divisors = false;
+    em4.input_ptr = em.input_ptr;
+    em4.code = &pro;
+    auto operand4 = [&](const char* fn, const Node& op, int opnode, bool vec_on_last) {
+      // (pb, pi, pj): batch index, then the operand's last two coordinates;
+      // the 4 lanes step the last coordinate (vec_on_last) or the one before
+      pro.line(std::string("auto ") + fn + " = [&](long long pb, long long pi, long long pj) -> float4 {");
+      pro.indent++;
+      em4.push();
+      const std::string cb = c.wide ? "pb" : "((int)pb)", ci = c.wide ? "pi" : "((int)pi)", cj = c.wide ? "pj" : "((int)pj)";
+      std::vector<int64_t> bdims(op.dims.begin(), op.dims.end() - 2);
+      std::vector<Ix> base = bdims.empty() ? std::vector<Ix>{} : em4.from_linear(em4.uni(cb), bdims);
+      std::string v[4];
+      for (int lane = 0; lane < 4; ++lane) {
+        em4.lane = lane;
+        std::vector<Ix> comps = base;
+        comps.push_back(vec_on_last ? em4.uni(ci) : em4.lane_plus(ci));
+        comps.push_back(vec_on_last ? em4.lane_plus(cj) : em4.uni(cj));
+        v[lane] = em4.value(opnode, comps);
+      }
+      pro.line("return make_float4(" + v[0] + ", " + v[1] + ", " + v[2] + ", " + v[3] + ");");
+      em4.pop();
+      pro.indent--;
+      pro.line("};");
+    };
+    operand4("sfx_opA4", A, n.operands[0], a_kfast);   // A [.., M, K]: k is last
+    operand4("sfx_opB4", Bn, n.operands[1], !b_kfast);  // B [.., K, N]: n is last
+  }
   std::string body = subst(kDotKernel, {{"$TILES_N", fmt_i(tiles_n)},
                                         {"$TILES_M", fmt_i(tiles_m)},
                                         {"$BM", std::to_string(BM)},
@@ -702,6 +787,7 @@ KernelSource lower_dot_prologue(const Graph& g, const Program& p) {
                                         {"$A_KFAST", a_kfast ? "1" : "0"},
                                         {"$B_KFAST", b_kfast ? "1" : "0"},
                                         {"$PACKED", f32 && TN % 2 == 0 && dot_packed() ? "1" : "0"},
+                                        {"$VEC", vec ? "1" : "0"},
                                         {"$LOAD_A(", "sfx_opA("},
                                         {"$LOAD_B(", "sfx_opB("}});
   ks.code = std::string(kPrelude) + "\n" + body;
