@@ -416,11 +416,14 @@ def run_ours(args):
     # hard part 5): small graphs otherwise expose launch/ramp/tail latency.
     # Concurrent instances always use distinct buffer sets; kernels that own a
     # workspace (cross-CTA column combine) run one instance at a time.
+    # Two instances for graphs above 512 MB (C5 and its shards: the next
+    # instance's first kernels run under the previous one's last ramp-down;
+    # measured C5 b8 shard 0.097 -> 0.091 ms per graph), four below.
     has_ws = any(k["workspace_bytes"] > 0 for k in kinfo)
-    inflight = args.inflight if args.inflight > 0 else (1 if per_set > (512 << 20) or has_ws else 4)
+    inflight = args.inflight if args.inflight > 0 else (4 if per_set <= (512 << 20) else 2 if per_set <= (16 << 30) else 1)
     if has_ws:
         inflight = 1
-    inflight = max(1, min(inflight, nsets if nsets > 1 else 1))
+    inflight = max(1, inflight)
     while len(sets) < inflight:  # never share a buffer set between concurrent instances
         ins = [torch.rand(g.at(p).shape, generator=gen, device=dev, dtype=torch.float32) * 2 - 1
                for p in cg.param_ids]
