@@ -418,10 +418,14 @@ def run_ours(args):
     # workspace (cross-CTA column combine) run one instance at a time.
     # Two instances for graphs above 512 MB (C5 and its shards: the next
     # instance's first kernels run under the previous one's last ramp-down;
-    # measured C5 b8 shard 0.097 -> 0.091 ms per graph), four below.
-    has_ws = any(k["workspace_bytes"] > 0 for k in kinfo)
+    # measured C5 b8 shard 0.097 -> 0.091 ms per graph), four below.  Kernels
+    # with a cross-CTA workspace (column combine) get one workspace per stream
+    # and per captured graph, so they run concurrently too; kernels that
+    # exchange with peer ranks run one instance at a time (every rank must
+    # issue them in the same order).
+    has_peer = peer
     inflight = args.inflight if args.inflight > 0 else (4 if per_set <= (512 << 20) else 2 if per_set <= (16 << 30) else 1)
-    if has_ws:
+    if has_peer:
         inflight = 1
     inflight = max(1, inflight)
     while len(sets) < inflight:  # never share a buffer set between concurrent instances

@@ -2,7 +2,7 @@
 named config and n in {1, 2, 4, 8}, time one rank's batch shard (the reference's
 own plan of the b/n shard graph, workloads/plans/<C>.shard<n>.json) alone, the
 way bench.py times a rank (CUDA-graph replay, rotating input sets > 3x L2,
-independent instances in flight for graphs < 512 MB without workspaces), and
+independent instances in flight: 4 below 512 MB, 2 above), and
 project the n-GPU job as n x (shard bytes / shard time).  The projection assumes
 ranks do not interfere (true on this path: no collective except C3's 4 KiB
 column combine, which it leaves out) — an upper bound on bench.py --gpus n, and
@@ -29,8 +29,8 @@ def time_plan(ctx, path, steps=200, warmup=5):
     per_set = sum(g.at(p).numel() * 4 for p in cg.param_ids) + sum(g.at(o).numel() * 4 for o in g.outputs)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     has_ws = any(k.info["workspace_bytes"] > 0 for k in cg.kernels)
-    inflight = 1 if has_ws else 4 if per_set <= (512 << 20) else 2 if per_set <= (16 << 30) else 1  # as bench.py
-    if os.environ.get("PROJ_INFLIGHT") and not has_ws:  # A/B: instances in flight
+    inflight = 4 if per_set <= (512 << 20) else 2 if per_set <= (16 << 30) else 1  # as bench.py (one rank: no peers)
+    if os.environ.get("PROJ_INFLIGHT"):  # A/B: instances in flight
         inflight = int(os.environ["PROJ_INFLIGHT"])
     nsets = max(inflight, min(64, math.ceil(3 * l2 / per_set)))
     sets = []
