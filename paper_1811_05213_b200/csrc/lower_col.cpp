@@ -397,6 +397,59 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   return ks;
 }
 
+// A second-level sum of squared deviations from the broadcast first-level
+// total, b = Σ (u - m)², m = A or scale(A), A = Σ u over the same dims
+// (batch-norm's var.sum over d2 = d * d, d = x - mean_b).  Such a b needs no
+// pass of its own: shifted sums S1 = Σ (u - K), S2 = Σ (u - K)² with
+// K = u at reduced index 0 of the column (the same K in every stripe) fold in
+// A's pass, and A = N·K + S1, b = S2 - 2δ·S1 + N·δ², δ = m - K with m the fp32
+// mean the graph computes from A (all in fp64: b is the sum of (u - m)² around
+// that fp32 mean, the rounding of each d and d² left out — a reduction-order
+// class difference within the fp64-checked tolerance).
+struct Var2 {
+  int a = -1, b = -1, u = -1, mb = -1;
+};
+static std::vector<Var2> find_var2(const Ctx& c, const ColBcPlan& bp) {
+  const Graph& g = c.g;
+  std::vector<Var2> out;
+  if (bp.max_level != 2 || c.peer) return out;
+  const char* env = std::getenv("SFX_COLBC_TWO_PASS");
+  if (env && env[0] == '1') return out;
+  auto is_ew = [&](int n, int kind) { return g.nodes[n].op == SFX_OP_ELEMENTWISE && g.nodes[n].kind == kind; };
+  auto sum_f32 = [&](int n) {
+    const Node& x = g.nodes[n];
+    return x.op == SFX_OP_REDUCE && x.reducer == SFX_REDUCE_SUM && x.dtype == SFX_F32;
+  };
+  for (int b : c.reduces) {
+    if (bp.level.at(b) != 2) continue;
+    if (!sum_f32(b)) return {};
+    const int sq = g.nodes[b].operands[0];
+    if (!c.p.is_member(sq) || !is_ew(sq, SFX_EW_MUL) || g.nodes[sq].operands[0] != g.nodes[sq].operands[1]) return {};
+    const int d = g.nodes[sq].operands[0];
+    if (!c.p.is_member(d) || !is_ew(d, SFX_EW_SUB)) return {};
+    bool found = false;
+    for (int side = 0; side < 2 && !found; ++side) {
+      const int u = g.nodes[d].operands[side], mb = g.nodes[d].operands[1 - side];
+      if (!c.p.is_member(mb) || g.nodes[mb].op != SFX_OP_BROADCAST) continue;
+      int m = g.nodes[mb].operands[0];
+      int a = m;
+      if (c.p.is_member(m) && is_ew(m, SFX_EW_SCALE)) a = g.nodes[m].operands[0];
+      if (!c.p.is_member(a) || !sum_f32(a) || bp.level.count(a) == 0 || bp.level.at(a) != 1) continue;
+      const Node& an = g.nodes[a];
+      if (an.operands[0] != u || an.reduce_dims != g.nodes[b].reduce_dims) continue;
+      if (g.nodes[mb].dims != g.nodes[u].dims || g.nodes[u].dtype != SFX_F32) continue;
+      std::vector<int64_t> kept;
+      for (int64_t k = 0; k < g.nodes[u].rank(); ++k)
+        if (std::find(an.reduce_dims.begin(), an.reduce_dims.end(), k) == an.reduce_dims.end()) kept.push_back(k);
+      if (g.nodes[mb].dim_map != kept) continue;
+      out.push_back({a, b, u, mb});
+      found = true;
+    }
+    if (!found) return {};
+  }
+  return out;
+}
+
 // Column reductions broadcast back (batch-norm): one launch, a co-resident
 // grid of column tiles x row stripes (2 CTAs/SM, one wave, cooperative
 // launch).  Per reduction level: every CTA folds its stripe (per-lane fp64
@@ -649,10 +702,35 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     body.indent--;
     body.line("}");
   };
-  for (int lv = 1; lv <= bp.max_level; ++lv) {
+  // one-pass second moments (find_var2): b folds in a's pass, one level less
+  const std::vector<Var2> var2 = find_var2(c, bp);
+  std::map<int, int> lvl = bp.level;
+  int max_level = bp.max_level;
+  std::map<int, const Var2*> var2_a, var2_b;
+  for (const Var2& q : var2) {
+    lvl[q.b] = lvl.at(q.a);
+    var2_a[q.a] = &q;
+    var2_b[q.b] = &q;
+  }
+  if (!var2.empty()) max_level = 1;
+  // K per (pair, lane): u at reduced index 0 of the thread's columns (co/ci are
+  // clamped to column 0 for threads past the last column)
+  std::map<int, std::vector<std::string>> shiftK;
+  for (const Var2& q : var2) {
+    const Node& un = c.g.nodes[q.u];
+    em.push();
+    for (int l = 0; l < V; ++l) {
+      const std::string v = em.value(q.u, orc_comps(em, un.dims, O, R, I, em.uni("co"), em.uni("0"), inner_ix(l)));
+      const std::string k = em.fresh("shk");
+      body.line("const double " + k + " = (double)" + v + ";");
+      shiftK[q.a].push_back(k);
+    }
+    em.pop();
+  }
+  for (int lv = 1; lv <= max_level; ++lv) {
     std::vector<int> red;
     for (int r : c.reduces)
-      if (bp.level.at(r) == lv) red.push_back(r);
+      if (lvl.at(r) == lv) red.push_back(r);
     std::vector<std::vector<std::string>> acc(red.size(), std::vector<std::string>(V));
     for (size_t k = 0; k < red.size(); ++k) {
       const Node& rn = c.g.nodes[red[k]];
@@ -669,9 +747,19 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
       for (int l = 0; l < V; ++l) {
         Ix iix = inner_ix(l);
         for (size_t k = 0; k < red.size(); ++k) {
+          if (var2_b.count(red[k])) continue;  // folded with its first-level sum
           const Node& rn = c.g.nodes[red[k]];
           const Node& in = c.g.nodes[rn.operands[0]];
           std::string v = em.value(rn.operands[0], orc_comps(em, in.dims, O, R, I, oix, rix, iix));
+          auto qa = var2_a.find(red[k]);
+          if (qa != var2_a.end()) {  // shifted sums S1 (a's accumulator), S2 (b's)
+            const size_t kb = std::find(red.begin(), red.end(), qa->second->b) - red.begin();
+            const std::string t = em.fresh("sh");
+            body.line("const double " + t + " = (double)" + v + " - " + shiftK[red[k]][l] + ";");
+            body.line(acc[k][l] + " += " + t + ";");
+            body.line(acc[kb][l] + " = fma(" + t + ", " + t + ", " + acc[kb][l] + ");");
+            continue;
+          }
           body.line(acc[k][l] + " = " + fold_fn(red[k]) + "(" + acc[k][l] + ", " + v + ");");
         }
       }
@@ -771,25 +859,53 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
       body.indent--;
       body.line("}");
     }
-    for (size_t k = 0; k < red.size(); ++k) {
-      const Node& rn = c.g.nodes[red[k]];
-      const std::string T = acc_t(red[k]);
+    std::vector<int> order;  // second moments after the first-level sums they use
+    for (int r : red)
+      if (!var2_b.count(r)) order.push_back(r);
+    for (int r : red)
+      if (var2_b.count(r)) order.push_back(r);
+    std::map<int, std::vector<std::string>> raw;  // fp64 totals as folded (S1 for var2 first levels)
+    for (int rk : order) {
+      const Node& rn = c.g.nodes[rk];
+      const std::string T = acc_t(rk);
       std::vector<std::string> tv(V);
       for (int l = 0; l < V; ++l) {
         tv[l] = em.fresh("tot");
         body.line(T + " " + tv[l] + " = __ldcg((const " + T + "*)((const unsigned long long*)(ws + " +
-                  fmt_i(tot_word[red[k]]) + ") + (cok ? c0 : 0) + " + std::to_string(l) + "));");
+                  fmt_i(tot_word[rk]) + ") + (cok ? c0 : 0) + " + std::to_string(l) + "));");
+      }
+      raw[rk] = tv;
+      if (var2_a.count(rk))  // A = N·K + S1
+        for (int l = 0; l < V; ++l) {
+          const std::string f = em.fresh("tot");
+          body.line("const double " + f + " = " + fmt_i(R) + ".0 * " + shiftK[rk][l] + " + " + tv[l] + ";");
+          tv[l] = f;
+        }
+      auto qb = var2_b.find(rk);
+      if (qb != var2_b.end()) {  // b = S2 - 2δ·S1 + N·δ², δ = m - K (m: the graph's fp32 mean)
+        const Var2& q = *qb->second;
+        const Node& mbn = c.g.nodes[q.mb];
+        em.push();
+        for (int l = 0; l < V; ++l) {
+          const std::string m = em.value(q.mb, orc_comps(em, mbn.dims, O, R, I, em.uni("co"), em.uni("0"), inner_ix(l)));
+          const std::string dl = em.fresh("dl"), f = em.fresh("tot");
+          body.line("const double " + dl + " = (double)" + m + " - " + shiftK[q.a][l] + ";");
+          body.line("const double " + f + " = " + tv[l] + " - 2.0 * " + dl + " * " + raw[q.a][l] + " + " + fmt_i(R) +
+                    ".0 * " + dl + " * " + dl + ";");
+          tv[l] = f;
+        }
+        em.pop();
       }
       if (c.peer) {  // the ranks' totals, in rank order (identical on every rank)
         body.line("if (pn > 1) {");
         body.line("  const long long par = (launch_seq * " + std::to_string(bp.max_level) + "u + " + std::to_string(lv) +
                   "u) & 1u;");
         body.line("  const unsigned long long* xs = (const unsigned long long*)(peers[prank] + poff) + (par * " +
-                  std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(red_index[red[k]]) + ") * " +
+                  std::to_string(PMAX) + " * " + std::to_string(NR) + " + " + std::to_string(red_index[rk]) + ") * " +
                   fmt_i(C) + " + (cok ? c0 : 0);");
         for (int l = 0; l < V; ++l) {
           body.line("  " + tv[l] + " = __ldcv((const " + T + "*)(xs + " + std::to_string(l) + "));");
-          body.line("  for (int q = 1; q < pn; ++q) " + tv[l] + " = " + fold_fn(red[k]) + "(" + tv[l] + ", __ldcv((const " +
+          body.line("  for (int q = 1; q < pn; ++q) " + tv[l] + " = " + fold_fn(rk) + "(" + tv[l] + ", __ldcv((const " +
                     T + "*)(xs + (long long)q * " + std::to_string(NR) + " * " + fmt_i(C) + " + " + std::to_string(l) +
                     ")));");
         }
@@ -811,7 +927,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
           em.pop();
         }
       }
-      total[red[k]] = tv;
+      total[rk] = tv;
     }
   }
   // final pass: element roots; column roots from stripe 0
@@ -874,7 +990,8 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   ks.vector_width = V;
   ks.note = "outer=" + std::to_string(O) + " reduced=" + std::to_string(R) + " inner=" + std::to_string(I) +
             " tiles=" + std::to_string(tiles) + " stripes=" + std::to_string(S) + " levels=" +
-            std::to_string(bp.max_level) + " (grid barriers, cooperative launch)" +
+            std::to_string(max_level) + " (grid barriers, cooperative launch)" +
+            (var2.empty() ? "" : ", " + std::to_string(var2.size()) + " second moment(s) in the first pass") +
             (NS > 0 ? ", cp.async ring " + std::to_string(NS) + " x " + std::to_string(UR) + " rows" : "");
   return ks;
 }

@@ -500,6 +500,25 @@ def test_colbc_cuda_graph_replay(ctx, name):
     assert not _check(g, got, inputs, strict=True)
 
 
+@pytest.mark.parametrize("name", ["bn_4096x256", "bn_mid_8x512x64", "bn_nhwc_16x16x8x128"])
+@pytest.mark.parametrize("two_pass", ["0", "1"])
+def test_colbc_second_moment_forms(ctx, name, two_pass, monkeypatch):
+    """Batch-norm variance as shifted sums folded in the mean's pass (default)
+    and as its own level (SFX_COLBC_TWO_PASS=1), on inputs with a common offset
+    (x = 10 + U(-1, 1): the shifted sums' cancellation case) and on a constant
+    column (variance exactly 0): both forms within the strict tolerance of the
+    fp64 oracle."""
+    monkeypatch.setenv("SFX_COLBC_TWO_PASS", two_pass)
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 23, -1.0, 1.0)
+    x = inputs["x"] + np.float32(10.0)
+    x.reshape(-1, x.shape[-1])[:, 3] = np.float32(0.375)  # one constant column
+    inputs["x"] = x.astype(np.float32)
+    outs, launched, strategies = _run(ctx, g, rep, inputs, "auto")
+    assert "colbc" in strategies and launched == len(rep.kernels)
+    assert not _check(g, outs, inputs, strict=True)
+
+
 @pytest.mark.parametrize("cuda_graph", [False, True])
 def test_concurrent_launches_on_four_streams(ctx, cuda_graph):
     """One compiled C3 graph (the column kernel owns a cross-CTA workspace:

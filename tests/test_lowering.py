@@ -84,10 +84,21 @@ def test_colbc_stages_stripes_through_a_cp_async_ring():
     assert "cp.async ring 3 x 4 rows" in note
 
 
-def test_colbc_is_cooperative_with_grid_barriers():
+def test_colbc_is_cooperative_with_grid_barriers(monkeypatch):
+    """Batch-norm's variance (a sum of squared deviations from the broadcast
+    mean) folds as shifted sums in the mean's pass: one reduction level, two
+    grid barriers, two passes; SFX_COLBC_TWO_PASS=1 keeps the two-level form."""
     src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
-    assert "sfx_grid_barrier(ws, 4u)" in src and "sfx_grid_exit(ws)" in src
-    assert "cooperative launch" in note
+    assert "sfx_grid_barrier(ws, 2u)" in src and "sfx_grid_barrier(ws, 3u)" not in src
+    assert "sfx_grid_exit(ws)" in src and "cooperative launch" in note
+    assert "levels=1" in note and "1 second moment(s) in the first pass" in note
+    assert "fma(sh" in src and "4096.0 * shk" in src
+    for n, k in (("bn_mid_8x512x64", 0), ("bn_nhwc_16x16x8x128", 1)):
+        _, _, note = _note(os.path.join(EXTRA, n + ".json"), k)
+        assert "1 second moment(s)" in note, note
+    monkeypatch.setenv("SFX_COLBC_TWO_PASS", "1")
+    src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
+    assert "sfx_grid_barrier(ws, 4u)" in src and "levels=2" in note and "second moment" not in note
 
 
 def test_long_rows_prefer_row_templates_over_colbc():
