@@ -722,7 +722,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     for (int l = 0; l < V; ++l) {
       const std::string v = em.value(q.u, orc_comps(em, un.dims, O, R, I, em.uni("co"), em.uni("0"), inner_ix(l)));
       const std::string k = em.fresh("shk");
-      body.line("const double " + k + " = (double)" + v + ";");
+      body.line("const double " + k + " = ((__float_as_uint(" + v + ") & 0x7f800000u) != 0x7f800000u) ? (double)" + v + " : 0.0;");
       shiftK[q.a].push_back(k);
     }
     em.pop();
@@ -890,8 +890,13 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
           const std::string m = em.value(q.mb, orc_comps(em, mbn.dims, O, R, I, em.uni("co"), em.uni("0"), inner_ix(l)));
           const std::string dl = em.fresh("dl"), f = em.fresh("tot");
           body.line("const double " + dl + " = (double)" + m + " - " + shiftK[q.a][l] + ";");
-          body.line("const double " + f + " = " + tv[l] + " - 2.0 * " + dl + " * " + raw[q.a][l] + " + " + fmt_i(R) +
-                    ".0 * " + dl + " * " + dl + ";");
+          // non-finite mean (an inf / NaN in the column, or an fp32 overflow of its
+          // sum): Σ (u - m)² as the two-level form gets it — NaN for a NaN mean or when
+          // some u equals the infinite mean (S1 not finite), else +inf
+          body.line("const double " + f + " = ((__float_as_uint(" + m + ") & 0x7f800000u) != 0x7f800000u) ? " + tv[l] + " - 2.0 * " + dl + " * " +
+                    raw[q.a][l] + " + " + fmt_i(R) + ".0 * " + dl + " * " + dl + " : (" + m + " != " + m +
+                    " || !(fabs(" + raw[q.a][l] + ") <= 1.7976931348623157e308)) ? (double)(" + m + " - " + m + ") : (double)(" + m +
+                    " * " + m + ");");
           tv[l] = f;
         }
         em.pop();

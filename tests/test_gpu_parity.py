@@ -519,6 +519,32 @@ def test_colbc_second_moment_forms(ctx, name, two_pass, monkeypatch):
     assert not _check(g, outs, inputs, strict=True)
 
 
+@pytest.mark.parametrize("name", ["bn_4096x256", "bn_nhwc_16x16x8x128"])
+@pytest.mark.parametrize("two_pass", ["0", "1"])
+def test_colbc_second_moment_special_values(ctx, name, two_pass, monkeypatch):
+    """Non-finite columns through both variance forms: a +inf, a NaN, an fp32
+    overflow of the column sum (mean = inf), -inf at reduced index 0 (the
+    shifted sums' K), +inf and -inf together (sum NaN) — the reference's
+    inf/NaN propagation (values_close: NaN == NaN, inf == inf)."""
+    monkeypatch.setenv("SFX_COLBC_TWO_PASS", two_pass)
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 29, -1.0, 1.0)
+    x = inputs["x"].copy()
+    v = x.reshape(-1, x.shape[-1])
+    n = v.shape[0]
+    v[n // 3, 5] = np.inf
+    v[n // 2, 6] = np.nan
+    v[:, 7] = np.float32(1e36)
+    v[0, 8] = -np.inf
+    v[1, 9], v[n - 1, 9] = np.inf, -np.inf
+    inputs["x"] = x
+    outs, launched, strategies = _run(ctx, g, rep, inputs, "auto")
+    assert "colbc" in strategies
+    assert not _check(g, outs, inputs)
+    y = outs["y"].reshape(-1, x.shape[-1])
+    assert np.isnan(y[:, 5:10]).all() and np.isfinite(y[:, 10:]).all()
+
+
 @pytest.mark.parametrize("cuda_graph", [False, True])
 def test_concurrent_launches_on_four_streams(ctx, cuda_graph):
     """One compiled C3 graph (the column kernel owns a cross-CTA workspace:
