@@ -397,22 +397,11 @@ KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& 
   return ks;
 }
 
-// A second-level sum of squared deviations from the broadcast first-level
-// total, b = Σ (u - m)², m = A or scale(A), A = Σ u over the same dims
-// (batch-norm's var.sum over d2 = d * d, d = x - mean_b).  Such a b needs no
-// pass of its own: shifted sums S1 = Σ (u - K), S2 = Σ (u - K)² with
-// K = u at reduced index 0 of the column (the same K in every stripe) fold in
-// A's pass, and A = N·K + S1, b = S2 - 2δ·S1 + N·δ², δ = m - K with m the fp32
-// mean the graph computes from A (all in fp64: b is the sum of (u - m)² around
-// that fp32 mean, the rounding of each d and d² left out — a reduction-order
-// class difference within the fp64-checked tolerance).
-struct Var2 {
-  int a = -1, b = -1, u = -1, mb = -1;
-};
-static std::vector<Var2> find_var2(const Ctx& c, const ColBcPlan& bp) {
+// Second moments folded in the first-level pass (lower_impl.hpp).
+std::vector<Var2> find_var2(const Ctx& c, const std::map<int, int>& level, int max_level) {
   const Graph& g = c.g;
   std::vector<Var2> out;
-  if (bp.max_level != 2 || c.peer) return out;
+  if (max_level != 2 || c.peer) return out;
   const char* env = std::getenv("SFX_COLBC_TWO_PASS");
   if (env && env[0] == '1') return out;
   auto is_ew = [&](int n, int kind) { return g.nodes[n].op == SFX_OP_ELEMENTWISE && g.nodes[n].kind == kind; };
@@ -421,7 +410,7 @@ static std::vector<Var2> find_var2(const Ctx& c, const ColBcPlan& bp) {
     return x.op == SFX_OP_REDUCE && x.reducer == SFX_REDUCE_SUM && x.dtype == SFX_F32;
   };
   for (int b : c.reduces) {
-    if (bp.level.at(b) != 2) continue;
+    if (level.at(b) != 2) continue;
     if (!sum_f32(b)) return {};
     const int sq = g.nodes[b].operands[0];
     if (!c.p.is_member(sq) || !is_ew(sq, SFX_EW_MUL) || g.nodes[sq].operands[0] != g.nodes[sq].operands[1]) return {};
@@ -434,7 +423,7 @@ static std::vector<Var2> find_var2(const Ctx& c, const ColBcPlan& bp) {
       int m = g.nodes[mb].operands[0];
       int a = m;
       if (c.p.is_member(m) && is_ew(m, SFX_EW_SCALE)) a = g.nodes[m].operands[0];
-      if (!c.p.is_member(a) || !sum_f32(a) || bp.level.count(a) == 0 || bp.level.at(a) != 1) continue;
+      if (!c.p.is_member(a) || !sum_f32(a) || level.count(a) == 0 || level.at(a) != 1) continue;
       const Node& an = g.nodes[a];
       if (an.operands[0] != u || an.reduce_dims != g.nodes[b].reduce_dims) continue;
       if (g.nodes[mb].dims != g.nodes[u].dims || g.nodes[u].dtype != SFX_F32) continue;
@@ -703,7 +692,7 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
     body.line("}");
   };
   // one-pass second moments (find_var2): b folds in a's pass, one level less
-  const std::vector<Var2> var2 = find_var2(c, bp);
+  const std::vector<Var2> var2 = find_var2(c, bp.level, bp.max_level);
   std::map<int, int> lvl = bp.level;
   int max_level = bp.max_level;
   std::map<int, const Var2*> var2_a, var2_b;

@@ -116,6 +116,21 @@ std::vector<Ix> orc_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t
                           const Ix& o, const Ix& r, const Ix& i);
 KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& o);
 KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_opts& o);
+// A second-level sum of squared deviations from the broadcast first-level
+// total, b = Σ (u - m)², m = A or scale(A), A = Σ u over the same dims
+// (batch-norm's / LayerNorm's var.sum over d2 = d * d, d = x - mean_b).  Such a
+// b needs no pass of its own: shifted sums S1 = Σ (u - K), S2 = Σ (u - K)² with
+// K = u at reduced index 0 (the same K for every partial of that reduction) fold in A's
+// pass, and A = N·K + S1, b = S2 - 2δ·S1 + N·δ², δ = m - K with m the fp32
+// mean the graph computes from A (all in fp64: b is the sum of (u - m)² around
+// that fp32 mean, the rounding of each d and d² left out — a reduction-order
+// class difference within the fp64-checked tolerance).  Empty unless every
+// level-2 reduce is such a b (max_level 2, no cross-rank combine);
+// SFX_COLBC_TWO_PASS=1 disables it.
+struct Var2 {
+  int a = -1, b = -1, u = -1, mb = -1;
+};
+std::vector<Var2> find_var2(const Ctx& c, const std::map<int, int>& level, int max_level);
 
 // ---- literal tier (lower_literal.cpp) ----
 KernelSource lower_literal(const Ctx& c);

@@ -215,8 +215,19 @@ std::map<int, int> plan_row_cache(const Ctx& c, const RowPlan& rp, const std::ve
 // Plain variant (inputs too large for a cluster, odd widths): one CTA per row,
 // one pass over the row per level plus a final pass, re-reading the row's
 // inputs (mostly from L2).  f32 sums accumulate in fp64 per thread.
-KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opts& o) {
+KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp_in, const sfx_compile_opts& o) {
   KernelSource ks;
+  // second moments folded in the first-level pass (find_var2): LayerNorm's
+  // variance needs no slice pass and no cluster combine of its own
+  const std::vector<Var2> var2 = find_var2(c, rp_in.level, rp_in.max_level);
+  RowPlan rp = rp_in;
+  std::map<int, const Var2*> var2_a, var2_b;
+  for (const Var2& q : var2) {
+    rp.level[q.b] = rp.level.at(q.a);
+    var2_a[q.a] = &q;
+    var2_b[q.b] = &q;
+  }
+  if (!var2.empty()) rp.max_level = 1;
   ks.strategy = "row";
   fill_common(c, ks);
   const int64_t R = rp.R, C = rp.C;
@@ -415,6 +426,21 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
     body.indent--;
     body.line("}");
   };
+  // K per second-moment pair: u at the row's column 0, from global memory (with
+  // a cluster it sits in rank 0's slice only); 0 when not finite
+  std::map<int, std::string> shiftK;
+  for (const Var2& q : var2) {
+    em.push();
+    em.staged.clear();
+    em.lane = 0;
+    const std::string v = em.value(q.u, rowcol_comps(em, c.g.nodes[q.u].dims, R, C, rowix, em.uni("0")));
+    const std::string k = em.fresh("shk");
+    body.line("const double " + k + " = ((__float_as_uint(" + v + ") & 0x7f800000u) != 0x7f800000u) ? (double)" + v +
+              " : 0.0;");
+    shiftK[q.a] = k;
+    em.staged = staged_map;
+    em.pop();
+  }
   for (int lv = 1; lv <= rp.max_level; ++lv) {
     std::vector<int> red;
     for (int r : c.reduces)
@@ -433,9 +459,19 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
         em.lane = lane;
         Ix col = V == 1 ? em.uni(cb) : em.lane_plus(cb);
         for (size_t k = 0; k < red.size(); ++k) {
+          if (var2_b.count(red[k])) continue;  // folded with its first-level sum
           const Node& rn = c.g.nodes[red[k]];
           const Node& in = c.g.nodes[rn.operands[0]];
           std::string v = em.value(rn.operands[0], rowcol_comps(em, in.dims, R, C, rowix, col));
+          auto qa = var2_a.find(red[k]);
+          if (qa != var2_a.end()) {  // shifted sums S1 (a's accumulator), S2 (b's)
+            const size_t kb = std::find(red.begin(), red.end(), qa->second->b) - red.begin();
+            const std::string t = em.fresh("sh");
+            body.line("const double " + t + " = (double)" + v + " - " + shiftK[red[k]] + ";");
+            body.line(acc[k] + " += " + t + ";");
+            body.line(acc[kb] + " = fma(" + t + ", " + t + ", " + acc[kb] + ");");
+            continue;
+          }
           body.line(acc[k] + " = " + fold_of(rn) + "(" + acc[k] + ", " + v + ");");
         }
       }
@@ -515,7 +551,13 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
       body.line("sfx_mbar_wait_bounded(" + cb_lv + ", " + (persist ? "(unsigned)((itr >> 1) & 1)" : "0u") + ");");
       if (persist) body.line("if (tid == 0) sfx_mbar_expect_tx(" + cb_lv + ", " + fmt_i(level_bytes[lv]) + "u);  // rearm for row itr + 2");
     }
-    for (size_t k = 0; k < red.size(); ++k) {
+    std::vector<size_t> order;  // second moments after the first-level sums they use
+    for (size_t k = 0; k < red.size(); ++k)
+      if (!var2_b.count(red[k])) order.push_back(k);
+    for (size_t k = 0; k < red.size(); ++k)
+      if (var2_b.count(red[k])) order.push_back(k);
+    std::map<int, std::string> raw;  // fp64 totals as folded (S1 for second-moment first levels)
+    for (size_t k : order) {
       const Node& rn = c.g.nodes[red[k]];
       const std::string T = acc_type(rn);
       if (push) {
@@ -525,9 +567,32 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
                   ", " + sl + "[r]);");
       }
       std::string fin = acc[k];
+      raw[red[k]] = acc[k];
+      if (var2_a.count(red[k])) {  // A = N·K + S1
+        fin = em.fresh("tot");
+        body.line("const double " + fin + " = " + fmt_i(C) + ".0 * " + shiftK[red[k]] + " + " + acc[k] + ";");
+      }
+      auto qb = var2_b.find(red[k]);
+      if (qb != var2_b.end()) {  // b = S2 - 2δ·S1 + N·δ², δ = m - K; a non-finite mean as in Σ (u - m)²
+        const Var2& q = *qb->second;
+        em.push();
+        em.staged.clear();
+        em.lane = 0;
+        const std::string m = em.value(q.mb, rowcol_comps(em, c.g.nodes[q.mb].dims, R, C, rowix, em.uni("0")));
+        em.staged = staged_map;
+        em.pop();
+        const std::string dl = em.fresh("dl");
+        fin = em.fresh("tot");
+        body.line("const double " + dl + " = (double)" + m + " - " + shiftK[q.a] + ";");
+        body.line("const double " + fin + " = ((__float_as_uint(" + m + ") & 0x7f800000u) != 0x7f800000u) ? " + acc[k] +
+                  " - 2.0 * " + dl + " * " + raw[q.a] + " + " + fmt_i(C) + ".0 * " + dl + " * " + dl + " : (" + m +
+                  " != " + m + " || !(fabs(" + raw[q.a] + ") <= 1.7976931348623157e308)) ? (double)(" + m + " - " + m +
+                  ") : (double)(" + m + " * " + m + ");");
+      }
       if (T == "double") {
+        const std::string d = fin;
         fin = em.fresh("red");
-        body.line("const float " + fin + " = (float)" + acc[k] + ";");
+        body.line("const float " + fin + " = (float)" + d + ";");
       }
       if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
         // the sequential fold's first element: the row's element 0, read from
@@ -607,11 +672,13 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp, const sfx_compile_opt
               " CTAs x " + std::to_string(B) + " threads per row, " + std::to_string(staged.size()) +
               " input slice(s) of " + std::to_string(slice_bytes) + " B in shared memory (TMA), " + (push ? "DSMEM push combine, " : "DSMEM combine, ") +
               (cache.empty() ? std::string() : std::to_string(cache.size()) + " member(s) cached over input slices, ") + "levels=" +
-              std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "");
+              std::to_string(rp.max_level) + (persist ? ", persistent: " + std::to_string(NCL) + " clusters, 2 stages" : "") +
+              (var2.empty() ? "" : ", " + std::to_string(var2.size()) + " second moment(s) in the first pass");
   else
     ks.note = "rows=" + std::to_string(R) + " cols=" + std::to_string(C) + " one CTA of " + std::to_string(B) +
               " threads per row, multi-pass (" + std::to_string(rp.max_level + (full_roots.empty() ? 0 : 1)) +
-              " passes, re-reads from L2) levels=" + std::to_string(rp.max_level);
+              " passes, re-reads from L2) levels=" + std::to_string(rp.max_level) +
+              (var2.empty() ? "" : ", " + std::to_string(var2.size()) + " second moment(s) in the first pass");
   return ks;
 }
 

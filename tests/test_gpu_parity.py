@@ -545,6 +545,29 @@ def test_colbc_second_moment_special_values(ctx, name, two_pass, monkeypatch):
     assert np.isnan(y[:, 5:10]).all() and np.isfinite(y[:, 10:]).all()
 
 
+@pytest.mark.parametrize("name", ["ln_r6_c98304", "ln_r5_c70001"])
+@pytest.mark.parametrize("two_pass", ["0", "1"])
+def test_long_row_layernorm_second_moment_forms(ctx, name, two_pass, monkeypatch):
+    """LayerNorm over long rows (cluster / multi-pass templates): the variance
+    as shifted sums in the mean's pass (default) and as its own level
+    (SFX_COLBC_TWO_PASS=1), on rows with a +10 offset, a constant row, and
+    non-finite rows (+inf, NaN, -inf at column 0 = the shift K)."""
+    monkeypatch.setenv("SFX_COLBC_TWO_PASS", two_pass)
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 31, -1.0, 1.0)
+    x = inputs["x"] + np.float32(10.0)
+    x[1, :] = np.float32(0.625)
+    x[2, 77] = np.inf
+    x[3, 5] = np.nan
+    x[4, 0] = -np.inf
+    inputs["x"] = x.astype(np.float32)
+    for kw in ({}, {"row_pipeline": 1}):
+        outs, launched, strategies = _run(ctx, g, rep, inputs, "auto", **kw)
+        assert strategies == ["row"] and launched == 1
+        assert not _check(g, outs, inputs, strict=True), kw
+        assert np.isnan(outs["y"][2:5]).all() and np.isfinite(outs["y"][[0, 1]]).all()
+
+
 @pytest.mark.parametrize("cuda_graph", [False, True])
 def test_concurrent_launches_on_four_streams(ctx, cuda_graph):
     """One compiled C3 graph (the column kernel owns a cross-CTA workspace:

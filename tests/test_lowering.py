@@ -96,7 +96,13 @@ def test_colbc_is_cooperative_with_grid_barriers(monkeypatch):
     for n, k in (("bn_mid_8x512x64", 0), ("bn_nhwc_16x16x8x128", 1)):
         _, _, note = _note(os.path.join(EXTRA, n + ".json"), k)
         assert "1 second moment(s)" in note, note
+    # LayerNorm over long rows: the same folding in the cluster and multi-pass templates
+    for n in ("ln_r6_c98304", "ln_r5_c70001"):
+        _, _, note = _note(os.path.join(EXTRA, n + ".json"))
+        assert "levels=1" in note and "1 second moment(s)" in note, note
     monkeypatch.setenv("SFX_COLBC_TWO_PASS", "1")
+    _, _, note = _note(os.path.join(EXTRA, "ln_r6_c98304.json"))
+    assert "levels=2" in note and "second moment" not in note
     src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))
     assert "sfx_grid_barrier(ws, 4u)" in src and "levels=2" in note and "second moment" not in note
 
