@@ -686,7 +686,20 @@ KernelSource lower_row_mp(const Ctx& c, const RowPlan& rp_in, const sfx_compile_
 // templates: reduction phases (per-thread fold -> shuffle tree -> broadcast
 // back through registers) then the element and row roots.  Expects `row`,
 // `lr` (lane within the row group), `gmask`, `gleader` in scope.
-void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int TPR, int V, int64_t NCH) {
+void emit_row_body(const Ctx& c, const RowPlan& rp_in, Emitter& em, Code& body, int TPR, int V, int64_t NCH) {
+  // SFX_ROW_VAR2=1: the variance folded in the mean's phase here too (fp64
+  // shifted sums; one shuffle / shared-memory round instead of two) — A/B
+  const char* v2env = std::getenv("SFX_ROW_VAR2");
+  const std::vector<Var2> var2 =
+      (v2env && v2env[0] == '1') ? find_var2(c, rp_in.level, rp_in.max_level) : std::vector<Var2>{};
+  RowPlan rp = rp_in;
+  std::map<int, const Var2*> var2_a, var2_b;
+  for (const Var2& q : var2) {
+    rp.level[q.b] = rp.level.at(q.a);
+    var2_a[q.a] = &q;
+    var2_b[q.b] = &q;
+  }
+  if (!var2.empty()) rp.max_level = 1;
   const int64_t R = rp.R, C = rp.C;
   const std::string& it = em.idx_t;
   std::vector<std::string> cb(NCH);
@@ -708,6 +721,20 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
     return f->second;
   };
 
+  std::map<int, std::string> shiftK;
+  for (const Var2& q : var2) {
+    em.push();
+    em.lane = 0;
+    const std::string v = em.value(q.u, rowcol_comps(em, c.g.nodes[q.u].dims, R, C, rowix, em.uni("0")));
+    const std::string k = em.fresh("shk");
+    body.line("const double " + k + " = ((__float_as_uint(" + v + ") & 0x7f800000u) != 0x7f800000u) ? (double)" + v +
+              " : 0.0;");
+    shiftK[q.a] = k;
+    em.pop();
+  }
+  auto vtype = [&](int r) -> std::string {
+    return var2_a.count(r) || var2_b.count(r) ? "double" : ctype(c.g.nodes[r].dtype);
+  };
   for (int lv = 1; lv <= rp.max_level; ++lv) {
     std::vector<int> red;
     for (int r : c.reduces)
@@ -715,16 +742,26 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
     std::vector<std::string> acc(red.size()), first(red.size());
     for (size_t k = 0; k < red.size(); ++k) {
       acc[k] = em.fresh("acc");
-      body.line(std::string(ctype(c.g.nodes[red[k]].dtype)) + " " + acc[k] + ";");
+      body.line(vtype(red[k]) + " " + acc[k] + (vtype(red[k]) == "double" ? " = 0.0;" : ";"));
     }
     for (int64_t j = 0; j < NCH; ++j)
       for (int lane = 0; lane < V; ++lane) {
         Ix col = col_ix(j, lane);
         for (size_t k = 0; k < red.size(); ++k) {
+          if (var2_b.count(red[k])) continue;  // folded with its first-level sum
           const Node& rn = c.g.nodes[red[k]];
           const Node& in = c.g.nodes[rn.operands[0]];
           std::vector<Ix> comps = rowcol_comps(em, in.dims, R, C, rowix, col);
           std::string v = em.value(rn.operands[0], comps);
+          auto qa = var2_a.find(red[k]);
+          if (qa != var2_a.end()) {
+            const size_t kb = std::find(red.begin(), red.end(), qa->second->b) - red.begin();
+            const std::string t = em.fresh("sh");
+            body.line("const double " + t + " = (double)" + v + " - " + shiftK[red[k]] + ";");
+            body.line(acc[k] + " += " + t + ";");
+            body.line(acc[kb] + " = fma(" + t + ", " + t + ", " + acc[kb] + ");");
+            continue;
+          }
           if (j == 0 && lane == 0) {
             body.line(acc[k] + " = " + v + ";");
             first[k] = v;
@@ -740,8 +777,10 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
       const char* f = rn.reducer == SFX_REDUCE_SUM ? "sfx_fold_sum"
                       : rn.reducer == SFX_REDUCE_MAX ? "sfx_fold_pmax" : "sfx_fold_pmin";
       for (int m = std::min(TPR, 32) / 2; m >= 1; m /= 2)
-        body.line(acc[k] + " = " + f + "(" + acc[k] + ", sfx_shfl_xor(" + acc[k] + ", " +
-                  std::to_string(m) + ", gmask));");
+        body.line(acc[k] + " = " + f + "(" + acc[k] + ", " +
+                  (vtype(red[k]) == "double" ? "__shfl_xor_sync(gmask, " + acc[k] + ", " + std::to_string(m) + ")"
+                                             : "sfx_shfl_xor(" + acc[k] + ", " + std::to_string(m) + ", gmask)") +
+                  ");");
     }
     const int W = TPR > 32 ? TPR / 32 : 1;  // warps per row
     std::vector<std::string> rsm(red.size()), rfm(red.size());
@@ -752,7 +791,7 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
       for (size_t k = 0; k < red.size(); ++k) {
         const Node& rn = c.g.nodes[red[k]];
         rsm[k] = em.fresh("rsm");
-        body.line(std::string("__shared__ ") + ctype(rn.dtype) + " " + rsm[k] + "[" + std::to_string(RPC) + "][" +
+        body.line("__shared__ " + vtype(red[k]) + " " + rsm[k] + "[" + std::to_string(RPC) + "][" +
                   std::to_string(W) + "];");
         body.line("if ((tid & 31) == 0) " + rsm[k] + "[rin][wir] = " + acc[k] + ";");
         if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
@@ -771,13 +810,39 @@ void emit_row_body(const Ctx& c, const RowPlan& rp, Emitter& em, Code& body, int
           body.line(acc[k] + " = " + f + "(" + acc[k] + ", " + rsm[k] + "[rin][" + std::to_string(w) + "]);");
       }
     }
-    for (size_t k = 0; k < red.size(); ++k) {
+    std::vector<size_t> order;  // second moments after the first-level sums they use
+    for (size_t k = 0; k < red.size(); ++k)
+      if (!var2_b.count(red[k])) order.push_back(k);
+    for (size_t k = 0; k < red.size(); ++k)
+      if (var2_b.count(red[k])) order.push_back(k);
+    for (size_t k : order) {
       const Node& rn = c.g.nodes[red[k]];
       if (rn.reducer != SFX_REDUCE_SUM && rn.dtype == SFX_F32) {
         std::string f0 = W > 1 ? rfm[k] + "[rin]" : TPR > 1 ? "sfx_shfl(" + first[k] + ", gleader, gmask)" : first[k];
         body.line(acc[k] + " = sfx_fold_first(" + f0 + ", " + acc[k] + ");");
       }
-      reduced[red[k]] = acc[k];
+      std::string fin = acc[k];
+      if (var2_a.count(red[k])) {  // A = N·K + S1
+        fin = em.fresh("red");
+        body.line("const float " + fin + " = (float)(" + fmt_i(C) + ".0 * " + shiftK[red[k]] + " + " + acc[k] + ");");
+      }
+      auto qb = var2_b.find(red[k]);
+      if (qb != var2_b.end()) {  // b = S2 - 2δ·S1 + N·δ², δ = m - K; a non-finite mean as in Σ (u - m)²
+        const Var2& q = *qb->second;
+        size_t ka = std::find(red.begin(), red.end(), q.a) - red.begin();
+        em.push();
+        em.lane = 0;
+        const std::string m = em.value(q.mb, rowcol_comps(em, c.g.nodes[q.mb].dims, R, C, rowix, em.uni("0")));
+        em.pop();
+        const std::string dl = em.fresh("dl");
+        fin = em.fresh("red");
+        body.line("const double " + dl + " = (double)" + m + " - " + shiftK[q.a] + ";");
+        body.line("const float " + fin + " = (float)(((__float_as_uint(" + m + ") & 0x7f800000u) != 0x7f800000u) ? " +
+                  acc[k] + " - 2.0 * " + dl + " * " + acc[ka] + " + " + fmt_i(C) + ".0 * " + dl + " * " + dl + " : (" +
+                  m + " != " + m + " || !(fabs(" + acc[ka] + ") <= 1.7976931348623157e308)) ? (double)(" + m + " - " + m +
+                  ") : (double)(" + m + " * " + m + "));");
+      }
+      reduced[red[k]] = fin;
     }
   }
 
