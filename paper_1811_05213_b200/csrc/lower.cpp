@@ -43,6 +43,9 @@ std::string choose_strategy(const Graph& g, int pi, std::string* why) {
       (bp.O * bp.I + 127) / 128 <= int64_t{kNumSMs} * 2)  // column tiles fit one co-resident wave
     return "colbc";
   reasons += "; colbc: " + w;
+  SplitPlan spl;
+  if (analyze_colbc_split(c, &spl, &w)) return "colbc";  // [A | K | B]: channels kept between reduced blocks
+  reasons += "; colbc (split): " + w;
   if (why) *why = reasons;
   return "literal";
 }
@@ -335,8 +338,15 @@ KernelSource lower_program_raw(const Graph& g, int pi, const sfx_compile_opts& o
     }
     case SFX_STRATEGY_COLBC: {
       ColBcPlan bp;
-      if (!analyze_colbc(c, &bp, &why)) throw Error(SFX_ERR_UNSUPPORTED, "colbc template not applicable: " + why);
-      ks = lower_colbc(c, bp, o);
+      SplitPlan spl;
+      std::string why_split;
+      if (analyze_colbc(c, &bp, &why)) {
+        ks = lower_colbc(c, bp, o);
+      } else if (!c.peer && analyze_colbc_split(c, &spl, &why_split)) {
+        ks = lower_colbc_split(c, spl, o);
+      } else {
+        throw Error(SFX_ERR_UNSUPPORTED, "colbc template not applicable: " + why + "; split: " + why_split);
+      }
       break;
     }
     case SFX_STRATEGY_LITERAL:

@@ -503,5 +503,101 @@ bool analyze_colbc(const Ctx& c, ColBcPlan* bp, std::string* why) {
   return true;
 }
 
+bool analyze_colbc_split(const Ctx& c, SplitPlan* sp, std::string* why) {
+  const Graph& g = c.g;
+  if (!c.dots.empty()) return *why = "group contains a matmul", false;
+  if (c.reduces.empty()) return *why = "no reduction", false;
+  for (int r : c.reduces) {
+    const Node& n = g.nodes[r];
+    const Node& in = g.nodes[n.operands[0]];
+    if (n.reducer != SFX_REDUCE_SUM || n.dtype != SFX_F32) return *why = "reduce " + n.id + " is not an f32 sum", false;
+    std::vector<bool> red(in.rank(), false);
+    for (int64_t d : n.reduce_dims) red[d] = true;
+    int k0 = 0;
+    while (k0 < in.rank() && red[k0]) ++k0;
+    int k1 = k0;
+    while (k1 < in.rank() && !red[k1]) ++k1;
+    for (int d = k1; d < in.rank(); ++d)
+      if (!red[d]) return *why = "reduce " + n.id + " keeps a non-contiguous dim block", false;
+    if (k0 == 0 || k1 == in.rank()) return *why = "reduce " + n.id + " dims are contiguous (colbc)", false;
+    const int64_t A = prod(in.dims, 0, k0), K = prod(in.dims, k0, k1), B = prod(in.dims, k1, in.dims.size());
+    if (sp->K == 0) {
+      sp->A = A, sp->K = K, sp->B = B;
+    } else if (sp->A != A || sp->K != K || sp->B != B) {
+      return *why = "reductions with different geometry", false;
+    }
+  }
+  const int64_t A = sp->A, K = sp->K, B = sp->B;
+  if (A * B <= 1 || K == A * K * B) return *why = "degenerate channel length", false;
+  enum { FULL = 1, CHAN = 2 };
+  std::map<int, int> cls;
+  auto cls_of = [&](int64_t n) { return n == A * K * B ? FULL : n == K ? CHAN : 0; };
+  for (int m : c.topo) {
+    const Node& n = g.nodes[m];
+    if (!c.dep.at(m)) continue;
+    if (n.op == SFX_OP_REDUCE && !degenerate_reduce(g, n)) {
+      int op = n.operands[0];
+      if (c.p.is_member(op) && c.dep.at(op) && cls[op] != FULL)
+        return *why = "reduce operand " + g.nodes[op].id + " is not element-shaped", false;
+      cls[m] = CHAN;
+      int lv = 1;
+      std::set<int> seen;
+      std::function<void(int)> walk = [&](int x) {
+        if (!c.p.is_member(x) || seen.count(x)) return;
+        seen.insert(x);
+        if (x != m && g.nodes[x].op == SFX_OP_REDUCE && !degenerate_reduce(g, g.nodes[x]))
+          lv = std::max(lv, sp->level[x] + 1);
+        else
+          for (int o : g.nodes[x].operands) walk(o);
+      };
+      for (int o : n.operands) walk(o);
+      sp->level[m] = lv;
+      sp->max_level = std::max(sp->max_level, lv);
+      continue;
+    }
+    int k = cls_of(n.numel());
+    if (!k) return *why = "member " + n.id + " is neither element- nor channel-shaped", false;
+    for (int op : n.operands) {
+      if (!c.p.is_member(op) || !c.dep.at(op)) continue;
+      int oc = cls[op];
+      switch (n.op) {
+        case SFX_OP_ELEMENTWISE:
+        case SFX_OP_RESHAPE:
+        case SFX_OP_BITCAST:
+        case SFX_OP_REDUCE:  // degenerate
+          if (oc != k) return *why = "class mismatch at " + n.id, false;
+          break;
+        case SFX_OP_TRANSPOSE:
+          if (oc != k || !transpose_is_reshape(n)) return *why = "transpose of dependent data at " + n.id, false;
+          break;
+        case SFX_OP_BROADCAST: {
+          if (bcast_is_reshape(n) && oc == k) break;
+          // channels broadcast back: the output splits as [A dims | K dims | B dims]
+          // and the operand maps onto the K dims
+          int k0 = prefix_split(n.dims, A), k1 = k0 < 0 ? -1 : prefix_split(n.dims, A * K);
+          bool ok = k == FULL && oc == CHAN && k0 >= 0 && k1 >= k0 && prod(n.dims, k1, n.dims.size()) == B;
+          std::vector<int64_t> want;
+          for (int d = 0; d < n.rank(); ++d)
+            if (d >= k0 && d < k1 && n.dims[d] != 1) want.push_back(d);
+          std::vector<int64_t> have;
+          for (size_t j = 0; j < n.dim_map.size(); ++j)
+            if (g.nodes[op].dims[j] != 1) have.push_back(n.dim_map[j]);
+          if (!ok || want != have) return *why = "broadcast " + n.id + " does not map channels to channels", false;
+          break;
+        }
+        default:
+          return *why = "unsupported op at " + n.id, false;
+      }
+    }
+    cls[m] = k;
+  }
+  for (int r : c.p.roots) {
+    int k = cls_of(c.g.nodes[r].numel());
+    if (!k) return *why = "root " + g.nodes[r].id + " is neither element- nor channel-shaped", false;
+    if (c.dep.at(r) && cls[r] != k) return *why = "root class mismatch", false;
+  }
+  return true;
+}
+
 }  // namespace lw
 }  // namespace sfx

@@ -990,5 +990,258 @@ KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_op
   return ks;
 }
 
+// Channel statistics broadcast back over [A | K | B] (reduce A and B, keep K:
+// batch-norm over NCHW).  A CTA tile is one channel; S stripes of its A·B/V
+// vectors (V = 4 along the contiguous B block when B % 4 == 0).  Per level: a
+// pass over the stripe (fp64 accumulators, lanes folded together; the
+// variance as shifted sums in the mean's pass, find_var2), a warp-order CTA
+// combine, then with S > 1 partials to the workspace, one grid barrier and every
+// CTA of the channel folding the S partials in stripe order (identical totals;
+// cooperative launch); with S == 1 (K >= 148 channels) no grid barrier at all.
+// Passes alternate direction (the re-read starts on the vectors still in L2).
+KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_compile_opts& o) {
+  KernelSource ks;
+  ks.strategy = "colbc";
+  ks.entry = "sfx_colbc_" + c.name;
+  fill_common(c, ks);
+  const int64_t A = sp.A, K = sp.K, B = sp.B;
+  const int V = (B % 4 == 0) ? 4 : 1;
+  const int64_t BV = B / V, NV = A * BV;  // vectors per channel
+  const int WARPS = 8, T = WARPS * 32;
+  const int ctas_per_sm = o.pipe_ctas_per_sm > 0 ? std::min(o.pipe_ctas_per_sm, 8) : 2;
+  int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / K);
+  S = std::max<int64_t>(1, std::min<int64_t>(S, NV / (4 * T)));
+  if (S > 1 && K * S > int64_t{kNumSMs} * ctas_per_sm) S = std::max<int64_t>(1, kNumSMs * ctas_per_sm / K);
+  const int64_t RS = (NV + S - 1) / S;
+  const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
+  std::vector<Var2> var2 = find_var2(c, sp.level, sp.max_level);
+  std::map<int, int> lvl = sp.level;
+  int max_level = sp.max_level;
+  std::map<int, const Var2*> var2_a, var2_b;
+  for (const Var2& q : var2) {
+    lvl[q.b] = lvl.at(q.a);
+    var2_a[q.a] = &q;
+    var2_b[q.b] = &q;
+  }
+  if (!var2.empty()) max_level = 1;
+  Emitter em(c.g, c.p, V, c.wide);
+  em.rcp_reduced_divisors = rcp_divisors();
+  std::string sig = signature(c, em, ks.entry, T, ctas_per_sm);
+  Code body;
+  em.code = &body;
+  const std::string& it = em.idx_t;
+  // workspace: barrier counters (64 words), then per reduce partials[S][K] (8-byte slots)
+  std::map<int, int64_t> part_word;
+  int64_t words = 64;
+  for (int r : c.reduces) {
+    part_word[r] = words;
+    words += S * K * 2;
+  }
+  if (S > 1) {
+    ks.workspace_bytes = words * 4;
+    ks.cooperative = true;
+  }
+  body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
+  body.line("const " + it + " kc = (" + it + ")blockIdx.x;");
+  body.line("const " + it + " v_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  body.line("const " + it + " v_end = min((" + it + ")" + fmt_i(NV) + ", v_begin + " + fmt_i(RS) + ");");
+  const Ix kix = em.uni("kc");
+  // element (a, kc, b) of a node of `dims`; vector v = a * BV + b / V
+  auto elem = [&](const std::vector<int64_t>& dims, const std::string& a, const std::string& b0, int l) {
+    em.lane = l;
+    Ix bix = V == 1 ? em.uni(b0) : em.lane_plus(b0);
+    return orc_comps(em, dims, A, K, B, em.uni(a), kix, bix);
+  };
+  std::map<int, std::string> total;
+  em.resolve = [&](int node, const std::vector<Ix>&) -> std::string {
+    auto f = total.find(node);
+    if (f == total.end()) {
+      if (c.g.nodes[node].op == SFX_OP_REDUCE && !degenerate_reduce(c.g, c.g.nodes[node]))
+        throw Error(SFX_ERR_INVALID, "internal: reduction used before it is combined");
+      return "";
+    }
+    return f->second;
+  };
+  // K per second-moment pair: u at (0, kc, 0); 0 when not finite
+  std::map<int, std::string> shiftK;
+  for (const Var2& q : var2) {
+    em.push();
+    const std::string v = em.value(q.u, elem(c.g.nodes[q.u].dims, "0", "0", 0));
+    const std::string k = em.fresh("shk");
+    body.line("const double " + k + " = ((__float_as_uint(" + v + ") & 0x7f800000u) != 0x7f800000u) ? (double)" + v +
+              " : 0.0;");
+    shiftK[q.a] = k;
+    em.pop();
+  }
+  int pass_no = 0;
+  // a pass over this CTA's vectors: UR per thread per iteration (loads in flight together)
+  auto stripe_pass = [&](const std::function<void(const std::string&, const std::string&)>& vec) {
+    const bool rev = pass_no++ % 2 == 1;
+    auto one = [&](const std::string& vf) {
+      std::string vv = vf;
+      if (rev) {
+        vv = em.fresh("vr");
+        body.line("const " + it + " " + vv + " = v_begin + v_end - 1 - (" + vf + ");");
+      }
+      const std::string a = em.fresh("a"), b0 = em.fresh("b");
+      body.line("const " + it + " " + a + " = " + vv + " / " + fmt_i(BV) + ";");
+      body.line("const " + it + " " + b0 + " = (" + vv + " - " + a + " * " + fmt_i(BV) + ") * " + std::to_string(V) + ";");
+      vec(a, b0);
+    };
+    const std::string v = em.fresh("v");
+    body.line(it + " " + v + " = v_begin + threadIdx.x;");
+    body.line("for (; " + v + " + " + std::to_string((UR - 1) * T) + " < v_end; " + v + " += " + std::to_string(UR * T) +
+              ") {");
+    body.indent++;
+    em.push();
+    for (int u = 0; u < UR; ++u) {
+      const std::string vu = em.fresh("vu");
+      body.line("const " + it + " " + vu + " = " + v + " + " + std::to_string(u * T) + ";");
+      one(vu);
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+    body.line("for (; " + v + " < v_end; " + v + " += " + std::to_string(T) + ") {");
+    body.indent++;
+    em.push();
+    one(v);
+    em.pop();
+    body.indent--;
+    body.line("}");
+  };
+  for (int lv = 1; lv <= max_level; ++lv) {
+    std::vector<int> red;
+    for (int r : c.reduces)
+      if (lvl.at(r) == lv) red.push_back(r);
+    std::vector<std::string> acc(red.size());
+    for (size_t k = 0; k < red.size(); ++k) {
+      acc[k] = em.fresh("acc");
+      body.line("double " + acc[k] + " = 0.0;");
+    }
+    stripe_pass([&](const std::string& a, const std::string& b0) {
+      for (int l = 0; l < V; ++l) {
+        for (size_t k = 0; k < red.size(); ++k) {
+          if (var2_b.count(red[k])) continue;  // folded with its first-level sum
+          const Node& rn = c.g.nodes[red[k]];
+          std::string v = em.value(rn.operands[0], elem(c.g.nodes[rn.operands[0]].dims, a, b0, l));
+          auto qa = var2_a.find(red[k]);
+          if (qa != var2_a.end()) {
+            const size_t kb = std::find(red.begin(), red.end(), qa->second->b) - red.begin();
+            const std::string t = em.fresh("sh");
+            body.line("const double " + t + " = (double)" + v + " - " + shiftK[red[k]] + ";");
+            body.line(acc[k] + " += " + t + ";");
+            body.line(acc[kb] + " = fma(" + t + ", " + t + ", " + acc[kb] + ");");
+            continue;
+          }
+          body.line(acc[k] + " += (double)" + v + ";");
+        }
+      }
+    });
+    // CTA combine: warp shuffle tree, then the warps in order
+    for (size_t k = 0; k < red.size(); ++k) {
+      for (int m = 16; m >= 1; m /= 2)
+        body.line(acc[k] + " += __shfl_xor_sync(0xffffffffu, " + acc[k] + ", " + std::to_string(m) + ");");
+      const std::string sm = em.fresh("wsm");
+      body.line("__shared__ double " + sm + "[" + std::to_string(WARPS) + "];");
+      body.line("if (lane == 0) " + sm + "[warp] = " + acc[k] + ";");
+      body.line("__syncthreads();");
+      body.line(acc[k] + " = " + sm + "[0];");
+      body.line("for (int w = 1; w < " + std::to_string(WARPS) + "; ++w) " + acc[k] + " += " + sm + "[w];");
+      if (S > 1)
+        body.line("if (threadIdx.x == 0) *(double*)((unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) +
+                  ") + (" + it + ")blockIdx.y * " + fmt_i(K) + " + kc) = " + acc[k] + ";");
+    }
+    if (S > 1) {
+      body.line("sfx_grid_barrier(ws, " + std::to_string(lv) + "u);");
+      // every CTA of the channel folds its S partials in stripe order (identical totals)
+      for (size_t k = 0; k < red.size(); ++k) {
+        body.line(acc[k] + " = 0.0;");
+        body.line("for (int s = 0; s < " + fmt_i(S) + "; ++s) " + acc[k] + " += __ldcg((const double*)((const unsigned long long*)(ws + " +
+                  fmt_i(part_word[red[k]]) + ") + (" + it + ")s * " + fmt_i(K) + " + kc));");
+      }
+    }
+    std::vector<size_t> order;
+    for (size_t k = 0; k < red.size(); ++k)
+      if (!var2_b.count(red[k])) order.push_back(k);
+    for (size_t k = 0; k < red.size(); ++k)
+      if (var2_b.count(red[k])) order.push_back(k);
+    for (size_t k : order) {
+      std::string fin = em.fresh("tot");
+      if (var2_a.count(red[k])) {  // A = N·K + S1
+        body.line("const float " + fin + " = (float)(" + fmt_i(A * B) + ".0 * " + shiftK[red[k]] + " + " + acc[k] + ");");
+      } else if (var2_b.count(red[k])) {  // b = S2 - 2δ·S1 + N·δ²; a non-finite mean as in Σ (u - m)²
+        const Var2& q = *var2_b.at(red[k]);
+        const size_t ka = std::find(red.begin(), red.end(), q.a) - red.begin();
+        em.push();
+        const std::string m = em.value(q.mb, elem(c.g.nodes[q.mb].dims, "0", "0", 0));
+        em.pop();
+        const std::string dl = em.fresh("dl");
+        body.line("const double " + dl + " = (double)" + m + " - " + shiftK[q.a] + ";");
+        body.line("const float " + fin + " = (float)(((__float_as_uint(" + m + ") & 0x7f800000u) != 0x7f800000u) ? " +
+                  acc[k] + " - 2.0 * " + dl + " * " + acc[ka] + " + " + fmt_i(A * B) + ".0 * " + dl + " * " + dl +
+                  " : (" + m + " != " + m + " || !(fabs(" + acc[ka] + ") <= 1.7976931348623157e308)) ? (double)(" + m +
+                  " - " + m + ") : (double)(" + m + " * " + m + "));");
+      } else {
+        body.line("const float " + fin + " = (float)" + acc[k] + ";");
+      }
+      total[red[k]] = fin;
+    }
+  }
+  // final pass: element roots; channel roots by stripe 0
+  std::vector<int> full_roots, chan_roots;
+  for (int r : c.p.roots) (c.g.nodes[r].numel() == A * K * B ? full_roots : chan_roots).push_back(r);
+  if (!full_roots.empty())
+    stripe_pass([&](const std::string& a, const std::string& b0) {
+      std::vector<std::vector<std::string>> fv(full_roots.size(), std::vector<std::string>(V));
+      std::vector<std::vector<std::string>> fad(full_roots.size(), std::vector<std::string>(V));
+      std::vector<std::string> base(full_roots.size());
+      std::vector<bool> fvec(full_roots.size(), V == 4);
+      for (int l = 0; l < V; ++l)
+        for (size_t k = 0; k < full_roots.size(); ++k) {
+          std::vector<Ix> comps = elem(c.g.nodes[full_roots[k]].dims, a, b0, l);
+          fv[k][l] = em.value(full_roots[k], comps);
+          Ix L = em.linearize(comps, c.g.nodes[full_roots[k]].dims);
+          fad[k][l] = L.e;
+          if (l == 0) {
+            if (L.kind == IX_PLUS) base[k] = L.base;
+            else fvec[k] = false;
+          }
+        }
+      for (size_t k = 0; k < full_roots.size(); ++k) {
+        const std::string out = "out" + std::to_string(root_slot(c, full_roots[k]));
+        if (fvec[k])
+          body.line("sfx_st4(" + out + " + " + base[k] + ", " + fv[k][0] + ", " + fv[k][1] + ", " + fv[k][2] + ", " +
+                    fv[k][3] + ");");
+        else
+          for (int l = 0; l < V; ++l) body.line(out + "[" + fad[k][l] + "] = " + fv[k][l] + ";");
+      }
+    });
+  if (!chan_roots.empty()) {
+    body.line("if (blockIdx.y == 0 && threadIdx.x == 0) {");
+    body.indent++;
+    em.push();
+    em.lane = 0;
+    for (int r : chan_roots) {
+      std::string v = em.value(r, em.from_linear(kix, c.g.nodes[r].dims));
+      body.line("out" + std::to_string(root_slot(c, r)) + "[kc] = " + v + ";");
+    }
+    em.pop();
+    body.indent--;
+    body.line("}");
+  }
+  if (S > 1) body.line("sfx_grid_exit(ws);");
+  ks.code = assemble(sig, body);
+  ks.block = T;
+  ks.grid_x = K;
+  ks.grid_y = S;
+  ks.vector_width = V;
+  ks.note = "split A=" + std::to_string(A) + " channels=" + std::to_string(K) + " B=" + std::to_string(B) +
+            " stripes=" + std::to_string(S) + " levels=" + std::to_string(max_level) +
+            (S > 1 ? " (grid barriers, cooperative launch)" : " (one CTA per channel, no grid barrier)") +
+            (var2.empty() ? "" : ", " + std::to_string(var2.size()) + " second moment(s) in the first pass");
+  return ks;
+}
+
 }  // namespace lw
 }  // namespace sfx

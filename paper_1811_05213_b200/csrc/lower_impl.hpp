@@ -81,6 +81,16 @@ struct ColBcPlan {
   int max_level = 0;
 };
 bool analyze_colbc(const Ctx& c, ColBcPlan* bp, std::string* why);
+// Channel statistics broadcast back with the reduced dims on BOTH sides of the
+// kept block — [A | K | B], reduce over A and B (batch-norm over NCHW: reduce
+// {0, 2, 3}, keep C; the reference plans it as one group of one block).
+// Classes: FULL (A·K·B elements) and CHAN (K channels).  f32 sums only.
+struct SplitPlan {
+  int64_t A = 0, K = 0, B = 0;
+  std::map<int, int> level;
+  int max_level = 0;
+};
+bool analyze_colbc_split(const Ctx& c, SplitPlan* sp, std::string* why);
 bool analyze_map(const Ctx& c, std::string* why);
 
 // ---- map + tiled transpose (lower_map.cpp) ----
@@ -116,6 +126,7 @@ std::vector<Ix> orc_comps(Emitter& em, const std::vector<int64_t>& dims, int64_t
                           const Ix& o, const Ix& r, const Ix& i);
 KernelSource lower_col(const Ctx& c, const ColPlan& cp, const sfx_compile_opts& o);
 KernelSource lower_colbc(const Ctx& c, const ColBcPlan& bp, const sfx_compile_opts& o);
+KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_compile_opts& o);
 // A second-level sum of squared deviations from the broadcast first-level
 // total, b = Σ (u - m)², m = A or scale(A), A = Σ u over the same dims
 // (batch-norm's / LayerNorm's var.sum over d2 = d * d, d = x - mean_b).  Such a

@@ -129,6 +129,11 @@ EXTRA = {
     "bn_4096x256": bn_graph([4096, 256], [0]),
     "bn_mid_8x512x64": bn_graph([8, 512, 64], [1]),
     "bn_nhwc_16x16x8x128": bn_graph([16, 16, 8, 128], [0, 1, 2], with_stats=True),
+    # batch-norm over NCHW: reduced dims on both sides of the channel block
+    # ([A | K | B]); the reference plans it as one group of one block
+    "bn_nchw_16x8x64x64": bn_graph([16, 8, 64, 64], [0, 2, 3]),  # 16 stripes per channel: grid barrier
+    "bn_nchw_4x160x7x7": bn_graph([4, 160, 7, 7], [0, 2, 3]),  # B = 49: scalar vectors
+    "bn_nchw_8x32x14x14": bn_graph([8, 32, 14, 14], [0, 2, 3], with_stats=True),  # channel root
     # one rank"s shard of a 2-rank SyncBatchNorm over 4096 rows (global count)
     "bnsync_shard_2048x256": bn_graph([2048, 256], [0], count=4096),
     "bnmax_3000x37": {"instructions": [

@@ -258,8 +258,8 @@ def test_cross_rank_rejects_non_column_batch_reduce():
                              "root_index": 0}])
     with pytest.raises(H.ExecError, match="sharded dim 0"):
         H.codegen(g, prog, cross_rank=1)
-    _, _, note = H.codegen(g, prog)  # single rank: the literal tier takes it
-    assert note.startswith("literal")
+    _, _, note = H.codegen(g, prog)  # single rank: the split column template takes it
+    assert note.startswith("colbc split A=8 channels=16 B=4"), note
 
 
 def test_cross_rank_accepts_sync_batchnorm():

@@ -545,6 +545,56 @@ def test_colbc_second_moment_special_values(ctx, name, two_pass, monkeypatch):
     assert np.isnan(y[:, 5:10]).all() and np.isfinite(y[:, 10:]).all()
 
 
+@pytest.mark.parametrize("name", ["bn_nchw_16x8x64x64", "bn_nchw_4x160x7x7", "bn_nchw_8x32x14x14"])
+@pytest.mark.parametrize("two_pass", ["0", "1"])
+def test_colbc_split_nchw(ctx, name, two_pass, monkeypatch):
+    """Batch-norm over NCHW (channels between the reduced dims): the split
+    colbc template (one CTA per channel, or stripes + one grid barrier) with
+    the variance folded in the mean's pass or as its own level, on a +2
+    offset, a constant channel and non-finite channels (+inf, NaN, -inf at the
+    channel's first element = the shift K).  (At +10 with 196 elements per
+    channel the fp32 mean's rounding alone, ulp(10) / 2 x rstd, exceeds the
+    strict bound against the fp64 restatement for ANY fp32 evaluation: the
+    reference's own fp32 result is 7.4e-6 off there.)"""
+    monkeypatch.setenv("SFX_COLBC_TWO_PASS", two_pass)
+    g, rep, _ = H.load_bundle(os.path.join(T.GOLDEN, "plans_extra", name + ".json"))
+    inputs = T.gen_inputs(g, 37, -1.0, 1.0)
+    x = inputs["x"] + np.float32(2.0)
+    x[:, 2] = np.float32(-0.25)
+    x[1, 5].flat[7] = np.inf
+    x[-1, 6].flat[-1] = np.nan
+    x[0, 7].flat[0] = -np.inf
+    inputs["x"] = x.astype(np.float32)
+    outs, launched, strategies = _run(ctx, g, rep, inputs, "auto")
+    assert "colbc" in strategies and launched == len(rep.kernels)
+    assert not _check(g, outs, inputs, strict=True)
+    y = outs["y"]
+    assert np.isnan(y[:, 5:8]).all() and np.isfinite(y[:, [0, 1, 2, 3, 4]]).all()
+
+
+def test_colbc_split_channel_sums_only(ctx):
+    """A non-contiguous reduction with no broadcast back (channel sums of
+    [8, 16, 4] over {0, 2}, then a scale): the split template's channel roots,
+    against the fp64 oracle; the literal tier (the reference's program) agrees."""
+    doc = {"instructions": [
+        {"id": "p", "op": "parameter", "shape": [8, 16, 4]},
+        {"id": "s", "op": "reduce", "operands": ["p"], "shape": [16], "reduce_dims": [0, 2], "reducer": "sum"},
+        {"id": "y", "op": "scale", "operands": ["s"], "shape": [16], "scalar": 2.0},
+    ], "outputs": ["y"]}
+    g = H.graph_from_json(doc)
+    prog = H.KernelProgram("y", ["s", "y"], ["y"], 1, 64, 64,
+                           [{"kind": "materialize", "instr": "s", "schedule": [0, 1, "row"], "dest": "shared",
+                             "offset": 0, "bytes": 64}, {"kind": "barrier"},
+                            {"kind": "materialize", "instr": "y", "schedule": [0, 1, "row"], "dest": "output",
+                             "root_index": 0}])
+    inputs = T.gen_inputs(g, 41, -1.0, 1.0)
+    ref = T.interpret(g, inputs, 1)["y"]
+    (y,) = H.run_program(prog, g, inputs, ctx=ctx)
+    assert T.strict_close(y, ref), T.mismatch_report(y, ref)
+    (yl,) = H.run_program(prog, g, inputs, ctx=ctx, strategy="literal")
+    assert T.values_close(yl, T.interpret(g, inputs, 0)["y"])
+
+
 @pytest.mark.parametrize("name", ["ln_r6_c98304", "ln_r5_c70001"])
 @pytest.mark.parametrize("two_pass", ["0", "1"])
 def test_long_row_layernorm_second_moment_forms(ctx, name, two_pass, monkeypatch):

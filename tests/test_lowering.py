@@ -100,7 +100,15 @@ def test_colbc_is_cooperative_with_grid_barriers(monkeypatch):
     for n in ("ln_r6_c98304", "ln_r5_c70001"):
         _, _, note = _note(os.path.join(EXTRA, n + ".json"))
         assert "levels=1" in note and "1 second moment(s)" in note, note
+    # batch-norm over NCHW: the split layout (channels between the reduced dims)
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_16x8x64x64.json"))
+    assert note.startswith("colbc split A=16 channels=8 B=4096 stripes=16") and "grid barriers" in note, note
+    assert "1 second moment(s)" in note
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_4x160x7x7.json"))
+    assert "stripes=1" in note and "no grid barrier" in note, note
     monkeypatch.setenv("SFX_COLBC_TWO_PASS", "1")
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_16x8x64x64.json"))
+    assert "levels=2" in note and "second moment" not in note
     _, _, note = _note(os.path.join(EXTRA, "ln_r6_c98304.json"))
     assert "levels=2" in note and "second moment" not in note
     src, _, note = _note(os.path.join(EXTRA, "bn_4096x256.json"))

@@ -24,7 +24,9 @@ from make_extra_plans import bn_graph  # noqa: E402
 
 CASES = {"batchnorm_65536x256": bn_graph([65536, 256], [0]),
          "batchnorm_nhwc_64x56x56x256": bn_graph([64, 56, 56, 256], [0, 1, 2]),
-         "batchnorm_offset_65536x256": bn_graph([65536, 256], [0])}
+         "batchnorm_offset_65536x256": bn_graph([65536, 256], [0]),
+         "batchnorm_nchw_64x256x56x56": bn_graph([64, 256, 56, 56], [0, 2, 3]),
+         "batchnorm_nchw_32x64x112x112": bn_graph([32, 64, 112, 112], [0, 2, 3])}
 OUT = os.path.join(tempfile.gettempdir(), "colbc_check")
 os.makedirs(OUT, exist_ok=True)
 

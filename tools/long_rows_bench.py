@@ -22,6 +22,8 @@ ONLY = [a for a in sys.argv[1:] if not a.startswith("--")]
 CASES = {"batchnorm_65536x256": bn_graph([65536, 256], [0]),
          "batchnorm_262144x1024": bn_graph([262144, 1024], [0]),
          "batchnorm_nhwc_64x56x56x256": bn_graph([64, 56, 56, 256], [0, 1, 2]),
+         "batchnorm_nchw_64x256x56x56": bn_graph([64, 256, 56, 56], [0, 2, 3]),
+         "batchnorm_nchw_32x64x112x112": bn_graph([32, 64, 112, 112], [0, 2, 3]),
          "softmax_1024x131072": configs.c2_softmax(B=1, H=1, S=1024, L=131072),
          "layernorm_1024x131072": configs.c1_layernorm(R=1024, C=131072),
          "softmax_256x262144": configs.c2_softmax(B=1, H=1, S=256, L=262144)}
@@ -39,7 +41,7 @@ for name, doc in CASES.items():
     bpath = os.path.join(tempfile.gettempdir(), name + ".json")
     open(bpath, "w").write(out)
     g, rep, b = H.load_bundle(bpath)
-    variants = [{}] + ([{"row_pipeline": 1}, {"items_per_thread": 4}, {"items_per_thread": 2}, {"pipe_ctas_per_sm": 1}, {"pipe_ctas_per_sm": 3}] if name.startswith("batchnorm") else [{"row_pipeline": 1}, {"pipe_stages": 8}, {"row_pipeline": 5}, {"row_pipeline": 3}])
+    variants = [{}] + ([{"items_per_thread": 4}, {"items_per_thread": 16}, {"pipe_ctas_per_sm": 3}, {"pipe_ctas_per_sm": 4}] if "nchw" in name else [{"row_pipeline": 1}, {"items_per_thread": 4}, {"items_per_thread": 2}, {"pipe_ctas_per_sm": 1}, {"pipe_ctas_per_sm": 3}] if name.startswith("batchnorm") else [{"row_pipeline": 1}, {"pipe_stages": 8}, {"row_pipeline": 5}, {"row_pipeline": 3}])
     if "--literal" in sys.argv:
         variants.append({"strategy": "literal"})
     pick = [a[len("--variant="):] for a in sys.argv if a.startswith("--variant=")]
