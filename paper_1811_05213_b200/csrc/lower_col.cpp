@@ -1012,7 +1012,18 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
   int64_t S = o.rows_per_cta > 0 ? o.rows_per_cta : std::max<int64_t>(1, kNumSMs * ctas_per_sm / K);
   S = std::max<int64_t>(1, std::min<int64_t>(S, NV / (4 * T)));
   if (S > 1 && K * S > int64_t{kNumSMs} * ctas_per_sm) S = std::max<int64_t>(1, kNumSMs * ctas_per_sm / K);
-  const int64_t RS = (NV + S - 1) / S;
+  // a channel per CTA leaves SMs unevenly loaded when K is not a multiple of
+  // the SM count (256 channels on 148 SMs: 108 SMs carry two): from 74 channels
+  // up, a thread-block cluster of CS CTAs takes each channel instead (>= 4
+  // clusters' worth of CTAs per SM), the CTAs combining their partials through
+  // distributed shared memory — no grid barrier.  pipe_stages = 1: one CTA per
+  // channel (A/B)
+  int CS = 1;
+  if (K >= 74 && o.pipe_stages != 1 && o.rows_per_cta <= 0) {
+    S = 1;
+    while (CS < 8 && K * CS < int64_t{kNumSMs} * 4 && NV / (CS * 2) >= 4 * T) CS *= 2;
+  }
+  const int64_t RS = (NV + S * CS - 1) / (S * CS);
   const int UR = o.items_per_thread > 0 ? std::min(o.items_per_thread, 16) : 8;
   std::vector<Var2> var2 = find_var2(c, sp.level, sp.max_level);
   std::map<int, int> lvl = sp.level;
@@ -1027,6 +1038,10 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
   Emitter em(c.g, c.p, V, c.wide);
   em.rcp_reduced_divisors = rcp_divisors();
   std::string sig = signature(c, em, ks.entry, T, ctas_per_sm);
+  if (CS > 1) {
+    const std::string gv = "__global__ void ";
+    sig.insert(sig.find(gv) + gv.size(), "__cluster_dims__(" + std::to_string(CS) + ", 1, 1) ");
+  }
   Code body;
   em.code = &body;
   const std::string& it = em.idx_t;
@@ -1042,8 +1057,13 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
     ks.cooperative = true;
   }
   body.line("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;");
-  body.line("const " + it + " kc = (" + it + ")blockIdx.x;");
-  body.line("const " + it + " v_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  if (CS > 1) {
+    body.line("const " + it + " kc = (" + it + ")blockIdx.x / " + std::to_string(CS) + ";");
+    body.line("const " + it + " v_begin = (" + it + ")(blockIdx.x % " + std::to_string(CS) + ") * " + fmt_i(RS) + ";");
+  } else {
+    body.line("const " + it + " kc = (" + it + ")blockIdx.x;");
+    body.line("const " + it + " v_begin = (" + it + ")blockIdx.y * " + fmt_i(RS) + ";");
+  }
   body.line("const " + it + " v_end = min((" + it + ")" + fmt_i(NV) + ", v_begin + " + fmt_i(RS) + ");");
   const Ix kix = em.uni("kc");
   // element (a, kc, b) of a node of `dims`; vector v = a * BV + b / V
@@ -1152,6 +1172,28 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
         body.line("if (threadIdx.x == 0) *(double*)((unsigned long long*)(ws + " + fmt_i(part_word[red[k]]) +
                   ") + (" + it + ")blockIdx.y * " + fmt_i(K) + " + kc) = " + acc[k] + ";");
     }
+    if (CS > 1) {
+      // cluster combine: every CTA folds the CS partials in rank order (identical
+      // totals); the second cluster barrier keeps every CTA's shared memory alive
+      // until its peers have read it
+      const std::string xp = em.fresh("xp"), xr = em.fresh("xr");
+      body.line("__shared__ double " + xp + "[" + std::to_string(red.size()) + "], " + xr + "[" +
+                std::to_string(red.size()) + "];");
+      for (size_t k = 0; k < red.size(); ++k)
+        body.line("if (threadIdx.x == 0) " + xp + "[" + std::to_string(k) + "] = " + acc[k] + ";");
+      body.line("sfx_cluster_sync();");
+      body.line("if (warp == 0) {");
+      for (size_t k = 0; k < red.size(); ++k) {
+        body.line("  { const double v = lane < " + std::to_string(CS) + " ? sfx_dsmem_ld(&" + xp + "[" +
+                  std::to_string(k) + "], (unsigned)lane) : 0.0;");
+        body.line("    double a = __shfl_sync(0xffffffffu, v, 0);");
+        body.line("    for (int r = 1; r < " + std::to_string(CS) + "; ++r) a += __shfl_sync(0xffffffffu, v, r);");
+        body.line("    if (lane == 0) " + xr + "[" + std::to_string(k) + "] = a; }");
+      }
+      body.line("}");
+      body.line("sfx_cluster_sync();");
+      for (size_t k = 0; k < red.size(); ++k) body.line(acc[k] + " = " + xr + "[" + std::to_string(k) + "];");
+    }
     if (S > 1) {
       body.line("sfx_grid_barrier(ws, " + std::to_string(lv) + "u);");
       // every CTA of the channel folds its S partials in stripe order (identical totals)
@@ -1218,7 +1260,7 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
       }
     });
   if (!chan_roots.empty()) {
-    body.line("if (blockIdx.y == 0 && threadIdx.x == 0) {");
+    body.line(std::string("if (") + (CS > 1 ? "v_begin == 0" : "blockIdx.y == 0") + " && threadIdx.x == 0) {");
     body.indent++;
     em.push();
     em.lane = 0;
@@ -1233,12 +1275,15 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
   if (S > 1) body.line("sfx_grid_exit(ws);");
   ks.code = assemble(sig, body);
   ks.block = T;
-  ks.grid_x = K;
+  ks.grid_x = K * CS;
   ks.grid_y = S;
+  ks.cluster = CS;
   ks.vector_width = V;
   ks.note = "split A=" + std::to_string(A) + " channels=" + std::to_string(K) + " B=" + std::to_string(B) +
             " stripes=" + std::to_string(S) + " levels=" + std::to_string(max_level) +
-            (S > 1 ? " (grid barriers, cooperative launch)" : " (one CTA per channel, no grid barrier)") +
+            (S > 1 ? " (grid barriers, cooperative launch)"
+             : CS > 1 ? " (a cluster of " + std::to_string(CS) + " CTAs per channel, DSMEM combine, no grid barrier)"
+                      : " (one CTA per channel, no grid barrier)") +
             (var2.empty() ? "" : ", " + std::to_string(var2.size()) + " second moment(s) in the first pass");
   return ks;
 }

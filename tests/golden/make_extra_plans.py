@@ -134,6 +134,8 @@ EXTRA = {
     "bn_nchw_16x8x64x64": bn_graph([16, 8, 64, 64], [0, 2, 3]),  # 16 stripes per channel: grid barrier
     "bn_nchw_4x160x7x7": bn_graph([4, 160, 7, 7], [0, 2, 3]),  # B = 49: scalar vectors
     "bn_nchw_8x32x14x14": bn_graph([8, 32, 14, 14], [0, 2, 3], with_stats=True),  # channel root
+    "bn_nchw_8x80x64x64": bn_graph([8, 80, 64, 64], [0, 2, 3], with_stats=True),  # clusters of 8 CTAs per channel
+    "bn_nchw_8x96x32x32": bn_graph([8, 96, 32, 32], [0, 2, 3]),  # clusters of 2
     # one rank"s shard of a 2-rank SyncBatchNorm over 4096 rows (global count)
     "bnsync_shard_2048x256": bn_graph([2048, 256], [0], count=4096),
     "bnmax_3000x37": {"instructions": [

@@ -545,11 +545,13 @@ def test_colbc_second_moment_special_values(ctx, name, two_pass, monkeypatch):
     assert np.isnan(y[:, 5:10]).all() and np.isfinite(y[:, 10:]).all()
 
 
-@pytest.mark.parametrize("name", ["bn_nchw_16x8x64x64", "bn_nchw_4x160x7x7", "bn_nchw_8x32x14x14"])
+@pytest.mark.parametrize("name", ["bn_nchw_16x8x64x64", "bn_nchw_4x160x7x7", "bn_nchw_8x32x14x14",
+                                  "bn_nchw_8x80x64x64", "bn_nchw_8x96x32x32"])
 @pytest.mark.parametrize("two_pass", ["0", "1"])
 def test_colbc_split_nchw(ctx, name, two_pass, monkeypatch):
     """Batch-norm over NCHW (channels between the reduced dims): the split
-    colbc template (one CTA per channel, or stripes + one grid barrier) with
+    colbc template (one CTA per channel, a cluster of 2 / 8 CTAs per channel
+    combining through DSMEM, or stripes + one grid barrier) with
     the variance folded in the mean's pass or as its own level, on a +2
     offset, a constant channel and non-finite channels (+inf, NaN, -inf at the
     channel's first element = the shift K).  (At +10 with 196 elements per

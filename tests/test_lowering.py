@@ -106,6 +106,12 @@ def test_colbc_is_cooperative_with_grid_barriers(monkeypatch):
     assert "1 second moment(s)" in note
     _, _, note = _note(os.path.join(EXTRA, "bn_nchw_4x160x7x7.json"))
     assert "stripes=1" in note and "no grid barrier" in note, note
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_8x80x64x64.json"), 1)
+    assert "a cluster of 8 CTAs per channel" in note, note
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_8x96x32x32.json"))
+    assert "a cluster of 2 CTAs per channel" in note, note
+    _, _, note = _note(os.path.join(EXTRA, "bn_nchw_8x96x32x32.json"), pipe_stages=1)  # clusters off (A/B)
+    assert "stripes=2" in note and "grid barriers" in note, note
     monkeypatch.setenv("SFX_COLBC_TWO_PASS", "1")
     _, _, note = _note(os.path.join(EXTRA, "bn_nchw_16x8x64x64.json"))
     assert "levels=2" in note and "second moment" not in note
