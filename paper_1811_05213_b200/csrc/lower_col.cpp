@@ -1013,13 +1013,13 @@ KernelSource lower_colbc_split(const Ctx& c, const SplitPlan& sp, const sfx_comp
   S = std::max<int64_t>(1, std::min<int64_t>(S, NV / (4 * T)));
   if (S > 1 && K * S > int64_t{kNumSMs} * ctas_per_sm) S = std::max<int64_t>(1, kNumSMs * ctas_per_sm / K);
   // a channel per CTA leaves SMs unevenly loaded when K is not a multiple of
-  // the SM count (256 channels on 148 SMs: 108 SMs carry two): from 74 channels
+  // the SM count (256 channels on 148 SMs: 108 SMs carry two): from 37 channels
   // up, a thread-block cluster of CS CTAs takes each channel instead (>= 4
   // clusters' worth of CTAs per SM), the CTAs combining their partials through
   // distributed shared memory — no grid barrier.  pipe_stages = 1: one CTA per
   // channel (A/B)
   int CS = 1;
-  if (K >= 74 && o.pipe_stages != 1 && o.rows_per_cta <= 0) {
+  if (K * 8 >= int64_t{kNumSMs} * 2 && o.pipe_stages != 1 && o.rows_per_cta <= 0) {
     S = 1;
     while (CS < 8 && K * CS < int64_t{kNumSMs} * 4 && NV / (CS * 2) >= 4 * T) CS *= 2;
   }
