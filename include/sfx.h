@@ -150,12 +150,13 @@ typedef struct sfx_graph_desc {
 
 /* Lowering options. */
 enum {
-  SFX_STRATEGY_AUTO = 0,    /* pick map/row/col template, else literal */
+  SFX_STRATEGY_AUTO = 0,    /* pick map/row/col/colbc template (or dot for fuse_dot groups), else literal */
   SFX_STRATEGY_LITERAL = 1, /* literal KernelProgram lowering (reference chunking and fold order) */
   SFX_STRATEGY_MAP = 2,
   SFX_STRATEGY_ROW = 3,
   SFX_STRATEGY_COL = 4,
-  SFX_STRATEGY_COLBC = 5    /* column reductions broadcast back (batch-norm): grid barriers, one launch */
+  SFX_STRATEGY_COLBC = 5    /* column reductions broadcast back (batch-norm): grid barriers, one launch; also the
+                               split layout [A | K | B] (batch-norm over NCHW): a cluster or CTA per channel */
 };
 typedef struct sfx_compile_opts {
   int32_t strategy;      /* SFX_STRATEGY_* ; forcing an inapplicable one fails with SFX_ERR_UNSUPPORTED */
@@ -186,7 +187,7 @@ typedef struct sfx_graph sfx_graph;
 
 /* Kernel facts for logging / measurement. */
 typedef struct sfx_kernel_info {
-  const char* strategy;      /* "map" | "row" | "col" | "literal" | "dot" */
+  const char* strategy;      /* "map" | "row" | "col" | "colbc" | "literal" | "dot" */
   const char* entry;         /* kernel symbol */
   int32_t n_inputs;
   int32_t n_outputs;
